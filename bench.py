@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark: particle-steps/s of the cuTAMP hot path (BASELINE.json metric) on 1..8 B200.
+
+One bench *step* = one optimisation round over one batch of synthetic particles, i.e. one pass of
+every SURVEY §8(a) row: K1 sampling (a2) -> `adam_steps` fused Eq. 4 Adam steps (a3-a10), with an
+Eq. 3 check + NCCL all-reduce of the satisfied counts every `check_every` steps (a11, a12) -> local
+best-k -> NCCL all-gather -> deterministic merge (a12).  value = particles x Adam steps of all ranks
+/ max-over-ranks device time of the timed steps.
+
+Usage:  python bench.py [--gpus N --steps K --warmup W] [--config 2] [--n PER_RANK] [--impl reference]
+        (N > 1: launched by torchrun, one process per GPU, NCCL over NVLink)
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from workloads import make_config, CONFIG_NAMES  # noqa: E402
+
+METRIC = "particle-steps/sec (cost+grad+update)"
+UNIT = "particle-steps/s"
+CONFIG_DESC = {
+    1: "pick-place skeleton, 7-DOF sphere arm, 1 table",
+    2: "obstruction stacking: move 2 obstructors, stack red on blue (3 pick-place)",
+    3: "Tetris-4 packing + min-object-distance goal cost",
+    4: "Tetris-6 packing with trajectory-knot collision costs",
+    5: "Tetris-4 packing skeleton (particle-count sweep)",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--n", type=int, default=None, help="particles per rank (default: the config's BASELINE size)")
+    p.add_argument("--adam-steps", type=int, default=100)
+    p.add_argument("--check-every", type=int, default=10)
+    p.add_argument("--k", type=int, default=16)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-ttfs", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)), "measured"
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------------------------------------
+# algorithmic work per particle-step: FP32-pipe instructions of the
+# minimal evaluation of each unit (FFMA = 1), independent of how the kernel maps or culls it.
+# ------------------------------------------------------------------------------------------------
+W_FK = 344          # 7 x (Rz apply 6 + sincos 2) + 8 x 3x4 compose 36
+W_SPH_XFORM = 9     # per robot sphere per conf
+W_SPH_BWD = 9       # wrench accumulation per robot sphere
+W_LINK_BWD = 8 * 6 + 7 * 15   # suffix sums + dq per conf
+W_PAIR_SB = 24      # sphere-OBB inactive test: R^T(w-c) 12, |p|-h 3, max 3, |q|^2 3, max 2, cmp 1
+W_PAIR_SS = 8       # sphere-sphere inactive test: diff 3, |d|^2 3, radius 1, cmp 1
+W_KIN = 90          # target compose 36, M 27, residuals ~27
+W_JL = 35
+W_PLACE = 100       # decode, support, containment per placed object
+W_GOAL_PAIR = 23
+W_SEG = 25
+W_ADAM = 12         # per coordinate
+
+
+def algorithmic_instr(w):
+    n_fk, S = w["n_fk"], w["n_robot_spheres"]
+    return (n_fk * (W_FK + S * (W_SPH_XFORM + W_SPH_BWD) + W_LINK_BWD + W_JL)
+            + W_PAIR_SB * w["pairs_sphere_obb"] + W_PAIR_SS * w["pairs_sphere_sphere"]
+            + W_KIN * w["n_kin"] + W_PLACE * w["n_place"] + W_GOAL_PAIR * w["n_goal_pairs"]
+            + W_SEG * w["n_traj_seg"] + W_ADAM * w["D"])
+
+
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        return world, rank, local, dist
+    return 1, 0, 0, None
+
+
+def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_rec=None):
+    """One bench step (see module docstring).  Returns the merged global best-k records."""
+    ctx.sample(seed)
+    for _ in range(args.adam_steps // args.check_every):
+        if events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ctx.optimize(args.check_every)
+            e1.record()
+            events.append((e0, e1))
+        else:
+            ctx.optimize(args.check_every)
+        if host_counts is not None and world == 1:
+            ctx.check(counts=host_counts)                 # D2H through the C ABI (host buffer)
+        else:
+            counts, _ = ctx.check()
+            if dist is not None:
+                dist.all_reduce(counts)                   # NCCL SUM of satisfied counts (C1)
+            if host_counts is not None:
+                host_counts.copy_(counts)                 # D2H
+    if host_rec is not None and world == 1:
+        ctx.best_k(args.k, out=host_rec)
+        return host_rec
+    rec = ctx.best_k(args.k)
+    if dist is not None:
+        gathered = [torch.empty_like(rec) for _ in range(world)]
+        dist.all_gather(gathered, rec)                    # C2
+        rec = torch.cat(gathered)
+    merged = ctx.merge_best_k(rec, args.k)                # K5
+    if host_rec is not None:
+        host_rec.copy_(merged)
+    return merged
+
+
+def max_over_ranks(v, dist):
+    if dist is None:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(args, spec, budget_s):
+    """The float64 oracle (as it stands) on the host cores: bounded sample of the same workload."""
+    from oracle import tamp_oracle as O
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    n = 256
+    csp = O.build_csp(spec)
+    x, g = O.initialize_particles(spec, csp, 1, np.arange(n))
+    st = O.new_state(x, g)
+    O.optimize(spec, csp, st, 1, 1.0 / n)               # warm-up
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        O.optimize(spec, csp, st, 1, 1.0 / n)
+        steps += 1
+        if time.perf_counter() - t0 >= budget_s and steps >= 2:
+            break
+    dt = time.perf_counter() - t0
+    torch.set_num_threads(1)
+    return {"value": n * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} particles x {steps} Adam steps of {CONFIG_NAMES[args.config]} "
+                      f"(float64 oracle, torch autograd, {cores} threads), {dt:.1f} s"}
+
+
+def bench_reference(args, world, rank, dist):
+    """--impl reference: the oracle timed on the host cores on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    from oracle import tamp_oracle as O
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    spec = make_config(args.config)
+    csp = O.build_csp(spec)
+    n, adam = 128, 4
+    x, g = O.initialize_particles(spec, csp, 7, np.arange(n))
+
+    def step(seed):
+        xs, gs = O.initialize_particles(spec, csp, seed, np.arange(n))
+        st = O.new_state(xs, gs)
+        O.optimize(spec, csp, st, adam, 1.0 / n)
+        cls, counts, J, soft, Jc = O.check(spec, csp, st)
+        O.best_k(cls, J, soft, np.arange(n), min(args.k, n))
+
+    for w in range(args.warmup):
+        step(100 + w)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        step(200 + s)
+    dt = time.perf_counter() - t0
+    value = n * adam * args.steps / dt
+    sample = f"{n} particles x {adam} Adam steps (+ sample, check, best-k) per step, float64 oracle, {cores} threads"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config{args.config}:{CONFIG_NAMES[args.config]}", "particles_per_step": n,
+                       "adam_steps_per_step": adam},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def ttfs(ctx, args, dist, world, seed, budget_steps=1000):
+    """Time-to-first-satisfying: wall time from sampling to the first all-reduced check with >= 1
+    satisfying particle (checks every `check_every` steps, budget 1000 steps)."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.sample(seed)
+    steps = 0
+    while steps < budget_steps:
+        ctx.optimize(args.check_every)
+        steps += args.check_every
+        counts, _ = ctx.check()
+        if dist is not None:
+            dist.all_reduce(counts)
+        if int(counts[-2].item()) > 0:
+            return {"s": time.perf_counter() - t0, "steps": steps, "satisfying": int(counts[-2].item())}
+    return {"s": None, "steps": steps, "satisfying": 0, "note": "not reached within budget"}
+
+
+def main():
+    args = parse()
+    world, rank, local, dist = dist_init(args)
+    if args.impl == "reference":
+        bench_reference(args, world, rank, dist)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    from paper_2411_11833_b200 import TampContext, kernel_launches
+    import paper_2411_11833_b200.build as bld
+    bld.build()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    torch.set_num_threads(1)
+    cfg = args.config
+    n = args.n or (make_config(cfg, n=1).n_particles if cfg != 5 else 1 << 20)
+    if cfg == 4 and args.n is None:
+        n = 131072 // 8                              # config 4: 128K particles over 8 GPUs (per-rank share)
+    spec = make_config(cfg, n=n)
+    n_global = n * world
+    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
+    for w in range(args.warmup):
+        run_round(ctx, 10_000 + w, args, dist, world)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    launches0 = kernel_launches()
+    opt_events, round_events = [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        for s in range(args.steps):
+            flush.zero_()                             # L2 flush between timed steps (not timed)
+            r0 = torch.cuda.Event(enable_timing=True)
+            r1 = torch.cuda.Event(enable_timing=True)
+            r0.record()
+            run_round(ctx, 20_000 + s, args, dist, world, events=opt_events)
+            r1.record()
+            round_events.append((r0, r1))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    launches = kernel_launches() - launches0
+    t_round = sum(a.elapsed_time(b) for a, b in round_events) / 1e3
+    t_round = max_over_ranks(t_round, dist)
+    opt_ms = [a.elapsed_time(b) for a, b in opt_events]
+    opt_avg = statistics.mean(opt_ms) / 1e3
+    opt_avg = max_over_ranks(opt_avg, dist)
+    ps = n_global * args.adam_steps * args.steps
+    value = ps / t_round
+    clocks = clk.summary()
+
+    # roofline of the dominant kernel (k_particle, fused Adam steps): ALU/FP32-pipe bound
+    pk, src = peaks()
+    w = dict(ctx.work)
+    instr = algorithmic_instr(w)
+    achieved = instr * n * args.check_every / opt_avg / 1e12          # T instr/s per GPU
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = nsm * 128 * sm_max * 1e6 / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinstr/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "k_particle<MODE_OPT>",
+            "note": f"FP32-pipe instructions (FFMA=1) of the minimal per-unit evaluation, {instr} per particle-step; "
+                    f"peak = {nsm} SM x 128 lanes x {sm_max:.0f} MHz ({src} sm_max_mhz)"}
+    if clocks:
+        roof["frac_at_measured_clock"] = achieved / (nsm * 128 * clocks["sm_mhz"] * 1e6 / 1e12)
+
+    # end-to-end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_counts = torch.zeros(ctx.n_hard + 2, dtype=torch.int32).pin_memory()
+        host_rec = torch.zeros(args.k, ctx.D + 4, dtype=torch.float32).pin_memory()
+        for w_ in range(2):
+            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev)
+            run_round(c2, 30_000 + w_, args, dist, world, host_counts=host_counts, host_rec=host_rec)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(3, min(args.steps, 10))
+        for s in range(e2e_steps):
+            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev)  # host descriptor in
+            run_round(c2, 40_000 + s, args, dist, world, host_counts=host_counts, host_rec=host_rec)
+        torch.cuda.synchronize()
+        te = max_over_ranks(time.perf_counter() - t0, dist)
+        import ctypes
+        from paper_2411_11833_b200.tamp import ProblemDesc
+        h2d = ctypes.sizeof(ProblemDesc) + 3 * ctx.D * 4
+        d2h = (args.adam_steps // args.check_every) * (ctx.n_hard + 2) * 4 + args.k * (ctx.D + 4) * 4
+        e2e = {"value": n_global * args.adam_steps * e2e_steps / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    tt = None if args.no_ttfs else ttfs(ctx, args, dist, world, seed=1000 * cfg)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, make_config(cfg, n=256), args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_round / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"config{cfg}:{CONFIG_NAMES[cfg]}", "description": CONFIG_DESC[cfg],
+                           "particles_per_gpu": n, "particles_global": n_global, "D": ctx.D,
+                           "hard_terms": ctx.n_hard, "adam_steps_per_step": args.adam_steps,
+                           "check_every": args.check_every, "best_k": args.k, "l2": "flushed between steps",
+                           "parallelism": f"dp{world}"},
+                "kernel_ms_per_launch": opt_avg * 1e3, "kernel_steps_per_launch": args.check_every,
+                "kernel_particle_steps_per_s": n_global * args.check_every / opt_avg,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks, "ttfs": tt}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

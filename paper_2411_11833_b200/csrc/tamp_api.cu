@@ -1,0 +1,825 @@
+// tamp_api.cu -- host side of libtamp: descriptor validation, skeleton -> CSP compiler, workspace,
+// and the extern "C" entry points declared in include/tamp.h.
+//
+// The compiler follows Listing 1 in deferred-motion mode plus knots for
+// motions that carry a trajectory variable, simulating the symbolic state along the
+// skeleton (which object is where / held) to decide which collision pairs each term checks
+// (SURVEY §8(c) L3).  Canonical term order (shared contract with the oracle):
+//   MoveFree/MoveHold with K knots: per knot  JL, CF
+//   Pick(o, g, p, q):                          JL(q), CF(q) [o excluded], KP(q), KR(q)
+//   Place(o, g, p, s, q):                      JL(q), CF(q) [held o excluded], KP(q), KR(q), SS(p), SC(p), CP(p)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tamp.h"
+#include "tamp_program.h"
+
+namespace tamp {
+cudaError_t launch_particle(int mode, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st);
+cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
+                          cudaStream_t st);
+cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
+                        cudaStream_t st, unsigned long long** kres, int32_t** pres);
+cudaError_t launch_make_keys(const uint8_t* cls, const float* cost, int64_t n, int64_t gofs, unsigned long long* keys,
+                             int32_t* pay, cudaStream_t st);
+cudaError_t launch_record_keys(const float* rec, int32_t n, int32_t width, unsigned long long* keys, int32_t* pay,
+                               cudaStream_t st);
+cudaError_t launch_gather_particles(const int32_t* pay, const unsigned long long* keys, int k, const float* x,
+                                    const float* cost, int D, int64_t gofs, float* rec, cudaStream_t st);
+cudaError_t launch_gather_records(const int32_t* pay, int k, const float* rin, int width, float* rout, cudaStream_t st);
+uint64_t launch_count();
+}  // namespace tamp
+
+using namespace tamp;
+
+static thread_local std::string g_err;
+
+static tamp_status fail(tamp_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+static tamp_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(TAMP_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(call, where)                          \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+struct tamp_ctx {
+    int device = 0;
+    int64_t n = 0, gofs = 0, nglob = 0;
+    KProgram P;
+    KSampleProgram SP;
+    char* base = nullptr;
+    size_t ws_bytes = 0;
+    // workspace offsets
+    size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, total;
+    int64_t n_keys = 0;
+    // shared-memory layout of the particle kernel (floats per particle)
+    int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
+    size_t smem = 0;
+    int32_t t = 0;
+    bool ready = false;
+    int32_t term_kind[TAMP_MAX_TERMS];
+    std::vector<float> coords;   // lr | lo | hi, uploaded at init
+    int64_t pairs_sb = 0, pairs_ss = 0;
+    int32_t n_robot_spheres = 0;
+
+    template <class T>
+    T* at(size_t off) const { return reinterpret_cast<T*>(base + off); }
+};
+
+// ------------------------------------------------------------------------------------------------
+// small double-precision transform helpers (host, compile time only)
+// ------------------------------------------------------------------------------------------------
+struct H34 {
+    double r[9];
+    double t[3];
+};
+static H34 h_ident() { H34 a{}; a.r[0] = a.r[4] = a.r[8] = 1.0; return a; }
+static H34 h_mul(const H34& a, const H34& b) {
+    H34 c{};
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j)
+            c.r[3 * i + j] = a.r[3 * i] * b.r[j] + a.r[3 * i + 1] * b.r[3 + j] + a.r[3 * i + 2] * b.r[6 + j];
+        c.t[i] = a.r[3 * i] * b.t[0] + a.r[3 * i + 1] * b.t[1] + a.r[3 * i + 2] * b.t[2] + a.t[i];
+    }
+    return c;
+}
+static H34 h_rx(double a) { H34 m = h_ident(); m.r[4] = cos(a); m.r[5] = -sin(a); m.r[7] = sin(a); m.r[8] = cos(a); return m; }
+static H34 h_rz(double a) { H34 m = h_ident(); m.r[0] = cos(a); m.r[1] = -sin(a); m.r[3] = sin(a); m.r[4] = cos(a); return m; }
+static H34 h_tr(double x, double y, double z) { H34 m = h_ident(); m.t[0] = x; m.t[1] = y; m.t[2] = z; return m; }
+static void h_store(const H34& a, float* o) {
+    for (int i = 0; i < 3; ++i) {
+        o[4 * i] = (float)a.r[3 * i]; o[4 * i + 1] = (float)a.r[3 * i + 1];
+        o[4 * i + 2] = (float)a.r[3 * i + 2]; o[4 * i + 3] = (float)a.t[i];
+    }
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// ------------------------------------------------------------------------------------------------
+// compiler
+// ------------------------------------------------------------------------------------------------
+struct Compiled {
+    KProgram P;
+    KSampleProgram SP;
+    std::vector<float> lr, lo, hi;
+    int32_t term_kind[TAMP_MAX_TERMS];
+    int64_t pairs_sb = 0, pairs_ss = 0;
+};
+
+// collision pairs evaluated per particle-step (all pairs; the kernel's culling is an implementation detail)
+static void count_pairs(const tamp_problem_desc& d, Compiled& C) {
+    const KProgram& P = C.P;
+    auto popc = [](uint32_t m) { int c = 0; while (m) { c += m & 1; m >>= 1; } return c; };
+    int64_t sb = 0, ss = 0;
+    for (int f = 0; f < P.n_fk; ++f) {
+        const KFk& K = P.fk[f];
+        if (K.term_cf < 0) continue;
+        int part_sph = 0;
+        for (int i = 0; i < K.part_count; ++i) part_sph += P.osph_n[P.inst[P.partners[K.part_begin + i]].obj];
+        const int nb = popc(K.obb_mask);
+        sb += (int64_t)d.robot.n_spheres * nb;
+        ss += (int64_t)d.robot.n_spheres * part_sph;
+        if (K.held_grasp >= 0) { sb += (int64_t)P.osph_n[K.held_obj] * nb; ss += (int64_t)P.osph_n[K.held_obj] * part_sph; }
+    }
+    for (int q = 0; q < P.n_place; ++q) {
+        const KPlace& Q = P.place[q];
+        int part_sph = 0;
+        for (int i = 0; i < Q.part_count; ++i) part_sph += P.osph_n[P.inst[P.partners[Q.part_begin + i]].obj];
+        const int no = P.osph_n[P.inst[Q.inst].obj];
+        sb += (int64_t)no * popc(Q.obb_mask);
+        ss += (int64_t)no * part_sph;
+    }
+    C.pairs_sb = sb;
+    C.pairs_ss = ss;
+}
+
+#define REQUIRE(cond, st, msg)                    \
+    do {                                          \
+        if (!(cond)) return fail(st, msg);        \
+    } while (0)
+
+static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compiled& C) {
+    std::memset(&C.P, 0, sizeof(C.P));
+    std::memset(&C.SP, 0, sizeof(C.SP));
+    KProgram& P = C.P;
+    KSampleProgram& SP = C.SP;
+    REQUIRE(d.abi_version == TAMP_ABI_VERSION, TAMP_E_INVALID, "abi_version mismatch");
+    const tamp_robot_desc& R = d.robot;
+    REQUIRE(d.n_obb >= 0 && d.n_obb <= TAMP_MAX_OBB, TAMP_E_UNSUPPORTED, "n_obb out of range");
+    REQUIRE(d.n_objects >= 0 && d.n_objects <= TAMP_MAX_OBJECTS, TAMP_E_UNSUPPORTED, "n_objects out of range");
+    REQUIRE(d.n_surfaces >= 0 && d.n_surfaces <= TAMP_MAX_SURFACES, TAMP_E_UNSUPPORTED, "n_surfaces out of range");
+    REQUIRE(d.n_vars >= 0 && d.n_vars <= TAMP_MAX_VARS, TAMP_E_UNSUPPORTED, "n_vars out of range");
+    REQUIRE(d.n_actions >= 0 && d.n_actions <= TAMP_MAX_ACTIONS, TAMP_E_UNSUPPORTED, "n_actions out of range");
+    REQUIRE(d.n_goal >= 0 && d.n_goal <= TAMP_MAX_GOAL, TAMP_E_UNSUPPORTED, "n_goal out of range");
+    REQUIRE(R.n_spheres >= 0 && R.n_spheres <= TAMP_MAX_ROBOT_SPHERES, TAMP_E_UNSUPPORTED, "robot n_spheres out of range");
+    for (int j = 0; j < TAMP_NJ; ++j)
+        REQUIRE(R.joint_lo[j] < R.joint_hi[j], TAMP_E_INVALID, "joint_lo must be < joint_hi (S:27)");
+    for (int k = 0; k < TAMP_N_TERM_KINDS; ++k) {
+        REQUIRE(d.lam[k] > 0.f && std::isfinite(d.lam[k]), TAMP_E_INVALID, "lambda must be > 0 (S:131)");
+        REQUIRE(d.eps[k] >= 0.f && std::isfinite(d.eps[k]), TAMP_E_INVALID, "eps must be >= 0 (S:131)");
+    }
+    REQUIRE(d.eta >= 0.f, TAMP_E_INVALID, "eta must be >= 0");
+    REQUIRE(d.beta1 >= 0.f && d.beta1 < 1.f && d.beta2 >= 0.f && d.beta2 < 1.f && d.adam_eps > 0.f, TAMP_E_INVALID,
+            "Adam betas must be in [0,1), eps > 0");
+    REQUIRE(d.lr_conf >= 0 && d.lr_pos >= 0 && d.lr_yaw >= 0 && d.lr_knot >= 0, TAMP_E_INVALID, "lr must be >= 0");
+    REQUIRE(d.lam_goal >= 0 && d.lam_traj >= 0, TAMP_E_INVALID, "soft weights must be >= 0");
+
+    // robot: fixed transforms (base folded into F_1) and per-link spheres
+    {
+        H34 T = h_mul(h_tr(R.base[0], R.base[1], R.base[2]), h_rz(R.base[3]));
+        for (int j = 0; j < TAMP_NJ; ++j) {
+            const double a = R.dh[j][0], dd = R.dh[j][1], al = R.dh[j][2];
+            H34 F = h_mul(h_rx(al), h_tr(a, 0.0, dd));
+            if (j == 0) F = h_mul(T, F);
+            h_store(F, P.F[j]);
+            P.jlo[j] = R.joint_lo[j];
+            P.jhi[j] = R.joint_hi[j];
+            SP.jlo[j] = R.joint_lo[j];
+            SP.jhi[j] = R.joint_hi[j];
+        }
+        H34 tool = h_mul(h_mul(h_tr(0, 0, R.flange_d), h_rz(R.tcp_yaw)), h_tr(0, 0, R.tcp_d));
+        h_store(tool, P.F[kGroup - 1]);
+        for (int s = 0; s < R.n_spheres; ++s) {
+            const int l = R.sphere_link[s];
+            REQUIRE(l >= 1 && l <= 8, TAMP_E_INVALID, "sphere_link must be in 1..8");
+            REQUIRE(R.sphere[s][3] > 0.f, TAMP_E_INVALID, "robot sphere radius must be > 0 (S:36)");
+            const int lane = l - 1;
+            REQUIRE(P.rsph_n[lane] < TAMP_MAX_SPHERES_PER_LINK, TAMP_E_UNSUPPORTED, "more than 4 spheres on a link");
+            for (int c = 0; c < 4; ++c) P.rsph[lane][P.rsph_n[lane]][c] = R.sphere[s][c];
+            P.rsph_n[lane]++;
+        }
+    }
+    // world
+    P.n_obb = d.n_obb;
+    REQUIRE(d.n_obb <= 16, TAMP_E_UNSUPPORTED, "n_obb > 16");
+    for (int b = 0; b < d.n_obb; ++b) {
+        const tamp_obb_desc& o = d.obb[b];
+        for (int k = 0; k < 3; ++k) REQUIRE(o.half[k] > 0.f, TAMP_E_INVALID, "OBB half extents must be > 0 (S:32)");
+        const double c = cos((double)o.yaw), s = sin((double)o.yaw);
+        KObb& B = P.obb[b];
+        const double Rm[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
+        for (int k = 0; k < 9; ++k) B.R[k] = (float)Rm[k];
+        for (int k = 0; k < 3; ++k) { B.c[k] = o.center[k]; B.h[k] = o.half[k]; }
+    }
+    const uint16_t all_obb = (uint16_t)((1u << d.n_obb) - 1u);
+    for (int o = 0; o < d.n_objects; ++o) {
+        const tamp_object_desc& ob = d.object[o];
+        REQUIRE(ob.n_spheres >= 1 && ob.n_spheres <= TAMP_MAX_OBJ_SPHERES, TAMP_E_UNSUPPORTED,
+                "object n_spheres must be in 1..8");
+        P.osph_n[o] = ob.n_spheres;
+        for (int k = 0; k < ob.n_spheres; ++k) {
+            REQUIRE(ob.sphere[k][3] > 0.f, TAMP_E_INVALID, "object sphere radius must be > 0 (S:36)");
+            for (int c = 0; c < 4; ++c) P.osph[o][k][c] = ob.sphere[k][c];
+        }
+    }
+    for (int s = 0; s < d.n_surfaces; ++s) {
+        const tamp_surface_desc& S = d.surface[s];
+        REQUIRE(S.lo[0] <= S.hi[0] && S.lo[1] <= S.hi[1], TAMP_E_INVALID, "surface lo must be <= hi");
+        REQUIRE(S.support_obb < d.n_obb && S.support_obj < d.n_objects, TAMP_E_INVALID, "surface support out of range");
+        for (int k = 0; k < 4; ++k) P.surf[s].frame[k] = S.frame[k];
+        for (int k = 0; k < 2; ++k) { P.surf[s].lo[k] = S.lo[k]; P.surf[s].hi[k] = S.hi[k]; }
+    }
+
+    // particle layout (free variables in declaration order; grasps frozen in their own array)
+    std::vector<int> xoff(d.n_vars, -1), gslot(d.n_vars, -1), cconf(d.n_vars, -1), inst_of(d.n_vars, -1);
+    int D = 0, G = 0, n_const = 0;
+    for (int v = 0; v < d.n_vars; ++v) {
+        const tamp_var_desc& V = d.var[v];
+        REQUIRE(V.kind >= 0 && V.kind <= 3, TAMP_E_INVALID, "bad variable kind");
+        if (V.kind == TAMP_VAR_GRASP) {
+            REQUIRE(V.obj >= 0 && V.obj < d.n_objects, TAMP_E_INVALID, "grasp variable without object");
+            REQUIRE(G < TAMP_MAX_GRASPS, TAMP_E_UNSUPPORTED, "too many grasps");
+            gslot[v] = G++;
+            continue;
+        }
+        if (V.is_const) {
+            if (V.kind == TAMP_VAR_CONF) {
+                REQUIRE(n_const < kMaxConstConf, TAMP_E_UNSUPPORTED, "too many constant confs");
+                for (int j = 0; j < 7; ++j) { P.const_conf[n_const][j] = V.value[j]; SP.const_conf[n_const][j] = V.value[j]; }
+                cconf[v] = n_const++;
+            }
+            REQUIRE(V.kind != TAMP_VAR_TRAJ, TAMP_E_UNSUPPORTED, "constant trajectories unsupported");
+            continue;
+        }
+        xoff[v] = D;
+        if (V.kind == TAMP_VAR_CONF) {
+            for (int j = 0; j < 7; ++j) { C.lr.push_back(d.lr_conf); C.lo.push_back(R.joint_lo[j]); C.hi.push_back(R.joint_hi[j]); }
+            D += 7;
+        } else if (V.kind == TAMP_VAR_PLACEMENT) {
+            REQUIRE(V.obj >= 0 && V.obj < d.n_objects, TAMP_E_INVALID, "placement variable without object");
+            REQUIRE(V.surface >= 0 && V.surface < d.n_surfaces, TAMP_E_INVALID, "placement variable without surface");
+            for (int j = 0; j < 4; ++j) {
+                REQUIRE(V.lo[j] <= V.hi[j], TAMP_E_INVALID, "placement bounds lo must be <= hi");
+                C.lr.push_back(j < 3 ? d.lr_pos : d.lr_yaw); C.lo.push_back(V.lo[j]); C.hi.push_back(V.hi[j]);
+            }
+            D += 4;
+        } else {   // TRAJ
+            REQUIRE(V.n_knots >= 0 && V.n_knots <= TAMP_MAX_KNOTS, TAMP_E_UNSUPPORTED, "n_knots out of range");
+            for (int k = 0; k < V.n_knots; ++k)
+                for (int j = 0; j < 7; ++j) { C.lr.push_back(d.lr_knot); C.lo.push_back(R.joint_lo[j]); C.hi.push_back(R.joint_hi[j]); }
+            D += 7 * V.n_knots;
+        }
+        REQUIRE(D <= TAMP_MAX_D, TAMP_E_UNSUPPORTED, "D exceeds TAMP_MAX_D");
+    }
+    P.D = SP.D = D;
+    P.n_grasp = SP.n_grasp = G;
+
+    // object instances: every placement variable (constant initial poses and Place targets)
+    int n_inst = 0;
+    std::vector<int> init_inst(d.n_objects, -1);
+    for (int v = 0; v < d.n_vars; ++v) {
+        const tamp_var_desc& V = d.var[v];
+        if (V.kind != TAMP_VAR_PLACEMENT) continue;
+        REQUIRE(V.obj >= 0 && V.obj < d.n_objects, TAMP_E_INVALID, "placement variable without object");
+        REQUIRE(n_inst < kMaxInst, TAMP_E_UNSUPPORTED, "too many object instances");
+        KInst& I = P.inst[n_inst];
+        I.obj = (int16_t)V.obj;
+        I.xoff = (int16_t)(V.is_const ? -1 : xoff[v]);
+        for (int k = 0; k < 4; ++k) I.pose[k] = V.is_const ? V.value[k] : 0.f;
+        if (V.is_const && init_inst[V.obj] < 0) init_inst[V.obj] = n_inst;
+        inst_of[v] = n_inst++;
+    }
+    P.n_inst = n_inst;
+    for (int o = 0; o < d.n_objects; ++o)
+        REQUIRE(init_inst[o] >= 0, TAMP_E_INVALID, "every object needs a constant initial placement variable");
+
+    // symbolic simulation along the skeleton
+    std::vector<int> pose(init_inst);     // object -> instance, -1 = held
+    int held = -1;
+    int n_terms = 0, n_fk = 0, n_place = 0, n_traj = 0, n_part = 0;
+    auto add_term = [&](int kind) -> int16_t {
+        if (n_terms >= TAMP_MAX_TERMS) return -1;
+        P.term_lam[n_terms] = d.lam[kind];
+        P.term_eps[n_terms] = d.eps[kind];
+        C.term_kind[n_terms] = kind;
+        return (int16_t)n_terms++;
+    };
+    auto add_partners = [&](int skip_a, int skip_b, int16_t& begin, int16_t& count) -> bool {
+        begin = (int16_t)n_part;
+        count = 0;
+        for (int o = 0; o < d.n_objects; ++o) {
+            if (pose[o] < 0 || o == skip_a || o == skip_b) continue;
+            if (n_part >= kMaxPartners) return false;
+            P.partners[n_part++] = (int16_t)pose[o];
+            count++;
+        }
+        return true;
+    };
+    auto conf_ok = [&](int v) { return v >= 0 && v < d.n_vars && d.var[v].kind == TAMP_VAR_CONF; };
+    for (int ai = 0; ai < d.n_actions; ++ai) {
+        const tamp_action_desc& a = d.action[ai];
+        if (a.kind == TAMP_MOVE_FREE || a.kind == TAMP_MOVE_HOLD) {
+            REQUIRE(conf_ok(a.q1) && conf_ok(a.q2), TAMP_E_INVALID, "motion endpoints must be conf variables");
+            if (a.kind == TAMP_MOVE_HOLD) REQUIRE(held == a.obj && a.obj >= 0, TAMP_E_INVALID, "MoveHold: object not held");
+            if (a.traj < 0) continue;
+            REQUIRE(a.traj < d.n_vars && d.var[a.traj].kind == TAMP_VAR_TRAJ && !d.var[a.traj].is_const, TAMP_E_INVALID,
+                    "motion traj must be a free traj variable");
+            const int K = d.var[a.traj].n_knots;
+            if (K == 0) continue;
+            const int hg = a.kind == TAMP_MOVE_HOLD ? gslot[a.grasp] : -1;
+            if (a.kind == TAMP_MOVE_HOLD)
+                REQUIRE(a.grasp >= 0 && a.grasp < d.n_vars && gslot[a.grasp] >= 0, TAMP_E_INVALID, "MoveHold grasp");
+            for (int j = 0; j < K; ++j) {
+                REQUIRE(n_fk < TAMP_MAX_FK, TAMP_E_UNSUPPORTED, "too many robot configurations (TAMP_MAX_FK)");
+                KFk& F = P.fk[n_fk++];
+                F.xoff = (int16_t)(xoff[a.traj] + 7 * j);
+                F.term_jl = add_term(TAMP_TERM_JL);
+                F.term_cf = add_term(TAMP_TERM_CF);
+                F.term_kp = F.term_kr = -1;
+                F.kin_inst = F.kin_grasp = -1;
+                F.held_grasp = (int16_t)hg;
+                F.held_obj = (int16_t)(hg >= 0 ? a.obj : -1);
+                F.obb_mask = all_obb;
+                REQUIRE(add_partners(-1, -1, F.part_begin, F.part_count), TAMP_E_UNSUPPORTED, "too many partners");
+            }
+            REQUIRE(n_traj < kMaxTraj, TAMP_E_UNSUPPORTED, "too many trajectories");
+            KTraj& Tj = P.traj[n_traj++];
+            Tj.q1_xoff = (int16_t)xoff[a.q1]; Tj.q1_const = (int16_t)cconf[a.q1];
+            Tj.q2_xoff = (int16_t)xoff[a.q2]; Tj.q2_const = (int16_t)cconf[a.q2];
+            Tj.knot_xoff = (int16_t)xoff[a.traj]; Tj.n_knots = (int16_t)K;
+        } else if (a.kind == TAMP_PICK || a.kind == TAMP_PLACE) {
+            REQUIRE(a.obj >= 0 && a.obj < d.n_objects, TAMP_E_INVALID, "pick/place object out of range");
+            REQUIRE(conf_ok(a.q1) && !d.var[a.q1].is_const, TAMP_E_UNSUPPORTED, "pick/place conf must be a free conf");
+            REQUIRE(a.grasp >= 0 && a.grasp < d.n_vars && gslot[a.grasp] >= 0 && d.var[a.grasp].obj == a.obj,
+                    TAMP_E_INVALID, "pick/place grasp must be a grasp variable of the object");
+            REQUIRE(a.placement >= 0 && a.placement < d.n_vars && inst_of[a.placement] >= 0 &&
+                    d.var[a.placement].obj == a.obj, TAMP_E_INVALID, "pick/place placement must belong to the object");
+            if (a.kind == TAMP_PICK) {
+                REQUIRE(held < 0, TAMP_E_INVALID, "Pick: hand not empty");
+                REQUIRE(pose[a.obj] == inst_of[a.placement], TAMP_E_INVALID, "Pick: object is not at that placement");
+            } else {
+                REQUIRE(held == a.obj, TAMP_E_INVALID, "Place: object not held");
+                REQUIRE(!d.var[a.placement].is_const, TAMP_E_UNSUPPORTED, "Place: placement must be free");
+                REQUIRE(a.surface >= 0 && a.surface < d.n_surfaces, TAMP_E_INVALID, "Place: surface out of range");
+            }
+            REQUIRE(n_fk < TAMP_MAX_FK, TAMP_E_UNSUPPORTED, "too many robot configurations (TAMP_MAX_FK)");
+            KFk& F = P.fk[n_fk++];
+            F.xoff = (int16_t)xoff[a.q1];
+            F.term_jl = add_term(TAMP_TERM_JL);
+            F.term_cf = add_term(TAMP_TERM_CF);
+            F.term_kp = add_term(TAMP_TERM_KP);
+            F.term_kr = add_term(TAMP_TERM_KR);
+            F.kin_inst = (int16_t)inst_of[a.placement];
+            F.kin_grasp = (int16_t)gslot[a.grasp];
+            F.held_grasp = F.held_obj = -1;
+            F.obb_mask = all_obb;
+            REQUIRE(add_partners(a.obj, -1, F.part_begin, F.part_count), TAMP_E_UNSUPPORTED, "too many partners");
+            if (a.kind == TAMP_PICK) {
+                held = a.obj;
+                pose[a.obj] = -1;
+            } else {
+                const tamp_surface_desc& S = d.surface[a.surface];
+                REQUIRE(n_place < kMaxPlace, TAMP_E_UNSUPPORTED, "too many Place actions");
+                KPlace& Q = P.place[n_place++];
+                Q.inst = (int16_t)inst_of[a.placement];
+                Q.term_ss = add_term(TAMP_TERM_SS);
+                Q.term_sc = add_term(TAMP_TERM_SC);
+                Q.term_cp = add_term(TAMP_TERM_CP);
+                Q.surface = (int16_t)a.surface;
+                Q.obb_mask = (uint16_t)(all_obb & ~(S.support_obb >= 0 ? (1u << S.support_obb) : 0u));
+                REQUIRE(add_partners(a.obj, S.support_obj, Q.part_begin, Q.part_count), TAMP_E_UNSUPPORTED,
+                        "too many partners");
+                if (S.support_obj >= 0)
+                    REQUIRE(pose[S.support_obj] >= 0 && P.inst[pose[S.support_obj]].xoff < 0, TAMP_E_UNSUPPORTED,
+                            "stacking on a moved object is not supported");
+                pose[a.obj] = inst_of[a.placement];
+                held = -1;
+            }
+        } else {
+            return fail(TAMP_E_INVALID, "bad action kind");
+        }
+        REQUIRE(n_terms < TAMP_MAX_TERMS, TAMP_E_UNSUPPORTED, "too many hard terms (TAMP_MAX_TERMS)");
+    }
+    P.n_terms = n_terms;
+    P.n_fk = n_fk;
+    P.n_place = n_place;
+    P.n_traj = n_traj;
+    P.n_goal = d.n_goal;
+    for (int k = 0; k < d.n_goal; ++k) {
+        const int o = d.goal_obj[k];
+        REQUIRE(o >= 0 && o < d.n_objects && pose[o] >= 0, TAMP_E_INVALID, "goal object must be placed at the end");
+        P.goal_inst[k] = (int16_t)pose[o];
+    }
+    P.grad_scale = d.grad_scale > 0.f ? d.grad_scale : (float)(1.0 / (double)n_global);
+    P.eta = d.eta;
+    P.beta1 = d.beta1;
+    P.beta2 = d.beta2;
+    P.adam_eps = d.adam_eps;
+    P.lam_goal = d.lam_goal;
+    P.lam_traj = d.lam_traj;
+
+    // sampler program (DAG order: grasps, placements, confs in declaration order; knots afterwards)
+    int ns = 0;
+    for (int v = 0; v < d.n_vars; ++v) {
+        const tamp_var_desc& V = d.var[v];
+        if (V.is_const) continue;
+        KSVar& S = SP.v[ns];
+        std::memset(&S, 0, sizeof(S));
+        S.var_id = (int16_t)v;
+        S.xoff = (int16_t)xoff[v];
+        S.slot = (int16_t)gslot[v];
+        if (V.kind == TAMP_VAR_GRASP) {
+            S.kind = KS_GRASP;
+            S.a[0] = d.object[V.obj].grasp_xy;
+            S.a[1] = d.object[V.obj].grasp_z;
+        } else if (V.kind == TAMP_VAR_PLACEMENT) {
+            const tamp_surface_desc& Sf = d.surface[V.surface];
+            S.kind = KS_PLACEMENT;
+            S.a[0] = Sf.lo[0]; S.a[1] = Sf.lo[1]; S.a[2] = Sf.hi[0]; S.a[3] = Sf.hi[1];
+            S.a[4] = d.object[V.obj].footprint;
+            S.a[5] = Sf.frame[0]; S.a[6] = Sf.frame[1]; S.a[7] = Sf.frame[2]; S.a[8] = Sf.frame[3];
+        } else if (V.kind == TAMP_VAR_CONF) {
+            S.kind = KS_CONF;
+        } else {
+            S.kind = KS_TRAJ;
+            S.n_knots = (int16_t)V.n_knots;
+            int found = -1;
+            for (int ai = 0; ai < d.n_actions; ++ai)
+                if ((d.action[ai].kind == TAMP_MOVE_FREE || d.action[ai].kind == TAMP_MOVE_HOLD) && d.action[ai].traj == v)
+                    found = ai;
+            REQUIRE(found >= 0 || V.n_knots == 0, TAMP_E_INVALID, "trajectory variable not used by a motion");
+            if (found >= 0) {
+                const tamp_action_desc& a = d.action[found];
+                S.q1_xoff = (int16_t)xoff[a.q1]; S.q1_const = (int16_t)cconf[a.q1];
+                S.q2_xoff = (int16_t)xoff[a.q2]; S.q2_const = (int16_t)cconf[a.q2];
+            }
+        }
+        ns++;
+    }
+    SP.n_vars = ns;
+    count_pairs(d, C);
+    return TAMP_OK;
+}
+
+// shared-memory layout of the particle kernel
+static void smem_layout(tamp_ctx* c) {
+    auto r4 = [](int v) { return (v + 3) & ~3; };
+    const KProgram& P = c->P;
+    int off = 0;
+    off += r4(P.D);
+    c->off_g = off;
+    off += r4(P.D);
+    c->off_ipose = off;
+    off += 16 * P.n_inst;
+    c->off_isph = off;
+    off += 4 * TAMP_MAX_OBJ_SPHERES * P.n_inst;
+    c->off_iwr = off;
+    off += 8 * P.n_inst;
+    c->off_gT = off;
+    off += 16 * P.n_grasp;
+    c->off_gTi = off;
+    off += 16 * P.n_grasp;
+    // stride = 8 (mod 32) floats so the four particles of a warp hit distinct banks on broadcasts
+    int stride = ((off + 31) / 32) * 32 + 8;
+    c->stride = stride;
+    c->smem = (size_t)16 * stride * sizeof(float);   // 16 particles per 128-thread block
+}
+
+static void ws_layout(tamp_ctx* c) {
+    const int64_t n = c->n;
+    const int D = c->P.D, G = c->P.n_grasp;
+    c->n_keys = n > 65536 ? n : 65536;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+    c->o_x = take((size_t)n * D * 4);
+    c->o_m = take((size_t)n * D * 4);
+    c->o_v = take((size_t)n * D * 4);
+    c->o_grasp = take((size_t)n * G * 12 * 4);
+    c->o_inv = take((size_t)n);
+    c->o_cls = take((size_t)n);
+    c->o_cost = take((size_t)n * 4);
+    c->o_ka = take((size_t)c->n_keys * 8);
+    c->o_kb = take((size_t)c->n_keys * 8);
+    c->o_pa = take((size_t)c->n_keys * 4);
+    c->o_pb = take((size_t)c->n_keys * 4);
+    c->o_coords = take((size_t)3 * (D > 0 ? D : 1) * 4);
+    c->o_counts = take((size_t)(TAMP_MAX_TERMS + 2) * 4);
+    c->o_stage = take((size_t)1024 * (D + 4) * 4);
+    c->total = o;
+}
+
+static bool is_host_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+static KArgs base_args(tamp_ctx* c) {
+    KArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.x = c->at<float>(c->o_x);
+    A.m = c->at<float>(c->o_m);
+    A.v = c->at<float>(c->o_v);
+    A.grasp = c->at<float>(c->o_grasp);
+    A.invalid = c->at<uint8_t>(c->o_inv);
+    const float* coords = c->at<float>(c->o_coords);
+    A.lr = coords;
+    A.lo = coords + c->P.D;
+    A.hi = coords + 2 * c->P.D;
+    A.n = c->n;
+    A.gofs = c->gofs;
+    A.stride = c->stride;
+    A.off_g = c->off_g;
+    A.off_ipose = c->off_ipose;
+    A.off_isph = c->off_isph;
+    A.off_iwr = c->off_iwr;
+    A.off_gT = c->off_gT;
+    A.off_gTi = c->off_gTi;
+    return A;
+}
+
+// ------------------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------------------
+extern "C" {
+
+int32_t tamp_abi_version(void) { return TAMP_ABI_VERSION; }
+
+const char* tamp_last_error(void) { return g_err.c_str(); }
+
+size_t tamp_sizeof_desc(void) { return sizeof(tamp_problem_desc); }
+
+size_t tamp_sizeof_info(void) { return sizeof(tamp_info); }
+
+uint64_t tamp_kernel_launches(void) { return tamp::launch_count(); }
+
+tamp_status tamp_query_workspace(const tamp_problem_desc* desc, int64_t n_local, size_t* bytes) {
+    if (!desc || !bytes) return fail(TAMP_E_INVALID, "null argument");
+    if (n_local < 1 || n_local > (1ll << 30)) return fail(TAMP_E_INVALID, "n_local must be in [1, 2^30]");
+    tamp_ctx tmp;
+    Compiled C;
+    tamp_status s = compile(*desc, n_local, C);
+    if (s != TAMP_OK) return s;
+    tmp.P = C.P;
+    tmp.n = n_local;
+    ws_layout(&tmp);
+    *bytes = tmp.total;
+    return TAMP_OK;
+}
+
+tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t n_local, int64_t global_offset,
+                              int64_t n_global, void* d_workspace, size_t ws_bytes, tamp_ctx** out) {
+    if (!desc || !out) return fail(TAMP_E_INVALID, "null argument");
+    *out = nullptr;
+    if (n_local < 1 || n_local > (1ll << 30)) return fail(TAMP_E_INVALID, "n_local must be in [1, 2^30]");
+    if (global_offset < 0 || n_global < global_offset + n_local || n_global > (1ll << 30))
+        return fail(TAMP_E_INVALID, "need 0 <= global_offset, global_offset + n_local <= n_global <= 2^30");
+    if (!d_workspace || (reinterpret_cast<uintptr_t>(d_workspace) & 255))
+        return fail(TAMP_E_INVALID, "workspace must be a 256-byte aligned device pointer");
+    Compiled C;
+    tamp_status s = compile(*desc, n_global, C);
+    if (s != TAMP_OK) return s;
+    tamp_ctx* c = new tamp_ctx();
+    c->device = device;
+    c->n = n_local;
+    c->gofs = global_offset;
+    c->nglob = n_global;
+    c->P = C.P;
+    c->SP = C.SP;
+    std::memcpy(c->term_kind, C.term_kind, sizeof(c->term_kind));
+    c->pairs_sb = C.pairs_sb;
+    c->pairs_ss = C.pairs_ss;
+    c->n_robot_spheres = desc->robot.n_spheres;
+    ws_layout(c);
+    smem_layout(c);
+    if (ws_bytes < c->total) {
+        delete c;
+        return fail(TAMP_E_NOMEM, "workspace too small: need " + std::to_string(c->total) + " bytes");
+    }
+    if (c->smem > 200 * 1024) {
+        delete c;
+        return fail(TAMP_E_UNSUPPORTED, "per-block shared memory exceeds 200 KB");
+    }
+    c->base = static_cast<char*>(d_workspace);
+    c->ws_bytes = ws_bytes;
+    c->coords.reserve(3 * C.lr.size());
+    c->coords.insert(c->coords.end(), C.lr.begin(), C.lr.end());
+    c->coords.insert(c->coords.end(), C.lo.begin(), C.lo.end());
+    c->coords.insert(c->coords.end(), C.hi.begin(), C.hi.end());
+    DeviceGuard g(device);
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, d_workspace) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        delete c;
+        return fail(TAMP_E_INVALID, "workspace is not device memory");
+    }
+    if (!c->coords.empty()) {
+        cudaError_t e = cudaMemcpy(c->at<float>(c->o_coords), c->coords.data(), c->coords.size() * 4,
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { delete c; return cuda_fail(e, "init: upload bounds"); }
+    }
+    *out = c;
+    return TAMP_OK;
+}
+
+tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
+    if (!c || !out) return fail(TAMP_E_INVALID, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->D = c->P.D;
+    out->n_hard = c->P.n_terms;
+    out->n_grasp = c->P.n_grasp;
+    out->n_fk = c->P.n_fk;
+    for (int i = 0; i < c->P.n_terms; ++i) out->term_kind[i] = c->term_kind[i];
+    out->n_local = c->n;
+    out->global_offset = c->gofs;
+    out->n_global = c->nglob;
+    out->t = c->t;
+    out->pairs_sphere_obb = c->pairs_sb;
+    out->pairs_sphere_sphere = c->pairs_ss;
+    int n_kin = 0, n_seg = 0;
+    for (int f = 0; f < c->P.n_fk; ++f) n_kin += c->P.fk[f].term_kp >= 0;
+    for (int i = 0; i < c->P.n_traj; ++i) n_seg += c->P.traj[i].n_knots + 1;
+    out->n_kin = n_kin;
+    out->n_place = c->P.n_place;
+    out->n_goal_pairs = c->P.n_goal * (c->P.n_goal - 1) / 2;
+    out->n_traj_seg = n_seg;
+    out->n_robot_spheres = c->n_robot_spheres;
+    return TAMP_OK;
+}
+
+tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(launch_sample(c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, st), "sample");
+    CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero m");
+    CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero v");
+    CUDA_TRY(cudaMemsetAsync(c->base + c->o_inv, 0, (size_t)c->n, st), "sample: zero invalid");
+    c->t = 0;
+    c->ready = true;
+    return TAMP_OK;
+}
+
+tamp_status tamp_optimize_step(tamp_ctx* c, int32_t n_steps, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!c->ready) return fail(TAMP_E_STATE, "optimize before sample/set_state");
+    if (n_steps < 0) return fail(TAMP_E_INVALID, "n_steps must be >= 0");
+    if (n_steps == 0) return TAMP_OK;
+    DeviceGuard g(c->device);
+    KArgs A = base_args(c);
+    A.n_steps = n_steps;
+    A.t0 = c->t;
+    CUDA_TRY(launch_particle(MODE_OPT, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "optimize");
+    c->t += n_steps;
+    return TAMP_OK;
+}
+
+static tamp_status run_check(tamp_ctx* c, cudaStream_t st) {
+    KArgs A = base_args(c);
+    A.out_cls = c->at<uint8_t>(c->o_cls);
+    A.out_cost = c->at<float>(c->o_cost);
+    A.out_counts = c->at<int32_t>(c->o_counts);
+    CUDA_TRY(cudaMemsetAsync(A.out_counts, 0, (TAMP_MAX_TERMS + 2) * 4, st), "check: zero counts");
+    CUDA_TRY(launch_particle(MODE_CHECK, c->P, A, c->smem, st), "check");
+    return TAMP_OK;
+}
+
+tamp_status tamp_check_satisfied(tamp_ctx* c, uint8_t* cls, int32_t* counts, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!c->ready) return fail(TAMP_E_STATE, "check before sample/set_state");
+    if (!counts) return fail(TAMP_E_INVALID, "counts must not be NULL");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    tamp_status s = run_check(c, st);
+    if (s != TAMP_OK) return s;
+    const size_t nb = (size_t)(c->P.n_terms + 2) * 4;
+    CUDA_TRY(cudaMemcpyAsync(counts, c->at<int32_t>(c->o_counts), nb, cudaMemcpyDefault, st), "check: counts copy");
+    if (cls) CUDA_TRY(cudaMemcpyAsync(cls, c->at<uint8_t>(c->o_cls), (size_t)c->n, cudaMemcpyDefault, st), "check: cls copy");
+    if (is_host_ptr(counts) || is_host_ptr(cls)) CUDA_TRY(cudaStreamSynchronize(st), "check: sync");
+    return TAMP_OK;
+}
+
+tamp_status tamp_best_k(tamp_ctx* c, int32_t k, float* records, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!c->ready) return fail(TAMP_E_STATE, "best_k before sample/set_state");
+    if (!records || k < 1 || k > 1024 || k > c->n) return fail(TAMP_E_INVALID, "need 1 <= k <= min(1024, n_local)");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    tamp_status s = run_check(c, st);
+    if (s != TAMP_OK) return s;
+    unsigned long long *ka = c->at<unsigned long long>(c->o_ka), *kb = c->at<unsigned long long>(c->o_kb);
+    int32_t *pa = c->at<int32_t>(c->o_pa), *pb = c->at<int32_t>(c->o_pb);
+    CUDA_TRY(launch_make_keys(c->at<uint8_t>(c->o_cls), c->at<float>(c->o_cost), c->n, c->gofs, ka, pa, st), "best_k: keys");
+    unsigned long long* kr;
+    int32_t* pr;
+    CUDA_TRY(launch_topk(ka, pa, kb, pb, c->n, k, st, &kr, &pr), "best_k: sort");
+    float* stage = c->at<float>(c->o_stage);
+    CUDA_TRY(launch_gather_particles(pr, kr, k, c->at<float>(c->o_x), c->at<float>(c->o_cost), c->P.D, c->gofs, stage, st),
+             "best_k: gather");
+    CUDA_TRY(cudaMemcpyAsync(records, stage, (size_t)k * (c->P.D + 4) * 4, cudaMemcpyDefault, st), "best_k: copy");
+    if (is_host_ptr(records)) CUDA_TRY(cudaStreamSynchronize(st), "best_k: sync");
+    return TAMP_OK;
+}
+
+tamp_status tamp_merge_best_k(tamp_ctx* c, const float* d_in, int32_t n_in, int32_t k, float* d_out, void* stream) {
+    if (!c || !d_in || !d_out) return fail(TAMP_E_INVALID, "null argument");
+    if (n_in < 1 || n_in > 65536 || k < 1 || k > n_in || k > 1024) return fail(TAMP_E_INVALID, "need 1 <= k <= n_in <= 65536, k <= 1024");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int width = c->P.D + 4;
+    unsigned long long *ka = c->at<unsigned long long>(c->o_ka), *kb = c->at<unsigned long long>(c->o_kb);
+    int32_t *pa = c->at<int32_t>(c->o_pa), *pb = c->at<int32_t>(c->o_pb);
+    CUDA_TRY(launch_record_keys(d_in, n_in, width, ka, pa, st), "merge: keys");
+    unsigned long long* kr;
+    int32_t* pr;
+    CUDA_TRY(launch_topk(ka, pa, kb, pb, n_in, k, st, &kr, &pr), "merge: sort");
+    CUDA_TRY(launch_gather_records(pr, k, d_in, width, d_out, st), "merge: gather");
+    return TAMP_OK;
+}
+
+tamp_status tamp_eval(tamp_ctx* c, float* J, float* soft, float* Jc, float* grad, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!c->ready) return fail(TAMP_E_STATE, "eval before sample/set_state");
+    for (const void* p : {(const void*)J, (const void*)soft, (const void*)Jc, (const void*)grad})
+        if (p && is_host_ptr(p)) return fail(TAMP_E_INVALID, "tamp_eval outputs must be device pointers");
+    DeviceGuard g(c->device);
+    KArgs A = base_args(c);
+    A.out_J = J;
+    A.out_soft = soft;
+    A.out_Jc = Jc;
+    A.out_grad = grad;
+    CUDA_TRY(launch_particle(MODE_EVAL, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "eval");
+    return TAMP_OK;
+}
+
+tamp_status tamp_get_state(tamp_ctx* c, float* x, float* m, float* v, float* grasp, uint8_t* invalid, int32_t* t,
+                           void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!c->ready) return fail(TAMP_E_STATE, "get_state before sample/set_state");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t nd = (size_t)c->n * c->P.D * 4;
+    bool host = false;
+    if (x) { CUDA_TRY(cudaMemcpyAsync(x, c->base + c->o_x, nd, cudaMemcpyDefault, st), "get x"); host |= is_host_ptr(x); }
+    if (m) { CUDA_TRY(cudaMemcpyAsync(m, c->base + c->o_m, nd, cudaMemcpyDefault, st), "get m"); host |= is_host_ptr(m); }
+    if (v) { CUDA_TRY(cudaMemcpyAsync(v, c->base + c->o_v, nd, cudaMemcpyDefault, st), "get v"); host |= is_host_ptr(v); }
+    if (grasp && c->P.n_grasp) {
+        CUDA_TRY(cudaMemcpyAsync(grasp, c->base + c->o_grasp, (size_t)c->n * c->P.n_grasp * 48, cudaMemcpyDefault, st), "get grasp");
+        host |= is_host_ptr(grasp);
+    }
+    if (invalid) {
+        CUDA_TRY(cudaMemcpyAsync(invalid, c->base + c->o_inv, (size_t)c->n, cudaMemcpyDefault, st), "get invalid");
+        host |= is_host_ptr(invalid);
+    }
+    if (t) *t = c->t;
+    if (host) CUDA_TRY(cudaStreamSynchronize(st), "get_state: sync");
+    return TAMP_OK;
+}
+
+tamp_status tamp_set_state(tamp_ctx* c, const float* x, const float* m, const float* v, const float* grasp,
+                           const uint8_t* invalid, int32_t t, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!x) return fail(TAMP_E_INVALID, "set_state needs x");
+    if (t < 0) return fail(TAMP_E_INVALID, "t must be >= 0");
+    if (!grasp && c->P.n_grasp && !c->ready) return fail(TAMP_E_STATE, "first set_state must provide grasps");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t nd = (size_t)c->n * c->P.D * 4;
+    CUDA_TRY(cudaMemcpyAsync(c->base + c->o_x, x, nd, cudaMemcpyDefault, st), "set x");
+    if (m) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_m, m, nd, cudaMemcpyDefault, st), "set m");
+    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, nd, st), "zero m");
+    if (v) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_v, v, nd, cudaMemcpyDefault, st), "set v");
+    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, nd, st), "zero v");
+    if (grasp && c->P.n_grasp)
+        CUDA_TRY(cudaMemcpyAsync(c->base + c->o_grasp, grasp, (size_t)c->n * c->P.n_grasp * 48, cudaMemcpyDefault, st), "set grasp");
+    if (invalid) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_inv, invalid, (size_t)c->n, cudaMemcpyDefault, st), "set invalid");
+    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_inv, 0, (size_t)c->n, st), "zero invalid");
+    if (is_host_ptr(x) || is_host_ptr(m) || is_host_ptr(v) || is_host_ptr(grasp) || is_host_ptr(invalid))
+        CUDA_TRY(cudaStreamSynchronize(st), "set_state: sync");
+    c->t = t;
+    c->ready = true;
+    return TAMP_OK;
+}
+
+void tamp_destroy(tamp_ctx* c) { delete c; }
+
+}  // extern "C"

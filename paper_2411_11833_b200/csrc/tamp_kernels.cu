@@ -1,0 +1,1054 @@
+// tamp_kernels.cu -- sm_100a kernels of the cuTAMP particle-optimisation hot path.
+//
+//   K1 k_sample      InitializeParticles: Philox4x32-10 counter RNG + samplers
+//   K2 k_particle    fused Eq. 2 cost + hand-derived backward + Adam/projection, n_steps per launch
+//                    (P:429-478); the same template also serves K3 (check, Eq. 3 + Eq. 5 counts) and
+//                    the eval/inspection mode
+//   K4 k_sort_chunk  best-k: bitonic sort of (key, payload) chunks, repeated until <= one chunk
+//   K5 k_gather      records of the selected particles / merge of gathered records
+//
+// Mapping: one particle per 8-lane group, 4 particles per warp.  Lane l
+// owns link frame l+1 of the 7-DOF chain (lane 7: the tool frame) and the <= 4 robot spheres on it.
+// FK is an inclusive product scan of the per-joint transforms across the 8 lanes (3 shuffle steps);
+// the backward is the reverse (suffix) scan of per-link wrenches:  dJ/dq_j = z_j . (M_j - o_j x F_j)
+// with F_j, M_j the total force / moment (about the world origin) on links >= j.  Object spheres live
+// in per-particle shared memory and are broadcast to the group; gradients on movable objects are
+// accumulated as wrenches per object instance and converted to placement gradients at the end.
+// No tensor cores: the math is 3x4 transform chains and pairwise distances (north_star).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "tamp_program.h"
+
+namespace tamp {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr float kPi = 3.14159265358979323846f;
+
+// ------------------------------------------------------------------------------------------------
+// small math
+// ------------------------------------------------------------------------------------------------
+struct M34 {
+    float r[9];   // row-major rotation
+    float t[3];
+};
+
+__device__ __forceinline__ M34 compose(const M34& a, const M34& b) {
+    M34 c;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            c.r[3 * i + j] = fmaf(a.r[3 * i], b.r[j], fmaf(a.r[3 * i + 1], b.r[3 + j], a.r[3 * i + 2] * b.r[6 + j]));
+        c.t[i] = fmaf(a.r[3 * i], b.t[0], fmaf(a.r[3 * i + 1], b.t[1], fmaf(a.r[3 * i + 2], b.t[2], a.t[i])));
+    }
+    return c;
+}
+
+__device__ __forceinline__ M34 shfl_m34(const M34& a, int src) {
+    M34 o;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) o.r[i] = __shfl_sync(FULL, a.r[i], src, kGroup);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) o.t[i] = __shfl_sync(FULL, a.t[i], src, kGroup);
+    return o;
+}
+
+__device__ __forceinline__ M34 shfl_up_m34(const M34& a, int d) {
+    M34 o;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) o.r[i] = __shfl_up_sync(FULL, a.r[i], d, kGroup);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) o.t[i] = __shfl_up_sync(FULL, a.t[i], d, kGroup);
+    return o;
+}
+
+__device__ __forceinline__ void load_m34(M34& a, const float* s) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        a.r[3 * i] = s[4 * i];
+        a.r[3 * i + 1] = s[4 * i + 1];
+        a.r[3 * i + 2] = s[4 * i + 2];
+        a.t[i] = s[4 * i + 3];
+    }
+}
+
+__device__ __forceinline__ void inv_m34(const M34& a, M34& o) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) o.r[3 * i + j] = a.r[3 * j + i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        o.t[i] = -(o.r[3 * i] * a.t[0] + o.r[3 * i + 1] * a.t[1] + o.r[3 * i + 2] * a.t[2]);
+}
+
+__device__ __forceinline__ void xform(const M34& T, float x, float y, float z, float& ox, float& oy, float& oz) {
+    ox = fmaf(T.r[0], x, fmaf(T.r[1], y, fmaf(T.r[2], z, T.t[0])));
+    oy = fmaf(T.r[3], x, fmaf(T.r[4], y, fmaf(T.r[5], z, T.t[1])));
+    oz = fmaf(T.r[6], x, fmaf(T.r[7], y, fmaf(T.r[8], z, T.t[2])));
+}
+
+__device__ __forceinline__ float gsum(float v) {      // butterfly sum over the 8-lane group
+    v += __shfl_xor_sync(FULL, v, 1, kGroup);
+    v += __shfl_xor_sync(FULL, v, 2, kGroup);
+    v += __shfl_xor_sync(FULL, v, 4, kGroup);
+    return v;
+}
+
+struct Wrench {
+    float f[3];
+    float m[3];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) f[i] = m[i] = 0.f;
+    }
+    // force g applied at point w: F += g, M += w x g
+    __device__ __forceinline__ void add_point(float wx, float wy, float wz, float gx, float gy, float gz) {
+        f[0] += gx; f[1] += gy; f[2] += gz;
+        m[0] = fmaf(wy, gz, fmaf(-wz, gy, m[0]));
+        m[1] = fmaf(wz, gx, fmaf(-wx, gz, m[1]));
+        m[2] = fmaf(wx, gy, fmaf(-wy, gx, m[2]));
+    }
+    __device__ __forceinline__ bool nonzero() const {
+        return (f[0] != 0.f) | (f[1] != 0.f) | (f[2] != 0.f) | (m[0] != 0.f) | (m[1] != 0.f) | (m[2] != 0.f);
+    }
+    __device__ __forceinline__ void group_sum() {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) { f[i] = gsum(f[i]); m[i] = gsum(m[i]); }
+    }
+};
+
+// ------------------------------------------------------------------------------------------------
+// collision primitives (hinge max(0, r + eta - sd), L1)
+// ------------------------------------------------------------------------------------------------
+// Sphere vs OBB.  Returns the hinge value; if GRAD adds lam * dJ/dw to (gx, gy, gz).
+template <bool GRAD>
+__device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float rr, const KObb& B, float lam,
+                                            float& gx, float& gy, float& gz) {
+    const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
+    const float px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
+    const float py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
+    const float pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
+    const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(pz) - B.h[2];
+    const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
+    const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+    const float mx = fmaxf(ax, fmaxf(ay, az));
+    if (mx > 0.f && s >= rr * rr) return 0.f;          // outside and beyond reach: inactive
+    float sd, gpx, gpy, gpz;
+    if (s > 1e-30f) {                                    // outside: sd = ||max(a, 0)||
+        const float inv = rsqrtf(s);
+        sd = s * inv;
+        gpx = copysignf(qx * inv, px);
+        gpy = copysignf(qy * inv, py);
+        gpz = copysignf(qz * inv, pz);
+    } else {                                             // inside: sd = max_k a_k, grad sign(p_k) e_k
+        sd = mx;
+        int k = 0;
+        float best = ax;
+        if (ay > best) { k = 1; best = ay; }
+        if (az > best) { k = 2; }
+        gpx = (k == 0) ? copysignf(1.f, px) : 0.f;
+        gpy = (k == 1) ? copysignf(1.f, py) : 0.f;
+        gpz = (k == 2) ? copysignf(1.f, pz) : 0.f;
+    }
+    const float pen = rr - sd;
+    if (!(pen > 0.f)) return 0.f;
+    if (GRAD) {   // dJ/dw = -R grad_p
+        gx = fmaf(-lam, fmaf(B.R[0], gpx, fmaf(B.R[1], gpy, B.R[2] * gpz)), gx);
+        gy = fmaf(-lam, fmaf(B.R[3], gpx, fmaf(B.R[4], gpy, B.R[5] * gpz)), gy);
+        gz = fmaf(-lam, fmaf(B.R[6], gpx, fmaf(B.R[7], gpy, B.R[8] * gpz)), gz);
+    }
+    return pen;
+}
+
+// Sphere vs sphere.  Returns the hinge; if GRAD: (ux, uy, uz) = lam * (w_a - w_b)/||.|| (0 if inactive).
+template <bool GRAD>
+__device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, float rr, float4 b,
+                                               float lam, float& ux, float& uy, float& uz) {
+    const float dx = ax - b.x, dy = ay - b.y, dz = az - b.z;
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float R = rr + b.w;
+    ux = uy = uz = 0.f;
+    if (d2 >= R * R) return 0.f;
+    if (d2 > 0.f) {
+        const float inv = rsqrtf(d2);
+        const float pen = R - d2 * inv;
+        if (!(pen > 0.f)) return 0.f;
+        if (GRAD) {
+            const float k = lam * inv;
+            ux = dx * k; uy = dy * k; uz = dz * k;
+        }
+        return pen;
+    }
+    return R;   // coincident centres: cost R, zero gradient (L13)
+}
+
+// ------------------------------------------------------------------------------------------------
+// K2 / K3 / eval: the fused per-particle kernel
+// ------------------------------------------------------------------------------------------------
+template <int MODE>
+struct TermSink {
+    float J = 0.f;
+    bool sat = true;
+};
+
+template <int MODE>
+__device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, TermSink<MODE>& sink, int term,
+                                            float val, int gl, bool active, int64_t p, int* s_counts) {
+    sink.J = fmaf(P.term_lam[term], val, sink.J);
+    if (MODE == MODE_EVAL) {
+        if (gl == 0 && active && A.out_Jc) A.out_Jc[p * P.n_terms + term] = val;
+    } else if (MODE == MODE_CHECK) {
+        const bool ok = val <= P.term_eps[term];
+        sink.sat = sink.sat && ok;
+        if (gl == 0 && active && ok) atomicAdd(&s_counts[term], 1);
+    }
+}
+
+// KM = register-resident Adam moments per lane (coords gl, gl+8, ...); 0 = moments stay in global memory
+template <int MODE, int KM>
+__global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
+    constexpr bool GRAD = MODE != MODE_CHECK;
+    extern __shared__ float4 smem4[];
+    __shared__ float4 s_osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES];
+    __shared__ int s_counts[TAMP_MAX_TERMS + 2];
+
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int grp = threadIdx.x / kGroup;
+    const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / kGroup) + grp;
+    const bool active = pid < A.n;
+    const int64_t p = active ? pid : (A.n - 1);
+    float* S = reinterpret_cast<float*>(smem4) + (size_t)grp * A.stride;
+    float* xs = S;
+    float* gs = S + A.off_g;
+    float* ipose = S + A.off_ipose;
+    float4* isph = reinterpret_cast<float4*>(S + A.off_isph);
+    float* iwr = S + A.off_iwr;
+    float* gT = S + A.off_gT;
+    float* gTi = S + A.off_gTi;
+    const int D = P.D;
+
+    for (int i = threadIdx.x; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += blockDim.x) {
+        const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
+        s_osph[o][k] = make_float4(P.osph[o][k][0], P.osph[o][k][1], P.osph[o][k][2], P.osph[o][k][3]);
+    }
+    if (MODE == MODE_CHECK)
+        for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
+
+    // per-lane robot data: fixed transform of my joint (lane 7: tool) and my link's spheres
+    M34 F;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        F.r[3 * i] = P.F[gl][4 * i]; F.r[3 * i + 1] = P.F[gl][4 * i + 1];
+        F.r[3 * i + 2] = P.F[gl][4 * i + 2]; F.t[i] = P.F[gl][4 * i + 3];
+    }
+    float sph[TAMP_MAX_SPHERES_PER_LINK][4];
+    const int nsph = P.rsph_n[gl];
+#pragma unroll
+    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sph[k][c] = P.rsph[gl][k][c];
+    const float jlo = gl < TAMP_NJ ? P.jlo[gl] : 0.f;
+    const float jhi = gl < TAMP_NJ ? P.jhi[gl] : 0.f;
+
+    // particle state -> shared memory / registers
+    const float* xg = A.x + p * D;
+    for (int d = gl; d < D; d += kGroup) xs[d] = xg[d];
+    float mreg[KM > 0 ? KM : 1], vreg[KM > 0 ? KM : 1];
+    if (MODE == MODE_OPT && KM > 0) {
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+            const int d = gl + kGroup * k;
+            mreg[k] = d < D ? A.m[p * D + d] : 0.f;
+            vreg[k] = d < D ? A.v[p * D + d] : 0.f;
+        }
+    }
+    for (int i = gl; i < P.n_grasp * 12; i += kGroup) gT[(i / 12) * 16 + (i % 12)] = A.grasp[(p * P.n_grasp) * 12 + i];
+    bool invalid = A.invalid[p] != 0;
+    __syncthreads();
+    if (gl == 0) {
+        for (int k = 0; k < P.n_grasp; ++k) {
+            M34 g, gi;
+            load_m34(g, gT + 16 * k);
+            inv_m34(g, gi);
+            float* o = gTi + 16 * k;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                o[4 * i] = gi.r[3 * i]; o[4 * i + 1] = gi.r[3 * i + 1]; o[4 * i + 2] = gi.r[3 * i + 2];
+                o[4 * i + 3] = gi.t[i];
+            }
+        }
+    }
+    __syncwarp();
+
+    const int n_iter = (MODE == MODE_OPT) ? A.n_steps : 1;
+    for (int it = 0; it < n_iter; ++it) {
+        TermSink<MODE> sink;
+        float soft = 0.f;
+
+        // ---- phase A: object instances (poses, world sphere centres), zero accumulators ----
+        for (int i = 0; i < P.n_inst; ++i) {
+            const KInst& I = P.inst[i];
+            float px, py, pz, yaw;
+            if (I.xoff >= 0) { px = xs[I.xoff]; py = xs[I.xoff + 1]; pz = xs[I.xoff + 2]; yaw = xs[I.xoff + 3]; }
+            else { px = I.pose[0]; py = I.pose[1]; pz = I.pose[2]; yaw = I.pose[3]; }
+            float sy, cy;
+            sincosf(yaw, &sy, &cy);
+            float* ip = ipose + 16 * i;      // [R row0 | t0, R row1 | t1, R row2 | t2]
+            if (gl == 0) {
+                ip[0] = cy; ip[1] = -sy; ip[2] = 0.f; ip[3] = px;
+                ip[4] = sy; ip[5] = cy; ip[6] = 0.f; ip[7] = py;
+                ip[8] = 0.f; ip[9] = 0.f; ip[10] = 1.f; ip[11] = pz;
+            }
+            if (gl < P.osph_n[I.obj]) {
+                const float4 c = s_osph[I.obj][gl];
+                isph[i * TAMP_MAX_OBJ_SPHERES + gl] =
+                    make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w);
+            }
+            if (GRAD && gl < 6) iwr[8 * i + gl] = 0.f;
+        }
+        if (GRAD) for (int d = gl; d < D; d += kGroup) gs[d] = 0.f;
+        __syncwarp();
+
+        // ---- phase B: robot configurations (Pick/Place confs, knots) ----
+        for (int f = 0; f < P.n_fk; ++f) {
+            const KFk K = P.fk[f];
+            const float q = gl < TAMP_NJ ? xs[K.xoff + gl] : 0.f;
+            // A_l = F_l Rz(q_l)
+            M34 T;
+            {
+                float s, c;
+                sincosf(q, &s, &c);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    T.r[3 * i] = fmaf(F.r[3 * i], c, F.r[3 * i + 1] * s);
+                    T.r[3 * i + 1] = fmaf(F.r[3 * i + 1], c, -F.r[3 * i] * s);
+                    T.r[3 * i + 2] = F.r[3 * i + 2];
+                    T.t[i] = F.t[i];
+                }
+            }
+            // inclusive product scan: T_l = A_0 A_1 ... A_l  (FK)
+#pragma unroll
+            for (int d = 1; d < kGroup; d <<= 1) {
+                const M34 U = shfl_up_m34(T, d);
+                if (gl >= d) T = compose(U, T);
+            }
+            const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
+            // my link's spheres in the world
+            float w[TAMP_MAX_SPHERES_PER_LINK][3], gw[TAMP_MAX_SPHERES_PER_LINK][3];
+#pragma unroll
+            for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                xform(T, sph[k][0], sph[k][1], sph[k][2], w[k][0], w[k][1], w[k][2]);
+                gw[k][0] = gw[k][1] = gw[k][2] = 0.f;
+            }
+            float jcf = 0.f;
+            Wrench link;
+            link.zero();
+            if (K.term_cf >= 0) {
+                // robot spheres vs OBBs
+                for (int b = 0; b < P.n_obb; ++b) {
+                    if (!((K.obb_mask >> b) & 1)) continue;
+                    const KObb& B = P.obb[b];
+#pragma unroll
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k)
+                        if (k < nsph) jcf += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], sph[k][3] + P.eta, B, lam_cf,
+                                                              gw[k][0], gw[k][1], gw[k][2]);
+                }
+                // robot spheres vs movable objects' spheres
+                for (int pi = 0; pi < K.part_count; ++pi) {
+                    const int ii = P.partners[K.part_begin + pi];
+                    const KInst& I = P.inst[ii];
+                    const int no = P.osph_n[I.obj];
+                    Wrench pw;
+                    pw.zero();
+                    for (int b = 0; b < no; ++b) {
+                        const float4 B = isph[ii * TAMP_MAX_OBJ_SPHERES + b];
+#pragma unroll
+                        for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                            if (k >= nsph) continue;
+                            float ux, uy, uz;
+                            jcf += sphere_sphere<GRAD>(w[k][0], w[k][1], w[k][2], sph[k][3] + P.eta, B, lam_cf, ux, uy, uz);
+                            if (GRAD) {
+                                gw[k][0] -= ux; gw[k][1] -= uy; gw[k][2] -= uz;
+                                pw.add_point(B.x, B.y, B.z, ux, uy, uz);
+                            }
+                        }
+                    }
+                    if (GRAD && I.xoff >= 0 && __any_sync(FULL, pw.nonzero())) {
+                        pw.group_sum();
+                        if (gl == 0) {
+                            float* dst = iwr + 8 * ii;
+                            dst[0] += pw.f[0]; dst[1] += pw.f[1]; dst[2] += pw.f[2];
+                            dst[3] += pw.m[0]; dst[4] += pw.m[1]; dst[5] += pw.m[2];
+                        }
+                    }
+                }
+            }
+            if (GRAD) {
+#pragma unroll
+                for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k)
+                    link.add_point(w[k][0], w[k][1], w[k][2], gw[k][0], gw[k][1], gw[k][2]);
+            }
+            // tool frame to every lane of the group
+            const M34 Tee = shfl_m34(T, kGroup - 1);
+            // held object at a MoveHold knot: attached spheres T_ee T(g)^-1 c (CFreeTrajHold)
+            if (K.held_grasp >= 0 && K.term_cf >= 0) {
+                M34 Gi, Tobj;
+                load_m34(Gi, gTi + 16 * K.held_grasp);
+                Tobj = compose(Tee, Gi);
+                const int ho = K.held_obj;
+                float hx = 0.f, hy = 0.f, hz = 0.f, hr = 0.f, ghx = 0.f, ghy = 0.f, ghz = 0.f;
+                const bool mine = gl < P.osph_n[ho];
+                if (mine) {
+                    const float4 c = s_osph[ho][gl];
+                    xform(Tobj, c.x, c.y, c.z, hx, hy, hz);
+                    hr = c.w + P.eta;
+                }
+                for (int b = 0; b < P.n_obb; ++b) {
+                    if (!((K.obb_mask >> b) & 1)) continue;
+                    if (mine) jcf += sphere_obb<GRAD>(hx, hy, hz, hr, P.obb[b], lam_cf, ghx, ghy, ghz);
+                }
+                for (int pi = 0; pi < K.part_count; ++pi) {
+                    const int ii = P.partners[K.part_begin + pi];
+                    const KInst& I = P.inst[ii];
+                    const int no = P.osph_n[I.obj];
+                    Wrench pw;
+                    pw.zero();
+                    for (int b = 0; b < no; ++b) {
+                        const float4 B = isph[ii * TAMP_MAX_OBJ_SPHERES + b];
+                        if (!mine) continue;
+                        float ux, uy, uz;
+                        jcf += sphere_sphere<GRAD>(hx, hy, hz, hr, B, lam_cf, ux, uy, uz);
+                        if (GRAD) {
+                            ghx -= ux; ghy -= uy; ghz -= uz;
+                            pw.add_point(B.x, B.y, B.z, ux, uy, uz);
+                        }
+                    }
+                    if (GRAD && I.xoff >= 0 && __any_sync(FULL, pw.nonzero())) {
+                        pw.group_sum();
+                        if (gl == 0) {
+                            float* dst = iwr + 8 * ii;
+                            dst[0] += pw.f[0]; dst[1] += pw.f[1]; dst[2] += pw.f[2];
+                            dst[3] += pw.m[0]; dst[4] += pw.m[1]; dst[5] += pw.m[2];
+                        }
+                    }
+                }
+                if (GRAD) {   // held-object wrench acts on the tool link (lane 7)
+                    Wrench hw;
+                    hw.zero();
+                    hw.add_point(hx, hy, hz, ghx, ghy, ghz);
+                    hw.group_sum();
+                    if (gl == kGroup - 1) {
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) { link.f[i] += hw.f[i]; link.m[i] += hw.m[i]; }
+                    }
+                }
+            }
+            if (K.term_cf >= 0) finish_term<MODE>(P, A, sink, K.term_cf, gsum(jcf), gl, active, p, s_counts);
+
+            // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane (uniform)
+            if (K.term_kp >= 0 || K.term_kr >= 0) {
+                M34 Tp, Tg;
+                load_m34(Tp, ipose + 16 * K.kin_inst);
+                load_m34(Tg, gT + 16 * K.kin_grasp);
+                const M34 Ts = compose(Tp, Tg);
+                // position error e = ||t_ee - t*||  (L5)
+                const float dx = Tee.t[0] - Ts.t[0], dy = Tee.t[1] - Ts.t[1], dz = Tee.t[2] - Ts.t[2];
+                const float e2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                const float epos = sqrtf(e2);
+                // rotation error: M = R_ee^T R*, theta = atan2(||vee(M - M^T)||/2, (tr M - 1)/2)  (L4)
+                float Mm[9];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        Mm[3 * i + j] = fmaf(Tee.r[i], Ts.r[j], fmaf(Tee.r[3 + i], Ts.r[3 + j], Tee.r[6 + i] * Ts.r[6 + j]));
+                const float wx = Mm[7] - Mm[5], wy = Mm[2] - Mm[6], wz = Mm[3] - Mm[1];
+                const float wn2 = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
+                const float wn = sqrtf(wn2);
+                const float erot = atan2f(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
+                if (K.term_kp >= 0) finish_term<MODE>(P, A, sink, K.term_kp, epos, gl, active, p, s_counts);
+                if (K.term_kr >= 0) finish_term<MODE>(P, A, sink, K.term_kr, erot, gl, active, p, s_counts);
+                if (GRAD) {
+                    Wrench tw;   // on the target placement instance
+                    tw.zero();
+                    if (K.term_kp >= 0 && epos > 0.f) {
+                        const float k = P.term_lam[K.term_kp] / epos;
+                        const float fx = dx * k, fy = dy * k, fz = dz * k;      // dJ/dt_ee
+                        if (gl == kGroup - 1) link.add_point(Tee.t[0], Tee.t[1], Tee.t[2], fx, fy, fz);
+                        tw.add_point(Ts.t[0], Ts.t[1], Ts.t[2], -fx, -fy, -fz);
+                    }
+                    if (K.term_kr >= 0 && wn > 0.f) {
+                        // u = R_ee w / ||w||: d theta = -u . omega_ee, +u . omega_target  (Appendix A.2)
+                        const float k = P.term_lam[K.term_kr] / wn;
+                        const float ux = k * fmaf(Tee.r[0], wx, fmaf(Tee.r[1], wy, Tee.r[2] * wz));
+                        const float uy = k * fmaf(Tee.r[3], wx, fmaf(Tee.r[4], wy, Tee.r[5] * wz));
+                        const float uz = k * fmaf(Tee.r[6], wx, fmaf(Tee.r[7], wy, Tee.r[8] * wz));
+                        if (gl == kGroup - 1) { link.m[0] -= ux; link.m[1] -= uy; link.m[2] -= uz; }
+                        tw.m[0] += ux; tw.m[1] += uy; tw.m[2] += uz;
+                    }
+                    if (gl == 0 && P.inst[K.kin_inst].xoff >= 0) {
+                        float* dst = iwr + 8 * K.kin_inst;
+                        dst[0] += tw.f[0]; dst[1] += tw.f[1]; dst[2] += tw.f[2];
+                        dst[3] += tw.m[0]; dst[4] += tw.m[1]; dst[5] += tw.m[2];
+                    }
+                }
+            }
+
+            // joint limits: dist_from_bounds(q, lo, hi)  (Listing 2; Motion P:1025)
+            float ejl = 0.f, jl = 0.f;
+            if (K.term_jl >= 0) {
+                ejl = gl < TAMP_NJ ? fmaxf(fmaxf(jlo - q, q - jhi), 0.f) : 0.f;
+                jl = sqrtf(gsum(ejl * ejl));
+                finish_term<MODE>(P, A, sink, K.term_jl, jl, gl, active, p, s_counts);
+            }
+            if (GRAD) {
+                // suffix sums of link wrenches over lanes >= l, then dJ/dq = z . (M - o x F)
+#pragma unroll
+                for (int d = 1; d < kGroup; d <<= 1) {
+                    float v[6];
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        v[i] = __shfl_down_sync(FULL, link.f[i], d, kGroup);
+                        v[3 + i] = __shfl_down_sync(FULL, link.m[i], d, kGroup);
+                    }
+                    if (gl + d < kGroup) {
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) { link.f[i] += v[i]; link.m[i] += v[3 + i]; }
+                    }
+                }
+                if (gl < TAMP_NJ) {
+                    const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
+                    const float ox = T.t[0], oy = T.t[1], oz = T.t[2];
+                    const float mx = link.m[0] - (oy * link.f[2] - oz * link.f[1]);
+                    const float my = link.m[1] - (oz * link.f[0] - ox * link.f[2]);
+                    const float mz = link.m[2] - (ox * link.f[1] - oy * link.f[0]);
+                    float dq = fmaf(zx, mx, fmaf(zy, my, zz * mz));
+                    if (K.term_jl >= 0 && jl > 0.f && ejl > 0.f)
+                        dq += P.term_lam[K.term_jl] * (q > jhi ? ejl : -ejl) / jl;
+                    gs[K.xoff + gl] += dq;
+                }
+            }
+        }
+
+        // ---- phase C: StablePlace (support, containment) and CFreePlace per Place ----
+        for (int pl = 0; pl < P.n_place; ++pl) {
+            const KPlace& Q = P.place[pl];
+            const int ii = Q.inst;
+            const KInst& I = P.inst[ii];
+            const KSurface& Sf = P.surf[Q.surface];
+            const float pz = xs[I.xoff + 2];
+            Wrench own;
+            own.zero();
+            // support: |z_bottom - z_top|  (L6; object frame origin at its bottom, L15)
+            {
+                const float e = fabsf(pz - Sf.frame[2]);
+                finish_term<MODE>(P, A, sink, Q.term_ss, e, gl, active, p, s_counts);
+                if (GRAD && gl == 0 && e > 0.f) {
+                    const float g = P.term_lam[Q.term_ss] * (pz > Sf.frame[2] ? 1.f : -1.f);
+                    own.add_point(xs[I.xoff], xs[I.xoff + 1], pz, 0.f, 0.f, g);
+                }
+            }
+            const int no = P.osph_n[I.obj];
+            const bool mine = gl < no;
+            float4 c = mine ? isph[ii * TAMP_MAX_OBJ_SPHERES + gl] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float gx = 0.f, gy = 0.f, gz = 0.f;
+            // containment: sum over spheres of dist_from_bounds(xy in surface frame, lo + r, hi - r)
+            {
+                float e = 0.f;
+                if (mine) {
+                    float sy, cy;
+                    sincosf(Sf.frame[3], &sy, &cy);
+                    const float rx = c.x - Sf.frame[0], ry = c.y - Sf.frame[1];
+                    const float lx = fmaf(cy, rx, sy * ry), ly = fmaf(-sy, rx, cy * ry);
+                    const float lox = Sf.lo[0] + c.w, hix = Sf.hi[0] - c.w;
+                    const float loy = Sf.lo[1] + c.w, hiy = Sf.hi[1] - c.w;
+                    const float ex = fmaxf(fmaxf(lox - lx, lx - hix), 0.f);
+                    const float ey = fmaxf(fmaxf(loy - ly, ly - hiy), 0.f);
+                    e = sqrtf(fmaf(ex, ex, ey * ey));
+                    if (GRAD && e > 0.f) {
+                        const float k = P.term_lam[Q.term_sc] / e;
+                        const float glx = (lx > hix ? ex : (lx < lox ? -ex : 0.f)) * k;
+                        const float gly = (ly > hiy ? ey : (ly < loy ? -ey : 0.f)) * k;
+                        gx += fmaf(cy, glx, -sy * gly);
+                        gy += fmaf(sy, glx, cy * gly);
+                    }
+                }
+                finish_term<MODE>(P, A, sink, Q.term_sc, gsum(e), gl, active, p, s_counts);
+            }
+            // CFreePlace: placed-object spheres vs OBBs (support excluded) and other objects
+            {
+                const float lam_cp = P.term_lam[Q.term_cp];
+                float jcp = 0.f;
+                const float rr = c.w + P.eta;
+                for (int b = 0; b < P.n_obb; ++b) {
+                    if (!((Q.obb_mask >> b) & 1)) continue;
+                    if (mine) jcp += sphere_obb<GRAD>(c.x, c.y, c.z, rr, P.obb[b], lam_cp, gx, gy, gz);
+                }
+                for (int pi = 0; pi < Q.part_count; ++pi) {
+                    const int jj = P.partners[Q.part_begin + pi];
+                    const KInst& J2 = P.inst[jj];
+                    const int n2 = P.osph_n[J2.obj];
+                    Wrench pw;
+                    pw.zero();
+                    for (int b = 0; b < n2; ++b) {
+                        const float4 B = isph[jj * TAMP_MAX_OBJ_SPHERES + b];
+                        if (!mine) continue;
+                        float ux, uy, uz;
+                        jcp += sphere_sphere<GRAD>(c.x, c.y, c.z, rr, B, lam_cp, ux, uy, uz);
+                        if (GRAD) {
+                            gx -= ux; gy -= uy; gz -= uz;
+                            pw.add_point(B.x, B.y, B.z, ux, uy, uz);
+                        }
+                    }
+                    if (GRAD && J2.xoff >= 0 && __any_sync(FULL, pw.nonzero())) {
+                        pw.group_sum();
+                        if (gl == 0) {
+                            float* dst = iwr + 8 * jj;
+                            dst[0] += pw.f[0]; dst[1] += pw.f[1]; dst[2] += pw.f[2];
+                            dst[3] += pw.m[0]; dst[4] += pw.m[1]; dst[5] += pw.m[2];
+                        }
+                    }
+                }
+                finish_term<MODE>(P, A, sink, Q.term_cp, gsum(jcp), gl, active, p, s_counts);
+            }
+            if (GRAD) {
+                if (mine) own.add_point(c.x, c.y, c.z, gx, gy, gz);
+                own.group_sum();
+                if (gl == 0) {
+                    float* dst = iwr + 8 * ii;
+                    dst[0] += own.f[0]; dst[1] += own.f[1]; dst[2] += own.f[2];
+                    dst[3] += own.m[0]; dst[4] += own.m[1]; dst[5] += own.m[2];
+                }
+            }
+        }
+
+        // ---- phase D: soft costs (Eq. 2 second sum) ----
+        if (P.n_goal > 1) {   // MinimizeObjDist: sum_{i<j} ||P_i - P_j||  (Listing 2 obj_dist)
+            for (int a = 0; a < P.n_goal; ++a) {
+                for (int b = a + 1; b < P.n_goal; ++b) {
+                    const float* pa = ipose + 16 * P.goal_inst[a];
+                    const float* pb = ipose + 16 * P.goal_inst[b];
+                    const float dx = pa[3] - pb[3], dy = pa[7] - pb[7], dz = pa[11] - pb[11];
+                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    soft = fmaf(P.lam_goal, d, soft);
+                    if (GRAD && gl == 0 && d > 0.f) {
+                        const float k = P.lam_goal / d;
+                        const int ia = P.goal_inst[a], ib = P.goal_inst[b];
+                        if (P.inst[ia].xoff >= 0) {
+                            float* t = iwr + 8 * ia;
+                            t[0] += dx * k; t[1] += dy * k; t[2] += dz * k;
+                            t[3] += pa[7] * dz * k - pa[11] * dy * k;
+                            t[4] += pa[11] * dx * k - pa[3] * dz * k;
+                            t[5] += pa[3] * dy * k - pa[7] * dx * k;
+                        }
+                        if (P.inst[ib].xoff >= 0) {
+                            float* t = iwr + 8 * ib;
+                            t[0] -= dx * k; t[1] -= dy * k; t[2] -= dz * k;
+                            t[3] -= pb[7] * dz * k - pb[11] * dy * k;
+                            t[4] -= pb[11] * dx * k - pb[3] * dz * k;
+                            t[5] -= pb[3] * dy * k - pb[7] * dx * k;
+                        }
+                    }
+                }
+            }
+        }
+        for (int tr = 0; tr < P.n_traj; ++tr) {   // TrajLength(tau) = sum_j ||k_{j+1} - k_j||  (Listing 1 cost)
+            const KTraj& Tj = P.traj[tr];
+            const int nseg = Tj.n_knots + 1;
+            const bool mine = gl < TAMP_NJ;
+            auto val = [&](int j) -> float {   // j = 0: q1, 1..K: knots, K+1: q2
+                if (!mine) return 0.f;
+                if (j == 0) return Tj.q1_xoff >= 0 ? xs[Tj.q1_xoff + gl] : P.const_conf[Tj.q1_const][gl];
+                if (j == nseg) return Tj.q2_xoff >= 0 ? xs[Tj.q2_xoff + gl] : P.const_conf[Tj.q2_const][gl];
+                return xs[Tj.knot_xoff + 7 * (j - 1) + gl];
+            };
+            auto xoff_of = [&](int j) -> int {
+                if (j == 0) return Tj.q1_xoff;
+                if (j == nseg) return Tj.q2_xoff;
+                return Tj.knot_xoff + 7 * (j - 1);
+            };
+            for (int j = 0; j < nseg; ++j) {
+                const float dlt = val(j + 1) - val(j);
+                const float len = sqrtf(gsum(dlt * dlt));
+                soft = fmaf(P.lam_traj, len, soft);
+                if (GRAD && mine && len > 0.f) {
+                    const float g = P.lam_traj * dlt / len;
+                    const int o1 = xoff_of(j + 1), o0 = xoff_of(j);
+                    if (o1 >= 0) gs[o1 + gl] += g;
+                    if (o0 >= 0) gs[o0 + gl] -= g;
+                }
+            }
+        }
+        const float Jtot = sink.J + soft;
+
+        // ---- phase E: instance wrenches -> placement gradients ----
+        if (GRAD) {
+            __syncwarp();
+            for (int i = 0; i < P.n_inst; ++i) {
+                const KInst& I = P.inst[i];
+                if (I.xoff < 0) continue;
+                const float* wr = iwr + 8 * i;
+                if (gl < 3) {
+                    gs[I.xoff + gl] += wr[gl];
+                } else if (gl == 3) {   // d/dyaw = z . (M - t x F)
+                    const float tx = xs[I.xoff], ty = xs[I.xoff + 1];
+                    gs[I.xoff + 3] += wr[5] - (tx * wr[1] - ty * wr[0]);
+                }
+            }
+            __syncwarp();
+        }
+
+        if (MODE == MODE_EVAL) {
+            if (active) {
+                if (gl == 0 && A.out_J) A.out_J[p] = Jtot;
+                if (gl == 0 && A.out_soft) A.out_soft[p] = soft;
+                if (A.out_grad) for (int d = gl; d < D; d += kGroup) A.out_grad[p * D + d] = gs[d];
+            }
+        } else if (MODE == MODE_CHECK) {
+            const bool inv = invalid || !isfinite(Jtot);
+            const int cls = inv ? 2 : (sink.sat ? 0 : 1);
+            if (gl == 0 && active) {
+                A.out_cls[p] = (uint8_t)cls;
+                A.out_cost[p] = cls == 0 ? soft : (cls == 1 ? Jtot : 0.f);
+                if (cls == 0) atomicAdd(&s_counts[P.n_terms], 1);
+                if (cls == 2) atomicAdd(&s_counts[P.n_terms + 1], 1);
+            }
+        } else {
+            // ---- phase F: Adam (Kingma & Ba) with grad scale 1/N (Eq. 4) + projection (L11) ----
+            bool bad = !isfinite(Jtot);
+            for (int d = gl; d < D; d += kGroup) bad |= !isfinite(gs[d]);
+            bad = ((__ballot_sync(FULL, bad) >> (threadIdx.x & 24)) & 0xffu) != 0u;   // any lane of my group
+            invalid = invalid || bad;
+            const int t = A.t0 + it + 1;
+            const float bc1 = 1.f - powf(P.beta1, (float)t);
+            const float bc2 = 1.f - powf(P.beta2, (float)t);
+            if (!invalid) {
+                if (KM > 0) {
+#pragma unroll
+                    for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
+                        const int d = gl + kGroup * k;
+                        if (d < D) {
+                            const float g = gs[d] * P.grad_scale;
+                            mreg[k] = fmaf(P.beta1, mreg[k], (1.f - P.beta1) * g);
+                            vreg[k] = fmaf(P.beta2, vreg[k], (1.f - P.beta2) * g * g);
+                            const float mh = mreg[k] / bc1;
+                            const float vh = vreg[k] / bc2;
+                            const float xn = xs[d] - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
+                            xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
+                        }
+                    }
+                } else {
+                    for (int d = gl; d < D; d += kGroup) {
+                        const float g = gs[d] * P.grad_scale;
+                        const float mm = fmaf(P.beta1, A.m[p * D + d], (1.f - P.beta1) * g);
+                        const float vv = fmaf(P.beta2, A.v[p * D + d], (1.f - P.beta2) * g * g);
+                        if (active) { A.m[p * D + d] = mm; A.v[p * D + d] = vv; }
+                        const float mh = mm / bc1;
+                        const float vh = vv / bc2;
+                        const float xn = xs[d] - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
+                        xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+
+    if (MODE == MODE_OPT && active) {
+        for (int d = gl; d < D; d += kGroup) A.x[p * D + d] = xs[d];
+        if (KM > 0) {
+#pragma unroll
+            for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
+                const int d = gl + kGroup * k;
+                if (d < D) { A.m[p * D + d] = mreg[k]; A.v[p * D + d] = vreg[k]; }
+            }
+        }
+        if (gl == 0) A.invalid[p] = invalid ? 1 : 0;
+    }
+    if (MODE == MODE_CHECK) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x)
+            if (s_counts[i]) atomicAdd(&A.out_counts[i], s_counts[i]);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// K1: particle initialisation (Philox4x32-10, Salmon et al. SC'11)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ void uniform4(uint64_t seed, uint64_t gidx, int var, int block, float u[4]) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)var, (uint32_t)block),
+                                  make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+    const float s = 1.0f / 16777216.0f;
+    u[0] = (float)(w.x >> 8) * s; u[1] = (float)(w.y >> 8) * s;
+    u[2] = (float)(w.z >> 8) * s; u[3] = (float)(w.w >> 8) * s;
+}
+
+__global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleProgram SP, float* __restrict__ x,
+                                                float* __restrict__ grasp, int64_t n, int64_t gofs, uint64_t seed) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t gidx = (uint64_t)(gofs + i);
+    float* xi = x + i * SP.D;
+    for (int vi = 0; vi < SP.n_vars; ++vi) {
+        const KSVar& V = SP.v[vi];
+        float u[8];
+        if (V.kind == KS_GRASP) {       // top-down grasp: Trans(gx, gy, gz) Rz(gamma) Rx(pi)
+            uniform4(seed, gidx, V.var_id, 0, u);
+            const float gxy = V.a[0];
+            const float gx = -gxy + 2.f * gxy * u[0];
+            const float gy = -gxy + 2.f * gxy * u[1];
+            const float gamma = -kPi + 2.f * kPi * u[2];
+            float s, c;
+            sincosf(gamma, &s, &c);
+            float* g = grasp + (i * SP.n_grasp + V.slot) * 12;
+            g[0] = c;   g[1] = s;   g[2] = 0.f;  g[3] = gx;
+            g[4] = s;   g[5] = -c;  g[6] = 0.f;  g[7] = gy;
+            g[8] = 0.f; g[9] = 0.f; g[10] = -1.f; g[11] = V.a[1];
+        } else if (V.kind == KS_PLACEMENT) {   // uniform on the surface region shrunk by the footprint
+            uniform4(seed, gidx, V.var_id, 0, u);
+            // a = [region lo x, lo y, hi x, hi y, footprint, frame x, frame y, frame z_top, frame yaw]
+            const float wx = fmaxf(V.a[2] - V.a[0] - 2.f * V.a[4], 0.f);
+            const float wy = fmaxf(V.a[3] - V.a[1] - 2.f * V.a[4], 0.f);
+            const float lx = (V.a[0] + V.a[2]) / 2.f - wx / 2.f + u[0] * wx;
+            const float ly = (V.a[1] + V.a[3]) / 2.f - wy / 2.f + u[1] * wy;
+            const float lyaw = -kPi + 2.f * kPi * u[2];
+            const float fyaw = V.a[8];
+            float s, c;
+            sincosf(fyaw, &s, &c);
+            xi[V.xoff + 0] = V.a[5] + c * lx - s * ly;
+            xi[V.xoff + 1] = V.a[6] + s * lx + c * ly;
+            xi[V.xoff + 2] = V.a[7];
+            xi[V.xoff + 3] = fyaw + lyaw;
+        } else if (V.kind == KS_CONF) {        // uniform within joint limits
+            uniform4(seed, gidx, V.var_id, 0, u);
+            uniform4(seed, gidx, V.var_id, 1, u + 4);
+#pragma unroll
+            for (int j = 0; j < TAMP_NJ; ++j) xi[V.xoff + j] = SP.jlo[j] + u[j] * (SP.jhi[j] - SP.jlo[j]);
+        }
+    }
+    // knots: linear interpolation between the motion's endpoint confs
+    for (int vi = 0; vi < SP.n_vars; ++vi) {
+        const KSVar& V = SP.v[vi];
+        if (V.kind != KS_TRAJ) continue;
+        for (int j = 0; j < V.n_knots; ++j) {
+            const float a = (float)(j + 1) / (float)(V.n_knots + 1);
+            for (int d = 0; d < TAMP_NJ; ++d) {
+                const float qa = V.q1_xoff >= 0 ? xi[V.q1_xoff + d] : SP.const_conf[V.q1_const][d];
+                const float qb = V.q2_xoff >= 0 ? xi[V.q2_xoff + d] : SP.const_conf[V.q2_const][d];
+                xi[V.xoff + 7 * j + d] = qa + a * (qb - qa);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// K4 / K5: best-k (key = class | ordered cost | global index)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ordered_bits(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ unsigned long long make_key(int cls, float cost, int64_t gidx) {
+    return ((unsigned long long)(cls & 3) << 62) | ((unsigned long long)ordered_bits(cost) << 30) |
+           ((unsigned long long)gidx & ((1ull << 30) - 1));
+}
+
+constexpr int kSortChunk = 2048;
+
+// keys from the check pass (payload = local particle index)
+__global__ void k_make_keys(const uint8_t* __restrict__ cls, const float* __restrict__ cost, int64_t n, int64_t gofs,
+                            unsigned long long* __restrict__ keys, int32_t* __restrict__ pay) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = make_key(cls[i], cost[i], gofs + i);
+    pay[i] = (int32_t)i;
+}
+
+// keys from gathered records [class, cost, gidx_lo, gidx_hi, x...] (payload = record row)
+__global__ void k_record_keys(const float* __restrict__ rec, int32_t n, int32_t width,
+                              unsigned long long* __restrict__ keys, int32_t* __restrict__ pay) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* r = rec + (int64_t)i * width;
+    const int64_t gidx = (int64_t)(uint32_t)__float_as_int(r[2]) | ((int64_t)__float_as_int(r[3]) << 32);
+    keys[i] = make_key((int)r[0], r[1], gidx);
+    pay[i] = i;
+}
+
+// Sort each chunk of kSortChunk (key, payload) pairs ascending and keep its first k.
+__global__ void __launch_bounds__(1024) k_sort_chunk(const unsigned long long* __restrict__ kin, const int32_t* __restrict__ pin,
+                                                     int64_t n, int k, unsigned long long* __restrict__ kout,
+                                                     int32_t* __restrict__ pout) {
+    __shared__ unsigned long long sk[kSortChunk];
+    __shared__ int32_t sp[kSortChunk];
+    const int64_t base = (int64_t)blockIdx.x * kSortChunk;
+    for (int i = threadIdx.x; i < kSortChunk; i += blockDim.x) {
+        const int64_t g = base + i;
+        sk[i] = g < n ? kin[g] : ~0ull;
+        sp[i] = g < n ? pin[g] : -1;
+    }
+    __syncthreads();
+    for (int size = 2; size <= kSortChunk; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < kSortChunk / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const unsigned long long a = sk[lo], b = sk[hi];
+                if ((a > b) == up) {
+                    sk[lo] = b; sk[hi] = a;
+                    const int32_t t = sp[lo]; sp[lo] = sp[hi]; sp[hi] = t;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        kout[(int64_t)blockIdx.x * k + i] = sk[i];
+        pout[(int64_t)blockIdx.x * k + i] = sp[i];
+    }
+}
+
+__global__ void k_gather_particles(const int32_t* __restrict__ pay, const unsigned long long* __restrict__ keys, int k,
+                                   const float* __restrict__ x, const float* __restrict__ cost, int D, int64_t gofs,
+                                   float* __restrict__ rec) {
+    const int r = blockIdx.x;
+    if (r >= k) return;
+    const int32_t i = pay[r];
+    float* o = rec + (int64_t)r * (D + 4);
+    if (threadIdx.x == 0) {
+        const int64_t gidx = gofs + i;
+        o[0] = (float)(int)(keys[r] >> 62);
+        o[1] = cost[i];
+        o[2] = __int_as_float((int32_t)(uint32_t)(gidx & 0xffffffffll));
+        o[3] = __int_as_float((int32_t)(gidx >> 32));
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x) o[4 + d] = x[(int64_t)i * D + d];
+}
+
+__global__ void k_gather_records(const int32_t* __restrict__ pay, int k, const float* __restrict__ rin, int width,
+                                 float* __restrict__ rout) {
+    const int r = blockIdx.x;
+    if (r >= k) return;
+    const float* s = rin + (int64_t)pay[r] * width;
+    for (int d = threadIdx.x; d < width; d += blockDim.x) rout[(int64_t)r * width + d] = s[d];
+}
+
+// ------------------------------------------------------------------------------------------------
+// launchers (called from tamp_api.cu)
+// ------------------------------------------------------------------------------------------------
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launch_count() { return g_launches.load(); }
+static inline void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static int km_bucket(int D) { return D <= 24 ? 3 : D <= 56 ? 7 : D <= 72 ? 9 : 0; }
+
+template <int MODE, int KM>
+static cudaError_t launch_particle_km(const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
+    auto fn = k_particle<MODE, KM>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int per_block = 128 / kGroup;
+    const int64_t blocks = (A.n + per_block - 1) / per_block;
+    fn<<<(unsigned)blocks, 128, smem, st>>>(P, A);
+    counted();
+    return cudaGetLastError();
+}
+
+template <int MODE>
+static cudaError_t launch_particle_mode(const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
+    if constexpr (MODE != MODE_OPT) {
+        return launch_particle_km<MODE, 1>(P, A, smem, st);
+    } else {
+        switch (km_bucket(P.D)) {
+            case 3: return launch_particle_km<MODE, 3>(P, A, smem, st);
+            case 7: return launch_particle_km<MODE, 7>(P, A, smem, st);
+            case 9: return launch_particle_km<MODE, 9>(P, A, smem, st);
+            default: return launch_particle_km<MODE, 0>(P, A, smem, st);
+        }
+    }
+}
+
+cudaError_t launch_particle(int mode, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
+    if (A.n <= 0) return cudaSuccess;
+    if (mode == MODE_OPT) return launch_particle_mode<MODE_OPT>(P, A, smem, st);
+    if (mode == MODE_EVAL) return launch_particle_mode<MODE_EVAL>(P, A, smem, st);
+    return launch_particle_mode<MODE_CHECK>(P, A, smem, st);
+}
+
+cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
+                          cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_sample<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(SP, x, grasp, n, gofs, seed);
+    counted();
+    return cudaGetLastError();
+}
+
+// top-k of n (key, payload) pairs in ka/pa (ping-pong with kb/pb).  Returns pointers to the result.
+cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
+                        cudaStream_t st, unsigned long long** kres, int32_t** pres) {
+    unsigned long long *ki = ka, *ko = kb;
+    int32_t *pi = pa, *po = pb;
+    int64_t cnt = n;
+    do {
+        const int64_t chunks = (cnt + kSortChunk - 1) / kSortChunk;
+        const int keep = (int)(cnt < k ? cnt : k);
+        k_sort_chunk<<<(unsigned)chunks, 1024, 0, st>>>(ki, pi, cnt, keep, ko, po);
+    counted();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        cnt = chunks * keep;
+        unsigned long long* t = ki; ki = ko; ko = t;
+        int32_t* u = pi; pi = po; po = u;
+        if (chunks == 1) break;
+    } while (true);
+    *kres = ki;
+    *pres = pi;
+    return cudaSuccess;
+}
+
+cudaError_t launch_make_keys(const uint8_t* cls, const float* cost, int64_t n, int64_t gofs, unsigned long long* keys,
+                             int32_t* pay, cudaStream_t st) {
+    k_make_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cls, cost, n, gofs, keys, pay);
+    counted();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_record_keys(const float* rec, int32_t n, int32_t width, unsigned long long* keys, int32_t* pay,
+                               cudaStream_t st) {
+    k_record_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rec, n, width, keys, pay);
+    counted();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_particles(const int32_t* pay, const unsigned long long* keys, int k, const float* x,
+                                    const float* cost, int D, int64_t gofs, float* rec, cudaStream_t st) {
+    k_gather_particles<<<k, 128, 0, st>>>(pay, keys, k, x, cost, D, gofs, rec);
+    counted();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_records(const int32_t* pay, int k, const float* rin, int width, float* rout, cudaStream_t st) {
+    k_gather_records<<<k, 128, 0, st>>>(pay, k, rin, width, rout);
+    counted();
+    return cudaGetLastError();
+}
+
+}  // namespace tamp

@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on identical seeded inputs.
+
+Sizes span several 16-particle blocks and a ragged tail (N = 97, 301) at the oracle's speed; the
+full-size case (config 2 at N = 8192, bench launch configuration) compares sampled particles that the
+oracle recomputes one by one (particles never couple)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import tamp_oracle as O
+from paper_2411_11833_b200 import TampContext, decode_records
+from paper_2411_11833_b200 import build as b
+from workloads import make_config
+
+from parity_utils import (COST_ATOL, COST_RTOL, STEP_RTOL, grad_ok, kink_mask, oracle_inputs, to_ctx_grasp)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    b.build()
+    torch.cuda.set_device(0)
+
+
+def _ctx(spec, n, x32, g32, gofs=0, n_global=None):
+    ctx = TampContext(spec, n, global_offset=gofs, n_global=n_global)
+    ctx.set_state(torch.from_numpy(x32).cuda(), grasp=to_ctx_grasp(g32).cuda())
+    return ctx
+
+
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_sampler_matches_oracle(cfg):
+    """K1 (Philox + samplers) vs the oracle's InitializeParticles; ragged N, nonzero global offset."""
+    n, gofs = 301, 1000
+    spec = make_config(cfg, n=n)
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, n, global_offset=gofs, n_global=4096)
+    ctx.sample(seed=77 + cfg)
+    st = ctx.get_state()
+    torch.cuda.synchronize()
+    x0, g0 = O.initialize_particles(spec, csp, 77 + cfg, np.arange(gofs, gofs + n))
+    np.testing.assert_allclose(st["x"].cpu().numpy(), x0, rtol=2e-6, atol=2e-6)
+    np.testing.assert_allclose(st["grasp"].cpu().numpy(), g0.reshape(n, -1, 12), rtol=0, atol=2e-6)
+    assert int(st["invalid"].sum()) == 0 and st["t"] == 0
+    assert float(st["m"].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_cost_and_gradient_match_oracle(cfg):
+    n = 97 if cfg != 4 else 40
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=10 + cfg)
+    ctx = _ctx(spec, n, x32, g32)
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(soft, softo, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    ok = grad_ok(grad, grado)
+    if not ok.all():
+        kinks = kink_mask(spec, csp, x32.astype(np.float64), g32.astype(np.float64), grado, np.random.default_rng(0))
+        assert np.all(ok | kinks), f"gradient mismatch on smooth particles {np.where(~ok & ~kinks)[0]}"
+        assert kinks.mean() < 0.1
+    assert ok.mean() > 0.85
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_one_adam_step_matches_oracle(cfg):
+    n = 97 if cfg != 4 else 40
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=20 + cfg)
+    ctx = _ctx(spec, n, x32, g32, n_global=1000)
+    ctx.optimize(1)
+    st = ctx.get_state()
+    x1 = st["x"].cpu().numpy()
+    so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
+    _, _, _, g0 = O.cost_and_grad(spec, csp, so.x, so.grasps)
+    O.optimize(spec, csp, so, 1, 1.0 / 1000)
+    tol = STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
+    close = np.abs(x1 - so.x) <= tol
+    # sign-unstable coordinates (|g| tiny relative to the particle's gradient) are reported, not failed
+    unstable = np.abs(g0) < 1e-4 * np.abs(g0).max(axis=1, keepdims=True)
+    kinks = kink_mask(spec, csp, x32.astype(np.float64), g32.astype(np.float64), g0, np.random.default_rng(1))
+    bad = ~close & ~unstable & ~kinks[:, None]
+    assert not bad.any(), f"{bad.sum()} coordinates differ after one step"
+    assert st["t"] == 1
+    # frozen grasps are bit-identical
+    assert np.array_equal(st["grasp"].cpu().numpy(), g32.reshape(n, -1, 12))
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_check_counts_and_classes_match_oracle(cfg):
+    n = 301
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=30 + cfg)
+    ctx = _ctx(spec, n, x32, g32)
+    cls = torch.empty(n, dtype=torch.uint8, device="cuda")
+    counts, _ = ctx.check(cls=cls)
+    counts = counts.cpu().numpy()
+    so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
+    cls_o, counts_o, J, soft, Jc = O.check(spec, csp, so)
+    eps = np.array([spec.eps[t.kind] for t in csp.terms])
+    # epsilon-marginal residuals (the only place fp32 vs fp64 may decide differently); exact zeros of
+    # clamped terms (JL = 0 = eps_JL) are computed exactly on both sides and are not marginal
+    marginal = (np.abs(Jc - eps[None, :]) <= 1e-4 * eps[None, :] + 1e-6) & (Jc > 0)
+    assert marginal.sum() == 0, "epsilon-marginal particles in a seeded test"
+    np.testing.assert_array_equal(cls.cpu().numpy(), cls_o)
+    np.testing.assert_array_equal(counts, counts_o)
+
+
+def test_constructed_satisfying_particles_are_class0():
+    """Hand-constructed satisfying particles (SURVEY §8(c) whole-step pin) are satisfying on the GPU too,
+    hinge/bounds terms exactly 0 with zero gradient."""
+    from test_oracle_csp import _clear_pickplace, satisfying_particle
+    spec = _clear_pickplace()
+    csp = O.build_csp(spec)
+    rng = np.random.default_rng(3)
+    xs, gs = zip(*[satisfying_particle(spec, csp, rng) for _ in range(20)])
+    x32 = np.array(xs, np.float32)
+    g32 = np.array(gs, np.float32)[:, None]
+    ctx = _ctx(spec, 20, x32, g32)
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    cls = torch.empty(20, dtype=torch.uint8, device="cuda")
+    counts, _ = ctx.check(cls=cls)
+    assert np.all(cls.cpu().numpy() == 0)
+    assert np.all(Jc[:, [0, 1, 4, 5, 8, 9, 10]] == 0.0)
+    assert np.all(Jc <= 1e-5)
+
+
+def test_best_k_exact_on_gpu_costs_and_oracle_order():
+    cfg, n, k = 2, 301, 16
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=40)
+    gofs = 5000
+    ctx = _ctx(spec, n, x32, g32, gofs=gofs, n_global=8192)
+    rec = ctx.best_k(k)
+    cls, cost, gidx, xk = decode_records(rec)
+    # exact against selection on the GPU's own (class, cost) arrays
+    clsg = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ctx.check(cls=clsg)
+    J, soft, _, _ = ctx.eval()
+    c = clsg.cpu().numpy()
+    costg = np.where(c == 0, soft.cpu().numpy(), np.where(c == 1, J.cpu().numpy(), 0.0)).astype(np.float32)
+    order = np.lexsort((np.arange(n), costg, c))[:k]
+    np.testing.assert_array_equal(gidx, order + gofs)
+    np.testing.assert_array_equal(xk, x32[order])
+    # oracle selection agrees where neighbouring keys are separated by more than the cost tolerance
+    so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
+    cls_o, _, Jo, softo, _ = O.check(spec, csp, so)
+    sel_o, _, cost_o = O.best_k(cls_o, Jo, softo, np.arange(n) + gofs, k)
+    sep = np.diff(np.sort(cost_o)) > 1e-3 * np.abs(cost_o[1:])
+    if sep.all():
+        np.testing.assert_array_equal(gidx, sel_o + gofs)
+
+
+def test_merge_best_k_equals_global_best_k():
+    """all-gather emulation: per-rank best-k records merged == best-k over the union."""
+    cfg, n, k = 1, 256, 8
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=50)
+    full = _ctx(spec, n, x32, g32, n_global=n)
+    ref = full.best_k(k)
+    parts = []
+    for r in range(4):
+        sl = slice(64 * r, 64 * (r + 1))
+        c = _ctx(spec, 64, np.ascontiguousarray(x32[sl]), np.ascontiguousarray(g32[sl]), gofs=64 * r, n_global=n)
+        parts.append(c.best_k(k))
+    merged = full.merge_best_k(torch.cat(parts), k)
+    np.testing.assert_array_equal(merged.cpu().numpy(), ref.cpu().numpy())
+
+
+def test_sharding_invariance_bit_exact():
+    """Per-particle state after T steps is bit-identical for 1 context vs 2 shards."""
+    spec = make_config(2, n=200)
+    one = TampContext(spec, 200, 0, 200)
+    one.sample(seed=9)
+    one.optimize(5)
+    a = TampContext(spec, 120, 0, 200)
+    b2 = TampContext(spec, 80, 120, 200)
+    for c in (a, b2):
+        c.sample(seed=9)
+        c.optimize(3)
+        c.optimize(2)
+    x = one.get_state()["x"].cpu().numpy()
+    xs = np.concatenate([a.get_state()["x"].cpu().numpy(), b2.get_state()["x"].cpu().numpy()])
+    assert np.array_equal(x, xs)
+
+
+def test_determinism_and_particle_independence():
+    spec = make_config(3, n=64)
+    r = []
+    for _ in range(2):
+        c = TampContext(spec, 64)
+        c.sample(seed=4)
+        c.optimize(3)
+        r.append(c.get_state()["x"].cpu().numpy())
+    assert np.array_equal(r[0], r[1])
+    # permuting particles permutes results exactly
+    st = c.get_state()
+    perm = np.random.default_rng(0).permutation(64)
+    c2 = TampContext(spec, 64)
+    c2.set_state(st["x"][perm], grasp=st["grasp"][perm], m=st["m"][perm], v=st["v"][perm], t=st["t"])
+    c.optimize(1)
+    c2.optimize(1)
+    assert np.array_equal(c.get_state()["x"].cpu().numpy()[perm], c2.get_state()["x"].cpu().numpy())
+
+
+def test_invalid_particles_are_sticky():
+    spec, csp, x32, g32 = oracle_inputs(1, 32, seed=60)
+    x32 = x32.copy()
+    x32[5, 2] = np.nan
+    ctx = _ctx(spec, 32, x32, g32)
+    ctx.optimize(2)
+    st = ctx.get_state()
+    inv = st["invalid"].cpu().numpy()
+    assert inv[5] == 1 and inv.sum() == 1
+    xn = st["x"].cpu().numpy()
+    assert np.isnan(xn[5, 2]) and np.array_equal(xn[5, 3:], x32[5, 3:])
+    cls = torch.empty(32, dtype=torch.uint8, device="cuda")
+    counts, _ = ctx.check(cls=cls)
+    assert cls.cpu().numpy()[5] == 2 and counts.cpu().numpy()[-1] == 1
+
+
+def test_host_buffers_through_the_c_abi():
+    """check / best_k / get / set accept host buffers (pinned and pageable) with identical results."""
+    spec, csp, x32, g32 = oracle_inputs(2, 64, seed=70)
+    ctx = TampContext(spec, 64)
+    ctx.set_state(torch.from_numpy(x32), grasp=to_ctx_grasp(g32))          # pageable host input
+    d_counts, _ = ctx.check()
+    h_counts = torch.zeros(ctx.n_hard + 2, dtype=torch.int32).pin_memory()
+    ctx.check(counts=h_counts)
+    assert torch.equal(d_counts.cpu(), h_counts)
+    d_rec = ctx.best_k(4)
+    h_rec = torch.empty(4, ctx.D + 4)
+    ctx.best_k(4, out=h_rec)
+    assert torch.equal(d_rec.cpu(), h_rec)
+    assert np.array_equal(ctx.get_state()["x"].cpu().numpy(), x32)
+
+
+def test_full_size_bench_config_sampled_against_oracle():
+    """Config 2 at its BASELINE size (8192 particles) in bench's launch configuration: sample + 1 fused
+    step; 48 sampled particles recomputed by the oracle one by one from the GPU-independent start."""
+    cfg, n = 2, 8192
+    spec = make_config(cfg, n=n)
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, n)
+    ctx.sample(seed=2000)
+    st0 = ctx.get_state()
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    ctx.optimize(1)
+    x1 = ctx.get_state()["x"].cpu().numpy()
+    idx = np.sort(np.random.default_rng(5).choice(n, 48, replace=False))
+    x0o, g0o = O.initialize_particles(spec, csp, 2000, idx)
+    np.testing.assert_allclose(st0["x"].cpu().numpy()[idx], x0o, rtol=2e-6, atol=2e-6)
+    x32 = st0["x"].cpu().numpy()[idx].astype(np.float64)
+    g32 = st0["grasp"].cpu().numpy()[idx].reshape(len(idx), -1, 3, 4).astype(np.float64)
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32, g32)
+    np.testing.assert_allclose(J[idx], Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(Jc[idx], Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    ok = grad_ok(grad[idx], grado)
+    kinks = kink_mask(spec, csp, x32, g32, grado, np.random.default_rng(2))
+    assert np.all(ok | kinks)
+    so = O.new_state(x32, g32)
+    O.optimize(spec, csp, so, 1, 1.0 / n)
+    unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
+    close = np.abs(x1[idx] - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
+    assert np.all(close | unstable | kinks[:, None])
+
+
+def test_edge_sizes():
+    """N = 1 (a lone particle in a 16-particle block) and k = N."""
+    spec, csp, x32, g32 = oracle_inputs(1, 1, seed=80)
+    ctx = _ctx(spec, 1, x32, g32)
+    J, _, _, _ = ctx.eval()
+    Jo, _, _, _ = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    np.testing.assert_allclose(J.cpu().numpy(), Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    rec = ctx.best_k(1)
+    assert decode_records(rec)[2][0] == 0
+    ctx.optimize(3)
+    assert ctx.t == 3

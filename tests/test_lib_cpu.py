@@ -1,0 +1,88 @@
+"""CPU-side checks of the C ABI library: it builds/loads, exports every symbol include/tamp.h declares,
+the ctypes layout matches, and the host-side skeleton compiler accepts the five configs and rejects bad
+descriptors (no GPU needed: tamp_query_workspace only compiles)."""
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+import paper_2411_11833_b200 as pkg
+from paper_2411_11833_b200 import build as b
+from paper_2411_11833_b200 import tamp as T
+from workloads import make_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    b.build()
+    return pkg.load()
+
+
+def test_exports_every_declared_symbol(lib):
+    hdr = open(os.path.join(ROOT, "include", "tamp.h")).read()
+    declared = set(re.findall(r"\b(tamp_[a-z_0-9]+)\s*\(", hdr))
+    assert len(declared) >= 15
+    cdll = ctypes.CDLL(T.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(cdll, name), f"libtamp.so does not export {name}"
+    assert set(T.EXPORTS) <= declared
+
+
+def test_struct_layout_matches(lib):
+    assert lib.tamp_sizeof_desc() == ctypes.sizeof(T.ProblemDesc)
+    assert lib.tamp_sizeof_info() == ctypes.sizeof(T.Info)
+    assert lib.tamp_abi_version() == T.ABI_VERSION
+
+
+def _query(lib, desc, n):
+    nb = ctypes.c_size_t()
+    st = lib.tamp_query_workspace(ctypes.byref(desc), n, ctypes.byref(nb))
+    return st, nb.value, lib.tamp_last_error().decode()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_compiler_accepts_configs(lib, cfg):
+    spec = make_config(cfg, n=16)
+    st, nb, msg = _query(lib, T.build_desc(spec), 1000)
+    assert st == 0, msg
+    assert nb > 1000 * 3 * 4
+
+
+def test_compiler_rejects_bad_descriptors(lib):
+    spec = make_config(1, n=4)
+    d = T.build_desc(spec)
+    d.robot.joint_lo[2] = d.robot.joint_hi[2] + 1
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "joint_lo" in msg
+    d = T.build_desc(spec)
+    d.lam[3] = 0.0
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "lambda" in msg
+    d = T.build_desc(spec)
+    d.obb[0].half[1] = -1
+    assert _query(lib, d, 10)[0] == 1
+    d = T.build_desc(spec)
+    d.abi_version = 99
+    assert _query(lib, d, 10)[0] == 1
+    d = T.build_desc(spec)
+    d.action[1].placement = d.action[3].placement      # Pick from a placement the object is not at
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "Pick" in msg
+    d = T.build_desc(spec)
+    d.robot.n_spheres = 33
+    assert _query(lib, d, 10)[0] == 5
+    assert _query(lib, T.build_desc(spec), 0)[0] == 1
+
+
+def test_product_path_fails_loudly_without_library(tmp_path):
+    with pytest.raises(RuntimeError):
+        T._lib_backup = T._lib
+        T._lib = None
+        try:
+            T.load(str(tmp_path / "missing.so"))
+        finally:
+            T._lib = T._lib_backup

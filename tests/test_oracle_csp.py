@@ -138,12 +138,13 @@ def test_eq3_boundary_semantics_and_weight_scaling():
     csp = O.build_csp(spec)
     x, Tg = satisfying_particle(spec, csp, np.random.default_rng(10))
     st = O.new_state(x[None], Tg[None, None])
-    spec.surfaces[0].frame[2] = -0.01             # |z_bottom - z_top| = |0 - (-0.01)| = eps_SS exactly
+    e_ss = spec.eps["SS"]                         # 1 cm (as float32, like every spec constant)
+    spec.surfaces[0].frame[2] = -e_ss             # |z_bottom - z_top| = |0 - (-eps)| = eps_SS exactly
     cls, counts, J, soft, Jc = O.check(spec, csp, st)
-    assert Jc[0, 8] == 0.01
+    assert Jc[0, 8] == e_ss and abs(e_ss - 0.01) < 1e-9
     assert cls[0] == 0 and counts[8] == 1
     spec_b = copy.deepcopy(spec)
-    spec_b.surfaces[0].frame[2] = -0.01 - 1e-9
+    spec_b.surfaces[0].frame[2] = -e_ss - 1e-9
     cls_b, counts_b, *_ = O.check(spec_b, csp, st)
     assert cls_b[0] == 1 and counts_b[8] == 0
     spec2 = copy.deepcopy(spec)
@@ -263,7 +264,7 @@ def test_adam_first_step_closed_form_and_zero_gradient():
     st = O.new_state(np.zeros((1, 5)), np.zeros((1, 0, 3, 4)))
     g = np.array([[1.0, -2.0, 1e-3, 0.0, 1e-9]])
     O.adam_update(spec, csp, st, g)
-    np.testing.assert_allclose(st.x[0], -0.01 * g[0] / (np.abs(g[0]) + 1e-8), rtol=1e-12, atol=1e-18)
+    np.testing.assert_allclose(st.x[0], -0.01 * g[0] / (np.abs(g[0]) + spec.adam_eps), rtol=1e-12, atol=1e-18)
     assert st.x[0, 3] == 0.0
 
 
@@ -274,7 +275,7 @@ def test_adam_matches_torch_optim_adam():
     x0 = rng.normal(size=(3, 7))
     st = O.new_state(x0, np.zeros((3, 0, 3, 4)))
     p = torch.nn.Parameter(torch.tensor(x0, dtype=DT))
-    opt = torch.optim.Adam([p], lr=0.03, betas=(0.9, 0.999), eps=1e-8)
+    opt = torch.optim.Adam([p], lr=0.03, betas=(spec.beta1, spec.beta2), eps=spec.adam_eps)
     for _ in range(50):
         g = rng.normal(size=(3, 7))
         O.adam_update(spec, csp, st, g)

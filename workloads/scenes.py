@@ -341,16 +341,40 @@ CONFIG_NAMES = {1: "pickplace", 2: "obstruction", 3: "tetris4_goal", 4: "tetris6
 CONFIG_SIZES = {1: 256, 2: 8192, 3: 32768, 4: 131072, 5: 1 << 20}
 
 
+def _f32(obj):
+    """Round every float constant to the nearest float32 (in place; ints/bools untouched).
+
+    The CUDA path receives the problem in float32; rounding the shared spec once makes the oracle
+    (float64 arithmetic) and the kernels (float32) solve exactly the same problem instance.
+    """
+    if isinstance(obj, list):
+        return [_f32(o) for o in obj]
+    if isinstance(obj, dict):
+        return {k: _f32(v) for k, v in obj.items()}
+    if isinstance(obj, np.ndarray):
+        return obj.astype(np.float32).astype(np.float64) if obj.dtype.kind == "f" else obj
+    if isinstance(obj, float):
+        return float(np.float32(obj))
+    if dataclasses.is_dataclass(obj):
+        for f in dataclasses.fields(obj):
+            setattr(obj, f.name, _f32(getattr(obj, f.name)))
+        return obj
+    return obj
+
+
 def make_config(cfg: int, n: Optional[int] = None, steps: int = 100) -> ProblemSpec:
+    """ProblemSpec of BASELINE.json config `cfg` (1-5) with all float constants float32-representable."""
     n = CONFIG_SIZES[cfg] if n is None else n
     if cfg == 1:
-        return config_pickplace(n, steps)
-    if cfg == 2:
-        return config_obstruction(n, steps)
-    if cfg == 3:
-        return config_tetris4(n, steps, goal=True)
-    if cfg == 4:
-        return config_tetris6_knots(n, steps)
-    if cfg == 5:
-        return config_tetris4(n, steps, goal=False)
-    raise ValueError(cfg)
+        spec = config_pickplace(n, steps)
+    elif cfg == 2:
+        spec = config_obstruction(n, steps)
+    elif cfg == 3:
+        spec = config_tetris4(n, steps, goal=True)
+    elif cfg == 4:
+        spec = config_tetris6_knots(n, steps)
+    elif cfg == 5:
+        spec = config_tetris4(n, steps, goal=False)
+    else:
+        raise ValueError(cfg)
+    return _f32(spec)
