@@ -26,7 +26,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from workloads import make_config, CONFIG_NAMES  # noqa: E402
+from workloads import make_config, CONFIG_NAMES, CONFIG_SIZES  # noqa: E402
 
 METRIC = "particle-steps/sec (cost+grad+update)"
 UNIT = "particle-steps/s"
@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-ttfs", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--lanes", type=int, default=0, help="lanes per particle in the particle kernel (0 = auto)")
     return p.parse_args()
 
 
@@ -303,12 +304,12 @@ def main():
     torch.cuda.set_device(dev)
     torch.set_num_threads(1)
     cfg = args.config
-    n = args.n or (make_config(cfg, n=1).n_particles if cfg != 5 else 1 << 20)
+    n = args.n or CONFIG_SIZES[cfg]
     if cfg == 4 and args.n is None:
         n = 131072 // 8                              # config 4: 128K particles over 8 GPUs (per-rank share)
     spec = make_config(cfg, n=n)
     n_global = n * world
-    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev)
+    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
     for w in range(args.warmup):
         run_round(ctx, 10_000 + w, args, dist, world)
@@ -363,7 +364,8 @@ def main():
         host_counts = torch.zeros(ctx.n_hard + 2, dtype=torch.int32).pin_memory()
         host_rec = torch.zeros(args.k, ctx.D + 4, dtype=torch.float32).pin_memory()
         for w_ in range(2):
-            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev)
+            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
+                             lanes_per_particle=args.lanes)
             run_round(c2, 30_000 + w_, args, dist, world, host_counts=host_counts, host_rec=host_rec)
         torch.cuda.synchronize()
         if dist is not None:
@@ -371,7 +373,8 @@ def main():
         t0 = time.perf_counter()
         e2e_steps = max(3, min(args.steps, 10))
         for s in range(e2e_steps):
-            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev)  # host descriptor in
+            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
+                             lanes_per_particle=args.lanes)                 # host descriptor in
             run_round(c2, 40_000 + s, args, dist, world, host_counts=host_counts, host_rec=host_rec)
         torch.cuda.synchronize()
         te = max_over_ranks(time.perf_counter() - t0, dist)
@@ -395,6 +398,7 @@ def main():
                            "particles_per_gpu": n, "particles_global": n_global, "D": ctx.D,
                            "hard_terms": ctx.n_hard, "adam_steps_per_step": args.adam_steps,
                            "check_every": args.check_every, "best_k": args.k, "l2": "flushed between steps",
+                           "lanes_per_particle": ctx.lanes_per_particle,
                            "parallelism": f"dp{world}"},
                 "kernel_ms_per_launch": opt_avg * 1e3, "kernel_steps_per_launch": args.check_every,
                 "kernel_particle_steps_per_s": n_global * args.check_every / opt_avg,

@@ -20,7 +20,7 @@
 #include "tamp_program.h"
 
 namespace tamp {
-cudaError_t launch_particle(int mode, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st);
+cudaError_t launch_particle(int mode, int gs, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st);
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
                           cudaStream_t st);
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
@@ -67,6 +67,7 @@ struct tamp_ctx {
     // shared-memory layout of the particle kernel (floats per particle)
     int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
     size_t smem = 0;
+    int gs = 8;                  // lanes per particle in the particle kernel
     int32_t t = 0;
     bool ready = false;
     int32_t term_kind[TAMP_MAX_TERMS];
@@ -481,10 +482,10 @@ static void smem_layout(tamp_ctx* c) {
     off += 16 * P.n_grasp;
     c->off_gTi = off;
     off += 16 * P.n_grasp;
-    // stride = 8 (mod 32) floats so the four particles of a warp hit distinct banks on broadcasts
+    // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
     int stride = ((off + 31) / 32) * 32 + 8;
     c->stride = stride;
-    c->smem = (size_t)16 * stride * sizeof(float);   // 16 particles per 128-thread block
+    c->smem = (size_t)(128 / c->gs) * stride * sizeof(float);   // 128-thread blocks
 }
 
 static void ws_layout(tamp_ctx* c) {
@@ -609,6 +610,13 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     c->pairs_sb = C.pairs_sb;
     c->pairs_ss = C.pairs_ss;
     c->n_robot_spheres = desc->robot.n_spheres;
+    if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 8 && desc->lanes_per_particle != 16) {
+        delete c;
+        return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 8 or 16");
+    }
+    // auto: 16 lanes (two per link frame) while there are fewer than ~220 particles per SM, so that small
+    // batches still put enough warps in flight; 8 lanes (one per link frame) for large batches
+    c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : (n_local < 32768 ? 16 : 8);
     ws_layout(c);
     smem_layout(c);
     if (ws_bytes < c->total) {
@@ -663,6 +671,7 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     out->n_goal_pairs = c->P.n_goal * (c->P.n_goal - 1) / 2;
     out->n_traj_seg = n_seg;
     out->n_robot_spheres = c->n_robot_spheres;
+    out->lanes_per_particle = c->gs;
     return TAMP_OK;
 }
 
@@ -688,7 +697,7 @@ tamp_status tamp_optimize_step(tamp_ctx* c, int32_t n_steps, void* stream) {
     KArgs A = base_args(c);
     A.n_steps = n_steps;
     A.t0 = c->t;
-    CUDA_TRY(launch_particle(MODE_OPT, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "optimize");
+    CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "optimize");
     c->t += n_steps;
     return TAMP_OK;
 }
@@ -699,7 +708,7 @@ static tamp_status run_check(tamp_ctx* c, cudaStream_t st) {
     A.out_cost = c->at<float>(c->o_cost);
     A.out_counts = c->at<int32_t>(c->o_counts);
     CUDA_TRY(cudaMemsetAsync(A.out_counts, 0, (TAMP_MAX_TERMS + 2) * 4, st), "check: zero counts");
-    CUDA_TRY(launch_particle(MODE_CHECK, c->P, A, c->smem, st), "check");
+    CUDA_TRY(launch_particle(MODE_CHECK, c->gs, c->P, A, c->smem, st), "check");
     return TAMP_OK;
 }
 
@@ -767,7 +776,7 @@ tamp_status tamp_eval(tamp_ctx* c, float* J, float* soft, float* Jc, float* grad
     A.out_soft = soft;
     A.out_Jc = Jc;
     A.out_grad = grad;
-    CUDA_TRY(launch_particle(MODE_EVAL, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "eval");
+    CUDA_TRY(launch_particle(MODE_EVAL, c->gs, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "eval");
     return TAMP_OK;
 }
 

@@ -92,11 +92,31 @@ __device__ __forceinline__ void xform(const M34& T, float x, float y, float z, f
     oz = fmaf(T.r[6], x, fmaf(T.r[7], y, fmaf(T.r[8], z, T.t[2])));
 }
 
-__device__ __forceinline__ float gsum(float v) {      // butterfly sum over the 8-lane group
-    v += __shfl_xor_sync(FULL, v, 1, kGroup);
-    v += __shfl_xor_sync(FULL, v, 2, kGroup);
-    v += __shfl_xor_sync(FULL, v, 4, kGroup);
+template <int GS>
+__device__ __forceinline__ float gsum(float v) {      // butterfly sum over the GS lanes of a particle group
+#pragma unroll
+    for (int m = 1; m < GS; m <<= 1) v += __shfl_xor_sync(FULL, v, m);
     return v;
+}
+
+// sin/cos without the large-argument (Payne-Hanek) path of sincosf: Cody-Waite reduction by pi/2 with a
+// three-part constant (exact for |x| < ~1e4; joint angles and yaws are within a few radians) and the
+// cephes single-precision minimax polynomials on [-pi/4, pi/4] (<= 2 ulp).  Branch-free and compact, so
+// the step loop's instruction footprint stays small.
+__device__ __forceinline__ void fsincos(float x, float* s, float* c) {
+    const float k = rintf(x * 0.636619772367581343f);
+    float r = fmaf(k, -1.57079601287841796875f, x);
+    r = fmaf(k, -3.13916473e-07f, r);
+    r = fmaf(k, -5.39030253e-15f, r);
+    const float r2 = r * r;
+    const float ps = fmaf(fmaf(fmaf(-1.9515295891e-4f, r2, 8.3321608736e-3f), r2, -1.6666654611e-1f), r2 * r, r);
+    const float pc = fmaf(fmaf(fmaf(fmaf(2.443315711809948e-5f, r2, -1.388731625493765e-3f), r2,
+                                    4.166664568298827e-2f), r2, -0.5f), r2, 1.0f);
+    const int q = (int)k;
+    const float sv = (q & 1) ? pc : ps;
+    const float cv = (q & 1) ? ps : pc;
+    *s = (q & 2) ? -sv : sv;
+    *c = ((q + 1) & 2) ? -cv : cv;
 }
 
 struct Wrench {
@@ -116,9 +136,10 @@ struct Wrench {
     __device__ __forceinline__ bool nonzero() const {
         return (f[0] != 0.f) | (f[1] != 0.f) | (f[2] != 0.f) | (m[0] != 0.f) | (m[1] != 0.f) | (m[2] != 0.f);
     }
+    template <int GS>
     __device__ __forceinline__ void group_sum() {
 #pragma unroll
-        for (int i = 0; i < 3; ++i) { f[i] = gsum(f[i]); m[i] = gsum(m[i]); }
+        for (int i = 0; i < 3; ++i) { f[i] = gsum<GS>(f[i]); m[i] = gsum<GS>(m[i]); }
     }
 };
 
@@ -173,7 +194,7 @@ __device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, flo
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float R = rr + b.w;
     ux = uy = uz = 0.f;
-    if (d2 >= R * R) return 0.f;
+    if (fmaf(-R, R, d2) >= 0.f) return 0.f;
     if (d2 > 0.f) {
         const float inv = rsqrtf(d2);
         const float pen = R - d2 * inv;
@@ -185,6 +206,86 @@ __device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, flo
         return pen;
     }
     return R;   // coincident centres: cost R, zero gradient (L13)
+}
+
+constexpr float kFar = 1e18f;   // position of padded (absent) spheres: never within reach of anything
+
+// NS query spheres per lane (registers) vs the 8 (padded) spheres of one object instance (shared memory,
+// broadcast to the group).  Fast path: branch-free test of all NS x 8 pairs (d^2 - (ra+rb)^2 < 0 ?), no
+// square roots; only if some pair of the warp is active are the hinges and gradients evaluated.
+// Returns the hinge sum; if GRAD accumulates dJ/dw_a (x lam) into g and the partner's wrench into pw.
+template <bool GRAD, int NS>
+__device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], const float (&rr)[NS], const float4* Bs,
+                                                   float lam, float (&g)[NS][3], Wrench& pw) {
+    float mn = 1.f;
+#pragma unroll
+    for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
+        const float4 B = Bs[b];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const float dx = w[k][0] - B.x, dy = w[k][1] - B.y, dz = w[k][2] - B.z;
+            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            const float R = rr[k] + B.w;
+            mn = fminf(mn, fmaf(-R, R, d2));
+        }
+    }
+    float j = 0.f;
+    if (__any_sync(FULL, mn < 0.f)) {
+#pragma unroll 1
+        for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
+            const float4 B = Bs[b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                float ux, uy, uz;
+                j += sphere_sphere<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, ux, uy, uz);
+                if (GRAD) {
+                    g[k][0] -= ux; g[k][1] -= uy; g[k][2] -= uz;
+                    pw.add_point(B.x, B.y, B.z, ux, uy, uz);
+                }
+            }
+        }
+    }
+    return j;
+}
+
+// NS query spheres per lane vs one OBB: branch-free reject (outside and |max(a,0)|^2 >= r^2), exact
+// hinge + gradient only if some sphere of the warp reaches the box.
+template <bool GRAD, int NS>
+__device__ __forceinline__ float spheres_vs_obb(const float (&w)[NS][3], const float (&rr)[NS], const KObb& B,
+                                                float lam, float (&g)[NS][3]) {
+    float mn = 1.f;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
+        const float px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
+        const float py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
+        const float pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
+        const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(pz) - B.h[2];
+        const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
+        const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+        const float mx = fmaxf(ax, fmaxf(ay, az));
+        mn = fminf(mn, mx > 0.f ? fmaf(-rr[k], rr[k], s) : -1.f);
+    }
+    float j = 0.f;
+    if (__any_sync(FULL, mn < 0.f)) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) j += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, g[k][0], g[k][1], g[k][2]);
+    }
+    return j;
+}
+
+__device__ __forceinline__ void add_wrench(float* dst, const Wrench& w) {
+    dst[0] += w.f[0]; dst[1] += w.f[1]; dst[2] += w.f[2];
+    dst[3] += w.m[0]; dst[4] += w.m[1]; dst[5] += w.m[2];
+}
+
+// reduce a per-lane partner wrench over the group and add it to the instance accumulator (lane 0)
+template <bool GRAD, int GS>
+__device__ __forceinline__ void flush_partner(Wrench& pw, bool movable, float* dst, int gl) {
+    if (GRAD && movable && __any_sync(FULL, pw.nonzero())) {
+        pw.template group_sum<GS>();
+        if (gl == 0) add_wrench(dst, pw);
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -209,17 +310,22 @@ __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, T
     }
 }
 
-// KM = register-resident Adam moments per lane (coords gl, gl+8, ...); 0 = moments stay in global memory
-template <int MODE, int KM>
-__global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
+// GS = lanes per particle: 8 (one per link frame) or 16 (two per link frame, each with half of the
+// link's spheres; more warps in flight for small particle counts).
+// KM = register-resident Adam moments per lane (coords gl, gl+GS, ...); 0 = moments stay in global memory
+template <int MODE, int KM, int GS>
+__global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     extern __shared__ float4 smem4[];
     __shared__ float4 s_osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES];
     __shared__ int s_counts[TAMP_MAX_TERMS + 2];
 
-    const int gl = threadIdx.x & (kGroup - 1);
-    const int grp = threadIdx.x / kGroup;
-    const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / kGroup) + grp;
+    constexpr int NS = TAMP_MAX_SPHERES_PER_LINK / (GS / kGroup);   // robot spheres per lane
+    const int gl = threadIdx.x & (GS - 1);          // lane within the particle group
+    const int ll = gl & (kGroup - 1);               // link frame owned by this lane
+    const int half = gl / kGroup;                   // which share of the link's spheres
+    const int grp = threadIdx.x / GS;
+    const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / GS) + grp;
     const bool active = pid < A.n;
     const int64_t p = active ? pid : (A.n - 1);
     float* S = reinterpret_cast<float*>(smem4) + (size_t)grp * A.stride;
@@ -239,35 +345,35 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
     if (MODE == MODE_CHECK)
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
 
-    // per-lane robot data: fixed transform of my joint (lane 7: tool) and my link's spheres
-    M34 F;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        F.r[3 * i] = P.F[gl][4 * i]; F.r[3 * i + 1] = P.F[gl][4 * i + 1];
-        F.r[3 * i + 2] = P.F[gl][4 * i + 2]; F.t[i] = P.F[gl][4 * i + 3];
+    // robot data in shared memory (read per FK instance instead of pinning ~28 registers): fixed transform
+    // of each joint (lane 7: tool) and each link's spheres
+    __shared__ float4 s_F[kGroup][3];
+    __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];
+    if (threadIdx.x < kGroup * 3) {
+        const int l = threadIdx.x / 3, r = threadIdx.x % 3;
+        s_F[l][r] = make_float4(P.F[l][4 * r], P.F[l][4 * r + 1], P.F[l][4 * r + 2], P.F[l][4 * r + 3]);
     }
-    float sph[TAMP_MAX_SPHERES_PER_LINK][4];
-    const int nsph = P.rsph_n[gl];
-#pragma unroll
-    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sph[k][c] = P.rsph[gl][k][c];
-    const float jlo = gl < TAMP_NJ ? P.jlo[gl] : 0.f;
-    const float jhi = gl < TAMP_NJ ? P.jhi[gl] : 0.f;
+    if (threadIdx.x < kGroup * TAMP_MAX_SPHERES_PER_LINK) {
+        const int l = threadIdx.x / TAMP_MAX_SPHERES_PER_LINK, k = threadIdx.x % TAMP_MAX_SPHERES_PER_LINK;
+        s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3]);
+    }
+    const int nsph = P.rsph_n[ll] - half * NS;      // my valid spheres (may be <= 0)
+    const float jlo = ll < TAMP_NJ ? P.jlo[ll] : 0.f;
+    const float jhi = ll < TAMP_NJ ? P.jhi[ll] : 0.f;
 
     // particle state -> shared memory / registers
     const float* xg = A.x + p * D;
-    for (int d = gl; d < D; d += kGroup) xs[d] = xg[d];
+    for (int d = gl; d < D; d += GS) xs[d] = xg[d];
     float mreg[KM > 0 ? KM : 1], vreg[KM > 0 ? KM : 1];
     if (MODE == MODE_OPT && KM > 0) {
 #pragma unroll
         for (int k = 0; k < KM; ++k) {
-            const int d = gl + kGroup * k;
+            const int d = gl + GS * k;
             mreg[k] = d < D ? A.m[p * D + d] : 0.f;
             vreg[k] = d < D ? A.v[p * D + d] : 0.f;
         }
     }
-    for (int i = gl; i < P.n_grasp * 12; i += kGroup) gT[(i / 12) * 16 + (i % 12)] = A.grasp[(p * P.n_grasp) * 12 + i];
+    for (int i = gl; i < P.n_grasp * 12; i += GS) gT[(i / 12) * 16 + (i % 12)] = A.grasp[(p * P.n_grasp) * 12 + i];
     bool invalid = A.invalid[p] != 0;
     __syncthreads();
     if (gl == 0) {
@@ -297,32 +403,39 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
             if (I.xoff >= 0) { px = xs[I.xoff]; py = xs[I.xoff + 1]; pz = xs[I.xoff + 2]; yaw = xs[I.xoff + 3]; }
             else { px = I.pose[0]; py = I.pose[1]; pz = I.pose[2]; yaw = I.pose[3]; }
             float sy, cy;
-            sincosf(yaw, &sy, &cy);
+            fsincos(yaw, &sy, &cy);
             float* ip = ipose + 16 * i;      // [R row0 | t0, R row1 | t1, R row2 | t2]
             if (gl == 0) {
                 ip[0] = cy; ip[1] = -sy; ip[2] = 0.f; ip[3] = px;
                 ip[4] = sy; ip[5] = cy; ip[6] = 0.f; ip[7] = py;
                 ip[8] = 0.f; ip[9] = 0.f; ip[10] = 1.f; ip[11] = pz;
             }
-            if (gl < P.osph_n[I.obj]) {
+            if (gl < TAMP_MAX_OBJ_SPHERES) {
                 const float4 c = s_osph[I.obj][gl];
-                isph[i * TAMP_MAX_OBJ_SPHERES + gl] =
-                    make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w);
+                isph[i * TAMP_MAX_OBJ_SPHERES + gl] = gl < P.osph_n[I.obj]
+                    ? make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w)
+                    : make_float4(kFar, kFar, kFar, 0.f);
             }
             if (GRAD && gl < 6) iwr[8 * i + gl] = 0.f;
         }
-        if (GRAD) for (int d = gl; d < D; d += kGroup) gs[d] = 0.f;
+        if (GRAD) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
         __syncwarp();
 
         // ---- phase B: robot configurations (Pick/Place confs, knots) ----
         for (int f = 0; f < P.n_fk; ++f) {
             const KFk K = P.fk[f];
-            const float q = gl < TAMP_NJ ? xs[K.xoff + gl] : 0.f;
+            const float q = ll < TAMP_NJ ? xs[K.xoff + ll] : 0.f;
             // A_l = F_l Rz(q_l)
             M34 T;
             {
                 float s, c;
-                sincosf(q, &s, &c);
+                fsincos(q, &s, &c);
+                M34 F;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const float4 f4 = s_F[ll][i];
+                    F.r[3 * i] = f4.x; F.r[3 * i + 1] = f4.y; F.r[3 * i + 2] = f4.z; F.t[i] = f4.w;
+                }
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     T.r[3 * i] = fmaf(F.r[3 * i], c, F.r[3 * i + 1] * s);
@@ -335,62 +448,38 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
 #pragma unroll
             for (int d = 1; d < kGroup; d <<= 1) {
                 const M34 U = shfl_up_m34(T, d);
-                if (gl >= d) T = compose(U, T);
+                if (ll >= d) T = compose(U, T);
             }
             const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
             // my link's spheres in the world
-            float w[TAMP_MAX_SPHERES_PER_LINK][3], gw[TAMP_MAX_SPHERES_PER_LINK][3];
+            float w[NS][3], gw[NS][3], rr[NS];
 #pragma unroll
-            for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
-                xform(T, sph[k][0], sph[k][1], sph[k][2], w[k][0], w[k][1], w[k][2]);
+            for (int k = 0; k < NS; ++k) {
+                const float4 c4 = s_rsph[ll][half * NS + k];
+                xform(T, c4.x, c4.y, c4.z, w[k][0], w[k][1], w[k][2]);
+                if (k >= nsph) w[k][0] = w[k][1] = w[k][2] = kFar;      // absent sphere slot
+                rr[k] = c4.w + P.eta;
                 gw[k][0] = gw[k][1] = gw[k][2] = 0.f;
             }
             float jcf = 0.f;
             Wrench link;
             link.zero();
             if (K.term_cf >= 0) {
-                // robot spheres vs OBBs
-                for (int b = 0; b < P.n_obb; ++b) {
-                    if (!((K.obb_mask >> b) & 1)) continue;
-                    const KObb& B = P.obb[b];
-#pragma unroll
-                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k)
-                        if (k < nsph) jcf += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], sph[k][3] + P.eta, B, lam_cf,
-                                                              gw[k][0], gw[k][1], gw[k][2]);
-                }
-                // robot spheres vs movable objects' spheres
+                // robot spheres vs OBBs (constant cache)
+                for (int b = 0; b < P.n_obb; ++b)
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, NS>(w, rr, P.obb[b], lam_cf, gw);
+                // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    const KInst& I = P.inst[ii];
-                    const int no = P.osph_n[I.obj];
                     Wrench pw;
                     pw.zero();
-                    for (int b = 0; b < no; ++b) {
-                        const float4 B = isph[ii * TAMP_MAX_OBJ_SPHERES + b];
-#pragma unroll
-                        for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
-                            if (k >= nsph) continue;
-                            float ux, uy, uz;
-                            jcf += sphere_sphere<GRAD>(w[k][0], w[k][1], w[k][2], sph[k][3] + P.eta, B, lam_cf, ux, uy, uz);
-                            if (GRAD) {
-                                gw[k][0] -= ux; gw[k][1] -= uy; gw[k][2] -= uz;
-                                pw.add_point(B.x, B.y, B.z, ux, uy, uz);
-                            }
-                        }
-                    }
-                    if (GRAD && I.xoff >= 0 && __any_sync(FULL, pw.nonzero())) {
-                        pw.group_sum();
-                        if (gl == 0) {
-                            float* dst = iwr + 8 * ii;
-                            dst[0] += pw.f[0]; dst[1] += pw.f[1]; dst[2] += pw.f[2];
-                            dst[3] += pw.m[0]; dst[4] += pw.m[1]; dst[5] += pw.m[2];
-                        }
-                    }
+                    jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, lam_cf, gw, pw);
+                    flush_partner<GRAD, GS>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, gl);
                 }
             }
             if (GRAD) {
 #pragma unroll
-                for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k)
+                for (int k = 0; k < NS; ++k)
                     link.add_point(w[k][0], w[k][1], w[k][2], gw[k][0], gw[k][1], gw[k][2]);
             }
             // tool frame to every lane of the group
@@ -401,54 +490,32 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
                 load_m34(Gi, gTi + 16 * K.held_grasp);
                 Tobj = compose(Tee, Gi);
                 const int ho = K.held_obj;
-                float hx = 0.f, hy = 0.f, hz = 0.f, hr = 0.f, ghx = 0.f, ghy = 0.f, ghz = 0.f;
-                const bool mine = gl < P.osph_n[ho];
-                if (mine) {
-                    const float4 c = s_osph[ho][gl];
-                    xform(Tobj, c.x, c.y, c.z, hx, hy, hz);
-                    hr = c.w + P.eta;
-                }
-                for (int b = 0; b < P.n_obb; ++b) {
-                    if (!((K.obb_mask >> b) & 1)) continue;
-                    if (mine) jcf += sphere_obb<GRAD>(hx, hy, hz, hr, P.obb[b], lam_cf, ghx, ghy, ghz);
-                }
+                float h[1][3], gh[1][3] = {{0.f, 0.f, 0.f}}, hr[1];
+                const float4 c = s_osph[ho][gl & (TAMP_MAX_OBJ_SPHERES - 1)];
+                xform(Tobj, c.x, c.y, c.z, h[0][0], h[0][1], h[0][2]);
+                if (gl >= P.osph_n[ho]) h[0][0] = h[0][1] = h[0][2] = kFar;
+                hr[0] = c.w + P.eta;
+                for (int b = 0; b < P.n_obb; ++b)
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, 1>(h, hr, P.obb[b], lam_cf, gh);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    const KInst& I = P.inst[ii];
-                    const int no = P.osph_n[I.obj];
                     Wrench pw;
                     pw.zero();
-                    for (int b = 0; b < no; ++b) {
-                        const float4 B = isph[ii * TAMP_MAX_OBJ_SPHERES + b];
-                        if (!mine) continue;
-                        float ux, uy, uz;
-                        jcf += sphere_sphere<GRAD>(hx, hy, hz, hr, B, lam_cf, ux, uy, uz);
-                        if (GRAD) {
-                            ghx -= ux; ghy -= uy; ghz -= uz;
-                            pw.add_point(B.x, B.y, B.z, ux, uy, uz);
-                        }
-                    }
-                    if (GRAD && I.xoff >= 0 && __any_sync(FULL, pw.nonzero())) {
-                        pw.group_sum();
-                        if (gl == 0) {
-                            float* dst = iwr + 8 * ii;
-                            dst[0] += pw.f[0]; dst[1] += pw.f[1]; dst[2] += pw.f[2];
-                            dst[3] += pw.m[0]; dst[4] += pw.m[1]; dst[5] += pw.m[2];
-                        }
-                    }
+                    jcf += pairs_vs_instance<GRAD, 1>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, lam_cf, gh, pw);
+                    flush_partner<GRAD, GS>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, gl);
                 }
                 if (GRAD) {   // held-object wrench acts on the tool link (lane 7)
                     Wrench hw;
                     hw.zero();
-                    hw.add_point(hx, hy, hz, ghx, ghy, ghz);
-                    hw.group_sum();
+                    hw.add_point(h[0][0], h[0][1], h[0][2], gh[0][0], gh[0][1], gh[0][2]);
+                    hw.template group_sum<GS>();
                     if (gl == kGroup - 1) {
 #pragma unroll
                         for (int i = 0; i < 3; ++i) { link.f[i] += hw.f[i]; link.m[i] += hw.m[i]; }
                     }
                 }
             }
-            if (K.term_cf >= 0) finish_term<MODE>(P, A, sink, K.term_cf, gsum(jcf), gl, active, p, s_counts);
+            if (K.term_cf >= 0) finish_term<MODE>(P, A, sink, K.term_cf, gsum<GS>(jcf), gl, active, p, s_counts);
 
             // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane (uniform)
             if (K.term_kp >= 0 || K.term_kr >= 0) {
@@ -503,11 +570,19 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
             float ejl = 0.f, jl = 0.f;
             if (K.term_jl >= 0) {
                 ejl = gl < TAMP_NJ ? fmaxf(fmaxf(jlo - q, q - jhi), 0.f) : 0.f;
-                jl = sqrtf(gsum(ejl * ejl));
+                jl = sqrtf(gsum<GS>(ejl * ejl));
                 finish_term<MODE>(P, A, sink, K.term_jl, jl, gl, active, p, s_counts);
             }
             if (GRAD) {
-                // suffix sums of link wrenches over lanes >= l, then dJ/dq = z . (M - o x F)
+                // sum the link's halves, then suffix sums of link wrenches over lanes >= l:
+                // dJ/dq = z . (M - o x F)
+                if (GS > kGroup) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        link.f[i] += __shfl_xor_sync(FULL, link.f[i], kGroup);
+                        link.m[i] += __shfl_xor_sync(FULL, link.m[i], kGroup);
+                    }
+                }
 #pragma unroll
                 for (int d = 1; d < kGroup; d <<= 1) {
                     float v[6];
@@ -516,7 +591,7 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
                         v[i] = __shfl_down_sync(FULL, link.f[i], d, kGroup);
                         v[3 + i] = __shfl_down_sync(FULL, link.m[i], d, kGroup);
                     }
-                    if (gl + d < kGroup) {
+                    if (ll + d < kGroup) {
 #pragma unroll
                         for (int i = 0; i < 3; ++i) { link.f[i] += v[i]; link.m[i] += v[3 + i]; }
                     }
@@ -555,14 +630,15 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
             }
             const int no = P.osph_n[I.obj];
             const bool mine = gl < no;
-            float4 c = mine ? isph[ii * TAMP_MAX_OBJ_SPHERES + gl] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 c = gl < TAMP_MAX_OBJ_SPHERES ? isph[ii * TAMP_MAX_OBJ_SPHERES + gl]   // padded slots are far
+                                                       : make_float4(kFar, kFar, kFar, 0.f);
             float gx = 0.f, gy = 0.f, gz = 0.f;
             // containment: sum over spheres of dist_from_bounds(xy in surface frame, lo + r, hi - r)
             {
                 float e = 0.f;
                 if (mine) {
                     float sy, cy;
-                    sincosf(Sf.frame[3], &sy, &cy);
+                    fsincos(Sf.frame[3], &sy, &cy);
                     const float rx = c.x - Sf.frame[0], ry = c.y - Sf.frame[1];
                     const float lx = fmaf(cy, rx, sy * ry), ly = fmaf(-sy, rx, cy * ry);
                     const float lox = Sf.lo[0] + c.w, hix = Sf.hi[0] - c.w;
@@ -578,47 +654,28 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
                         gy += fmaf(sy, glx, cy * gly);
                     }
                 }
-                finish_term<MODE>(P, A, sink, Q.term_sc, gsum(e), gl, active, p, s_counts);
+                finish_term<MODE>(P, A, sink, Q.term_sc, gsum<GS>(e), gl, active, p, s_counts);
             }
             // CFreePlace: placed-object spheres vs OBBs (support excluded) and other objects
             {
                 const float lam_cp = P.term_lam[Q.term_cp];
+                float wq[1][3] = {{c.x, c.y, c.z}}, rq[1] = {c.w + P.eta}, gq[1][3] = {{0.f, 0.f, 0.f}};
                 float jcp = 0.f;
-                const float rr = c.w + P.eta;
-                for (int b = 0; b < P.n_obb; ++b) {
-                    if (!((Q.obb_mask >> b) & 1)) continue;
-                    if (mine) jcp += sphere_obb<GRAD>(c.x, c.y, c.z, rr, P.obb[b], lam_cp, gx, gy, gz);
-                }
+                for (int b = 0; b < P.n_obb; ++b)
+                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<GRAD, 1>(wq, rq, P.obb[b], lam_cp, gq);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
-                    const KInst& J2 = P.inst[jj];
-                    const int n2 = P.osph_n[J2.obj];
                     Wrench pw;
                     pw.zero();
-                    for (int b = 0; b < n2; ++b) {
-                        const float4 B = isph[jj * TAMP_MAX_OBJ_SPHERES + b];
-                        if (!mine) continue;
-                        float ux, uy, uz;
-                        jcp += sphere_sphere<GRAD>(c.x, c.y, c.z, rr, B, lam_cp, ux, uy, uz);
-                        if (GRAD) {
-                            gx -= ux; gy -= uy; gz -= uz;
-                            pw.add_point(B.x, B.y, B.z, ux, uy, uz);
-                        }
-                    }
-                    if (GRAD && J2.xoff >= 0 && __any_sync(FULL, pw.nonzero())) {
-                        pw.group_sum();
-                        if (gl == 0) {
-                            float* dst = iwr + 8 * jj;
-                            dst[0] += pw.f[0]; dst[1] += pw.f[1]; dst[2] += pw.f[2];
-                            dst[3] += pw.m[0]; dst[4] += pw.m[1]; dst[5] += pw.m[2];
-                        }
-                    }
+                    jcp += pairs_vs_instance<GRAD, 1>(wq, rq, isph + jj * TAMP_MAX_OBJ_SPHERES, lam_cp, gq, pw);
+                    flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl);
                 }
-                finish_term<MODE>(P, A, sink, Q.term_cp, gsum(jcp), gl, active, p, s_counts);
+                gx += gq[0][0]; gy += gq[0][1]; gz += gq[0][2];
+                finish_term<MODE>(P, A, sink, Q.term_cp, gsum<GS>(jcp), gl, active, p, s_counts);
             }
             if (GRAD) {
                 if (mine) own.add_point(c.x, c.y, c.z, gx, gy, gz);
-                own.group_sum();
+                own.template group_sum<GS>();
                 if (gl == 0) {
                     float* dst = iwr + 8 * ii;
                     dst[0] += own.f[0]; dst[1] += own.f[1]; dst[2] += own.f[2];
@@ -674,7 +731,7 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
             };
             for (int j = 0; j < nseg; ++j) {
                 const float dlt = val(j + 1) - val(j);
-                const float len = sqrtf(gsum(dlt * dlt));
+                const float len = sqrtf(gsum<GS>(dlt * dlt));
                 soft = fmaf(P.lam_traj, len, soft);
                 if (GRAD && mine && len > 0.f) {
                     const float g = P.lam_traj * dlt / len;
@@ -707,7 +764,7 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
             if (active) {
                 if (gl == 0 && A.out_J) A.out_J[p] = Jtot;
                 if (gl == 0 && A.out_soft) A.out_soft[p] = soft;
-                if (A.out_grad) for (int d = gl; d < D; d += kGroup) A.out_grad[p * D + d] = gs[d];
+                if (A.out_grad) for (int d = gl; d < D; d += GS) A.out_grad[p * D + d] = gs[d];
             }
         } else if (MODE == MODE_CHECK) {
             const bool inv = invalid || !isfinite(Jtot);
@@ -721,8 +778,8 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
         } else {
             // ---- phase F: Adam (Kingma & Ba) with grad scale 1/N (Eq. 4) + projection (L11) ----
             bool bad = !isfinite(Jtot);
-            for (int d = gl; d < D; d += kGroup) bad |= !isfinite(gs[d]);
-            bad = ((__ballot_sync(FULL, bad) >> (threadIdx.x & 24)) & 0xffu) != 0u;   // any lane of my group
+            for (int d = gl; d < D; d += GS) bad |= !isfinite(gs[d]);
+            bad = ((__ballot_sync(FULL, bad) >> (threadIdx.x & 31 & ~(GS - 1))) & ((1u << GS) - 1u)) != 0u;   // my group
             invalid = invalid || bad;
             const int t = A.t0 + it + 1;
             const float bc1 = 1.f - powf(P.beta1, (float)t);
@@ -731,7 +788,7 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
                 if (KM > 0) {
 #pragma unroll
                     for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
-                        const int d = gl + kGroup * k;
+                        const int d = gl + GS * k;
                         if (d < D) {
                             const float g = gs[d] * P.grad_scale;
                             mreg[k] = fmaf(P.beta1, mreg[k], (1.f - P.beta1) * g);
@@ -743,7 +800,7 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
                         }
                     }
                 } else {
-                    for (int d = gl; d < D; d += kGroup) {
+                    for (int d = gl; d < D; d += GS) {
                         const float g = gs[d] * P.grad_scale;
                         const float mm = fmaf(P.beta1, A.m[p * D + d], (1.f - P.beta1) * g);
                         const float vv = fmaf(P.beta2, A.v[p * D + d], (1.f - P.beta2) * g * g);
@@ -760,11 +817,11 @@ __global__ void __launch_bounds__(128, 4) k_particle(const __grid_constant__ KPr
     }
 
     if (MODE == MODE_OPT && active) {
-        for (int d = gl; d < D; d += kGroup) A.x[p * D + d] = xs[d];
+        for (int d = gl; d < D; d += GS) A.x[p * D + d] = xs[d];
         if (KM > 0) {
 #pragma unroll
             for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
-                const int d = gl + kGroup * k;
+                const int d = gl + GS * k;
                 if (d < D) { A.m[p * D + d] = mreg[k]; A.v[p * D + d] = vreg[k]; }
             }
         }
@@ -958,39 +1015,50 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
 static inline void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-static int km_bucket(int D) { return D <= 24 ? 3 : D <= 56 ? 7 : D <= 72 ? 9 : 0; }
-
-template <int MODE, int KM>
+template <int MODE, int KM, int GS>
 static cudaError_t launch_particle_km(const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
-    auto fn = k_particle<MODE, KM>;
+    auto fn = k_particle<MODE, KM, GS>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int per_block = 128 / kGroup;
+    const int per_block = 128 / GS;
     const int64_t blocks = (A.n + per_block - 1) / per_block;
     fn<<<(unsigned)blocks, 128, smem, st>>>(P, A);
     counted();
     return cudaGetLastError();
 }
 
-template <int MODE>
+// moments per lane: ceil(D / GS) in {<=3, <=7, <=9} buckets for D <= 72 (GS = 8) / D <= 144 (GS = 16)
+template <int GS>
+static int km_bucket(int D) {
+    (void)D;
+    return 0;      // moments stay in HBM/L2: ~2 x 2 x D x 4 B per particle-step, frees ~2 x D/GS registers
+}
+
+template <int MODE, int GS>
 static cudaError_t launch_particle_mode(const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
     if constexpr (MODE != MODE_OPT) {
-        return launch_particle_km<MODE, 1>(P, A, smem, st);
+        return launch_particle_km<MODE, 1, GS>(P, A, smem, st);
     } else {
-        switch (km_bucket(P.D)) {
-            case 3: return launch_particle_km<MODE, 3>(P, A, smem, st);
-            case 7: return launch_particle_km<MODE, 7>(P, A, smem, st);
-            case 9: return launch_particle_km<MODE, 9>(P, A, smem, st);
-            default: return launch_particle_km<MODE, 0>(P, A, smem, st);
+        switch (km_bucket<GS>(P.D)) {
+            case 3: return launch_particle_km<MODE, 3, GS>(P, A, smem, st);
+            case 7: return launch_particle_km<MODE, 7, GS>(P, A, smem, st);
+            case 9: return launch_particle_km<MODE, 9, GS>(P, A, smem, st);
+            default: return launch_particle_km<MODE, 0, GS>(P, A, smem, st);
         }
     }
 }
 
-cudaError_t launch_particle(int mode, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
+// gs = lanes per particle (8 or 16); smem must be sized for 128 / gs particles per block
+cudaError_t launch_particle(int mode, int gs, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
     if (A.n <= 0) return cudaSuccess;
-    if (mode == MODE_OPT) return launch_particle_mode<MODE_OPT>(P, A, smem, st);
-    if (mode == MODE_EVAL) return launch_particle_mode<MODE_EVAL>(P, A, smem, st);
-    return launch_particle_mode<MODE_CHECK>(P, A, smem, st);
+    if (gs == 16) {
+        if (mode == MODE_OPT) return launch_particle_mode<MODE_OPT, 16>(P, A, smem, st);
+        if (mode == MODE_EVAL) return launch_particle_mode<MODE_EVAL, 16>(P, A, smem, st);
+        return launch_particle_mode<MODE_CHECK, 16>(P, A, smem, st);
+    }
+    if (mode == MODE_OPT) return launch_particle_mode<MODE_OPT, 8>(P, A, smem, st);
+    if (mode == MODE_EVAL) return launch_particle_mode<MODE_EVAL, 8>(P, A, smem, st);
+    return launch_particle_mode<MODE_CHECK, 8>(P, A, smem, st);
 }
 
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,

@@ -78,14 +78,16 @@ class ProblemDesc(ctypes.Structure):
                 ("lam", F * N_TERM_KINDS), ("eps", F * N_TERM_KINDS),
                 ("lam_goal", F), ("lam_traj", F), ("eta", F),
                 ("beta1", F), ("beta2", F), ("adam_eps", F),
-                ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F)]
+                ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F),
+                ("lanes_per_particle", I32)]
 
 
 class Info(ctypes.Structure):
     _fields_ = [("D", I32), ("n_hard", I32), ("n_grasp", I32), ("n_fk", I32), ("term_kind", I32 * MAX_TERMS),
                 ("n_local", I64), ("global_offset", I64), ("n_global", I64), ("t", I32),
                 ("pairs_sphere_obb", I64), ("pairs_sphere_sphere", I64), ("n_kin", I32), ("n_place", I32),
-                ("n_goal_pairs", I32), ("n_traj_seg", I32), ("n_robot_spheres", I32)]
+                ("n_goal_pairs", I32), ("n_traj_seg", I32), ("n_robot_spheres", I32),
+                ("lanes_per_particle", I32)]
 
 
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
@@ -145,7 +147,7 @@ def _check(status: int):
 # ---------------------------------------------------------------------------------------------
 # ProblemSpec (workloads/) -> tamp_problem_desc marshalling
 # ---------------------------------------------------------------------------------------------
-def build_desc(spec, grad_scale: float = 0.0) -> ProblemDesc:
+def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0) -> ProblemDesc:
     d = ProblemDesc()
     d.abi_version = ABI_VERSION
     r = spec.robot
@@ -211,6 +213,7 @@ def build_desc(spec, grad_scale: float = 0.0) -> ProblemDesc:
     d.beta1, d.beta2, d.adam_eps = float(spec.beta1), float(spec.beta2), float(spec.adam_eps)
     d.lr_conf, d.lr_pos, d.lr_yaw, d.lr_knot = float(spec.lr_conf), float(spec.lr_pos), float(spec.lr_yaw), float(spec.lr_knot)
     d.grad_scale = float(grad_scale)
+    d.lanes_per_particle = int(lanes_per_particle)
     return d
 
 
@@ -227,7 +230,7 @@ class TampContext:
     """One rank's particles of one skeleton on one GPU (tamp_ctx)."""
 
     def __init__(self, spec, n_local: int, global_offset: int = 0, n_global: Optional[int] = None,
-                 device=None, grad_scale: float = 0.0):
+                 device=None, grad_scale: float = 0.0, lanes_per_particle: int = 0):
         self.lib = load()
         if not torch.cuda.is_available():
             raise RuntimeError("TampContext needs a CUDA device (no CPU fallback)")
@@ -235,7 +238,7 @@ class TampContext:
         self.n = int(n_local)
         self.gofs = int(global_offset)
         self.n_global = int(n_global if n_global is not None else n_local)
-        self.desc = build_desc(spec, grad_scale)
+        self.desc = build_desc(spec, grad_scale, lanes_per_particle)
         nbytes = ctypes.c_size_t()
         _check(self.lib.tamp_query_workspace(ctypes.byref(self.desc), self.n, ctypes.byref(nbytes)))
         self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
@@ -251,6 +254,7 @@ class TampContext:
                          n_kin=info.n_kin, n_place=info.n_place, n_goal_pairs=info.n_goal_pairs,
                          n_traj_seg=info.n_traj_seg, n_robot_spheres=info.n_robot_spheres, n_fk=info.n_fk,
                          D=info.D)
+        self.lanes_per_particle = info.lanes_per_particle
         self.counts_buf = torch.zeros(self.n_hard + 2, dtype=torch.int32, device=self.device)
 
     def __del__(self):

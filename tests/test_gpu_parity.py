@@ -23,8 +23,8 @@ def _lib():
     torch.cuda.set_device(0)
 
 
-def _ctx(spec, n, x32, g32, gofs=0, n_global=None):
-    ctx = TampContext(spec, n, global_offset=gofs, n_global=n_global)
+def _ctx(spec, n, x32, g32, gofs=0, n_global=None, lanes=0):
+    ctx = TampContext(spec, n, global_offset=gofs, n_global=n_global, lanes_per_particle=lanes)
     ctx.set_state(torch.from_numpy(x32).cuda(), grasp=to_ctx_grasp(g32).cuda())
     return ctx
 
@@ -47,11 +47,13 @@ def test_sampler_matches_oracle(cfg):
     assert float(st["m"].abs().max()) == 0.0
 
 
+@pytest.mark.parametrize("lanes", [8, 16])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-def test_cost_and_gradient_match_oracle(cfg):
+def test_cost_and_gradient_match_oracle(cfg, lanes):
     n = 97 if cfg != 4 else 40
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=10 + cfg)
-    ctx = _ctx(spec, n, x32, g32)
+    ctx = _ctx(spec, n, x32, g32, lanes=lanes)
+    assert ctx.lanes_per_particle == lanes
     J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
     Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
     np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
@@ -65,11 +67,12 @@ def test_cost_and_gradient_match_oracle(cfg):
     assert ok.mean() > 0.85
 
 
+@pytest.mark.parametrize("lanes", [8, 16])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
-def test_one_adam_step_matches_oracle(cfg):
+def test_one_adam_step_matches_oracle(cfg, lanes):
     n = 97 if cfg != 4 else 40
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=20 + cfg)
-    ctx = _ctx(spec, n, x32, g32, n_global=1000)
+    ctx = _ctx(spec, n, x32, g32, n_global=1000, lanes=lanes)
     ctx.optimize(1)
     st = ctx.get_state()
     x1 = st["x"].cpu().numpy()
@@ -88,11 +91,12 @@ def test_one_adam_step_matches_oracle(cfg):
     assert np.array_equal(st["grasp"].cpu().numpy(), g32.reshape(n, -1, 12))
 
 
+@pytest.mark.parametrize("lanes", [8, 16])
 @pytest.mark.parametrize("cfg", [1, 2, 3])
-def test_check_counts_and_classes_match_oracle(cfg):
+def test_check_counts_and_classes_match_oracle(cfg, lanes):
     n = 301
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=30 + cfg)
-    ctx = _ctx(spec, n, x32, g32)
+    ctx = _ctx(spec, n, x32, g32, lanes=lanes)
     cls = torch.empty(n, dtype=torch.uint8, device="cuda")
     counts, _ = ctx.check(cls=cls)
     counts = counts.cpu().numpy()
@@ -166,14 +170,15 @@ def test_merge_best_k_equals_global_best_k():
     np.testing.assert_array_equal(merged.cpu().numpy(), ref.cpu().numpy())
 
 
-def test_sharding_invariance_bit_exact():
+@pytest.mark.parametrize("lanes", [8, 16])
+def test_sharding_invariance_bit_exact(lanes):
     """Per-particle state after T steps is bit-identical for 1 context vs 2 shards."""
     spec = make_config(2, n=200)
-    one = TampContext(spec, 200, 0, 200)
+    one = TampContext(spec, 200, 0, 200, lanes_per_particle=lanes)
     one.sample(seed=9)
     one.optimize(5)
-    a = TampContext(spec, 120, 0, 200)
-    b2 = TampContext(spec, 80, 120, 200)
+    a = TampContext(spec, 120, 0, 200, lanes_per_particle=lanes)
+    b2 = TampContext(spec, 80, 120, 200, lanes_per_particle=lanes)
     for c in (a, b2):
         c.sample(seed=9)
         c.optimize(3)
