@@ -10,6 +10,7 @@
 //   Place(o, g, p, s, q):                      JL(q), CF(q) [held o excluded], KP(q), KR(q), SS(p), SC(p), CP(p)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -213,6 +214,8 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         const double Rm[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
         for (int k = 0; k < 9; ++k) B.R[k] = (float)Rm[k];
         for (int k = 0; k < 3; ++k) { B.c[k] = o.center[k]; B.h[k] = o.half[k]; }
+        B.rad = (float)(std::sqrt((double)o.half[0] * o.half[0] + (double)o.half[1] * o.half[1] +
+                                  (double)o.half[2] * o.half[2]) * (1.0 + 1e-6));
     }
     const uint16_t all_obb = (uint16_t)((1u << d.n_obb) - 1u);
     for (int o = 0; o < d.n_objects; ++o) {
@@ -220,10 +223,19 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         REQUIRE(ob.n_spheres >= 1 && ob.n_spheres <= TAMP_MAX_OBJ_SPHERES, TAMP_E_UNSUPPORTED,
                 "object n_spheres must be in 1..8");
         P.osph_n[o] = ob.n_spheres;
+        double ctr[3] = {0, 0, 0};
         for (int k = 0; k < ob.n_spheres; ++k) {
             REQUIRE(ob.sphere[k][3] > 0.f, TAMP_E_INVALID, "object sphere radius must be > 0 (S:36)");
             for (int c = 0; c < 4; ++c) P.osph[o][k][c] = ob.sphere[k][c];
+            for (int c = 0; c < 3; ++c) ctr[c] += ob.sphere[k][c] / ob.n_spheres;
         }
+        double rad = 0;   // bounding sphere (broad phase only: it never changes a cost, it skips far pairs)
+        for (int k = 0; k < ob.n_spheres; ++k) {
+            const double dx = ob.sphere[k][0] - ctr[0], dy = ob.sphere[k][1] - ctr[1], dz = ob.sphere[k][2] - ctr[2];
+            rad = std::max(rad, std::sqrt(dx * dx + dy * dy + dz * dz) + ob.sphere[k][3]);
+        }
+        for (int c = 0; c < 3; ++c) P.obound[o][c] = (float)ctr[c];
+        P.obound[o][3] = (float)(rad * (1.0 + 1e-5) + 1e-6);
     }
     for (int s = 0; s < d.n_surfaces; ++s) {
         const tamp_surface_desc& S = d.surface[s];
@@ -614,9 +626,9 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         delete c;
         return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 8 or 16");
     }
-    // auto: 16 lanes (two per link frame) while there are fewer than ~220 particles per SM, so that small
-    // batches still put enough warps in flight; 8 lanes (one per link frame) for large batches
-    c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : (n_local < 32768 ? 16 : 8);
+    // auto: 8 lanes (one per link frame) -- measured faster than 16 on every config, even at 8K particles
+    // (profiles/r1: the 16-lane mapping doubles the FK/kin instruction count for little latency gain)
+    c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : 8;
     ws_layout(c);
     smem_layout(c);
     if (ws_bytes < c->total) {

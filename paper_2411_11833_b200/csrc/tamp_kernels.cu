@@ -216,7 +216,16 @@ constexpr float kFar = 1e18f;   // position of padded (absent) spheres: never wi
 // Returns the hinge sum; if GRAD accumulates dJ/dw_a (x lam) into g and the partner's wrench into pw.
 template <bool GRAD, int NS>
 __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], const float (&rr)[NS], const float4* Bs,
-                                                   float lam, float (&g)[NS][3], Wrench& pw) {
+                                                   const float4 bound, float lam, float (&g)[NS][3], Wrench& pw) {
+    // broad phase: skip the instance unless some query sphere of the warp reaches its bounding sphere
+    float mb = 1.f;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const float dx = w[k][0] - bound.x, dy = w[k][1] - bound.y, dz = w[k][2] - bound.z;
+        const float R = rr[k] + bound.w;
+        mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+    }
+    if (!__any_sync(FULL, mb < 0.f)) return 0.f;
     float mn = 1.f;
 #pragma unroll
     for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
@@ -253,6 +262,15 @@ __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], cons
 template <bool GRAD, int NS>
 __device__ __forceinline__ float spheres_vs_obb(const float (&w)[NS][3], const float (&rr)[NS], const KObb& B,
                                                 float lam, float (&g)[NS][3]) {
+    // broad phase: bounding sphere of the box
+    float mb = 1.f;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
+        const float R = rr[k] + B.rad;
+        mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+    }
+    if (!__any_sync(FULL, mb < 0.f)) return 0.f;
     float mn = 1.f;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -337,6 +355,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
     float* gT = S + A.off_gT;
     float* gTi = S + A.off_gTi;
     const int D = P.D;
+    auto ibound = [&](int i) { return *reinterpret_cast<const float4*>(ipose + 16 * i + 12); };
 
     for (int i = threadIdx.x; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += blockDim.x) {
         const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
@@ -409,6 +428,11 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                 ip[0] = cy; ip[1] = -sy; ip[2] = 0.f; ip[3] = px;
                 ip[4] = sy; ip[5] = cy; ip[6] = 0.f; ip[7] = py;
                 ip[8] = 0.f; ip[9] = 0.f; ip[10] = 1.f; ip[11] = pz;
+                const float* ob = P.obound[I.obj];   // world bounding sphere (broad phase)
+                ip[12] = fmaf(cy, ob[0], fmaf(-sy, ob[1], px));
+                ip[13] = fmaf(sy, ob[0], fmaf(cy, ob[1], py));
+                ip[14] = pz + ob[2];
+                ip[15] = ob[3];
             }
             if (gl < TAMP_MAX_OBJ_SPHERES) {
                 const float4 c = s_osph[I.obj][gl];
@@ -473,7 +497,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                     const int ii = P.partners[K.part_begin + pi];
                     Wrench pw;
                     pw.zero();
-                    jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, lam_cf, gw, pw);
+                    jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw, pw);
                     flush_partner<GRAD, GS>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, gl);
                 }
             }
@@ -501,7 +525,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                     const int ii = P.partners[K.part_begin + pi];
                     Wrench pw;
                     pw.zero();
-                    jcf += pairs_vs_instance<GRAD, 1>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, lam_cf, gh, pw);
+                    jcf += pairs_vs_instance<GRAD, 1>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh, pw);
                     flush_partner<GRAD, GS>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, gl);
                 }
                 if (GRAD) {   // held-object wrench acts on the tool link (lane 7)
@@ -667,7 +691,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                     const int jj = P.partners[Q.part_begin + pi];
                     Wrench pw;
                     pw.zero();
-                    jcp += pairs_vs_instance<GRAD, 1>(wq, rq, isph + jj * TAMP_MAX_OBJ_SPHERES, lam_cp, gq, pw);
+                    jcp += pairs_vs_instance<GRAD, 1>(wq, rq, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq, pw);
                     flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl);
                 }
                 gx += gq[0][0]; gy += gq[0][1]; gz += gq[0][2];

@@ -53,7 +53,7 @@ struct KTraj {
 };
 
 struct KSurface { float frame[4]; float lo[2], hi[2]; };
-struct KObb { float R[9]; float c[3]; float h[3]; };
+struct KObb { float R[9]; float c[3]; float h[3]; float rad; };   // rad = |h| (bounding sphere)
 
 struct KProgram {
     int32_t D, n_terms, n_fk, n_inst, n_place, n_traj, n_goal, n_grasp, n_obb;
@@ -78,6 +78,7 @@ struct KProgram {
     // objects
     float osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES][4];
     int32_t osph_n[TAMP_MAX_OBJECTS];
+    float obound[TAMP_MAX_OBJECTS][4];   // bounding sphere of each object's spheres (object frame xyz, radius)
 };
 
 // Particle-initialisation program (K1).
