@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--no-ttfs", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--lanes", type=int, default=0, help="lanes per particle in the particle kernel (0 = auto)")
+    p.add_argument("--block-threads", type=int, default=0, help="particle-kernel block size (0 = auto)")
+    p.add_argument("--block-sync", type=int, default=-1, help="block-synchronous phases (1/0, -1 = auto)")
     return p.parse_args()
 
 
@@ -309,7 +311,8 @@ def main():
         n = 131072 // 8                              # config 4: 128K particles over 8 GPUs (per-rank share)
     spec = make_config(cfg, n=n)
     n_global = n * world
-    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes)
+    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes,
+                      block_threads=args.block_threads, block_sync=args.block_sync)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
     for w in range(args.warmup):
         run_round(ctx, 10_000 + w, args, dist, world)
@@ -365,7 +368,8 @@ def main():
         host_rec = torch.zeros(args.k, ctx.D + 4, dtype=torch.float32).pin_memory()
         for w_ in range(2):
             c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
-                             lanes_per_particle=args.lanes)
+                             lanes_per_particle=args.lanes,
+                      block_threads=args.block_threads, block_sync=args.block_sync)
             run_round(c2, 30_000 + w_, args, dist, world, host_counts=host_counts, host_rec=host_rec)
         torch.cuda.synchronize()
         if dist is not None:
@@ -374,7 +378,8 @@ def main():
         e2e_steps = max(3, min(args.steps, 10))
         for s in range(e2e_steps):
             c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
-                             lanes_per_particle=args.lanes)                 # host descriptor in
+                             lanes_per_particle=args.lanes,
+                      block_threads=args.block_threads, block_sync=args.block_sync)                 # host descriptor in
             run_round(c2, 40_000 + s, args, dist, world, host_counts=host_counts, host_rec=host_rec)
         torch.cuda.synchronize()
         te = max_over_ranks(time.perf_counter() - t0, dist)
@@ -398,7 +403,8 @@ def main():
                            "particles_per_gpu": n, "particles_global": n_global, "D": ctx.D,
                            "hard_terms": ctx.n_hard, "adam_steps_per_step": args.adam_steps,
                            "check_every": args.check_every, "best_k": args.k, "l2": "flushed between steps",
-                           "lanes_per_particle": ctx.lanes_per_particle,
+                           "lanes_per_particle": ctx.lanes_per_particle, "block_threads": ctx.block_threads,
+                           "block_sync": ctx.block_sync,
                            "parallelism": f"dp{world}"},
                 "kernel_ms_per_launch": opt_avg * 1e3, "kernel_steps_per_launch": args.check_every,
                 "kernel_particle_steps_per_s": n_global * args.check_every / opt_avg,

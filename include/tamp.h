@@ -146,6 +146,8 @@ typedef struct {
     float lr_conf, lr_pos, lr_yaw, lr_knot;
     float grad_scale;                     /* <= 0: use 1 / n_global (Eq. 4) */
     int32_t lanes_per_particle;           /* kernel mapping: 8 or 16 lanes per particle; 0 = auto */
+    int32_t block_threads;                /* particle-kernel block size (multiple of 32, <= 768); 0 = auto */
+    int32_t block_sync;                   /* block-synchronous phases: 0 off, 1 on, -1 auto */
 } tamp_problem_desc;
 
 /* what the compiled CSP looks like (term order = DESIGN.md "canonical term order") */
@@ -162,6 +164,7 @@ typedef struct {
     int64_t pairs_sphere_obb, pairs_sphere_sphere;
     int32_t n_kin, n_place, n_goal_pairs, n_traj_seg, n_robot_spheres;
     int32_t lanes_per_particle;           /* mapping chosen for the particle kernel */
+    int32_t block_threads, block_sync;    /* launch configuration chosen for the particle kernel */
 } tamp_info;
 
 typedef struct tamp_ctx tamp_ctx;

@@ -21,7 +21,8 @@
 #include "tamp_program.h"
 
 namespace tamp {
-cudaError_t launch_particle(int mode, int gs, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st);
+cudaError_t launch_particle(int mode, int gs, bool bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
+                            cudaStream_t st);
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
                           cudaStream_t st);
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
@@ -69,6 +70,9 @@ struct tamp_ctx {
     int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
     size_t smem = 0;
     int gs = 8;                  // lanes per particle in the particle kernel
+    int threads = 128;           // particle-kernel block size
+    bool bsync = false;          // block-synchronous phases
+    int stride_bytes = 0;
     int32_t t = 0;
     bool ready = false;
     int32_t term_kind[TAMP_MAX_TERMS];
@@ -497,7 +501,7 @@ static void smem_layout(tamp_ctx* c) {
     // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
     int stride = ((off + 31) / 32) * 32 + 8;
     c->stride = stride;
-    c->smem = (size_t)(128 / c->gs) * stride * sizeof(float);   // 128-thread blocks
+    c->stride_bytes = stride * (int)sizeof(float);
 }
 
 static void ws_layout(tamp_ctx* c) {
@@ -631,14 +635,43 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : 8;
     ws_layout(c);
     smem_layout(c);
+    {
+        // launch configuration of the particle kernel.  Auto: block-synchronous phases with one large block
+        // per SM holding that SM's share of the particles (all warps of an SM walk the same code region ->
+        // shared instruction cache), bounded by 768 threads and by shared memory.
+        int n_sm = 148, smem_optin = 227 * 1024;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        cudaGetLastError();
+        const int ppw = 32 / c->gs;                                     // particles per warp
+        const int static_smem = 4096;
+        int max_pp = std::min(768 / c->gs, (smem_optin - static_smem) / c->stride_bytes);
+        max_pp = (max_pp / ppw) * ppw;
+        if (desc->block_threads) {
+            if (desc->block_threads % 32 || desc->block_threads < 32 || desc->block_threads > 768) {
+                delete c;
+                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 768]");
+            }
+            c->threads = desc->block_threads;
+        } else {
+            // measured (profiles/README.md): 256-thread blocks with block-synchronous phases are at or near
+            // the best for every config as long as >= 2 blocks fit an SM's shared memory; otherwise 128
+            const int pp256 = 256 / c->gs;
+            c->threads = (2 * pp256 * c->stride_bytes + 2 * static_smem <= smem_optin) ? 256 : 128;
+            c->threads = std::min(c->threads, std::max(ppw, max_pp) * c->gs);
+        }
+        if (c->threads / c->gs > max_pp) {
+            delete c;
+            return fail(TAMP_E_UNSUPPORTED, "block too large for shared memory");
+        }
+        c->bsync = desc->block_sync < 0 ? true : desc->block_sync != 0;
+        c->smem = (size_t)(c->threads / c->gs) * c->stride_bytes;
+    }
     if (ws_bytes < c->total) {
         delete c;
         return fail(TAMP_E_NOMEM, "workspace too small: need " + std::to_string(c->total) + " bytes");
     }
-    if (c->smem > 200 * 1024) {
-        delete c;
-        return fail(TAMP_E_UNSUPPORTED, "per-block shared memory exceeds 200 KB");
-    }
+
     c->base = static_cast<char*>(d_workspace);
     c->ws_bytes = ws_bytes;
     c->coords.reserve(3 * C.lr.size());
@@ -684,6 +717,8 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     out->n_traj_seg = n_seg;
     out->n_robot_spheres = c->n_robot_spheres;
     out->lanes_per_particle = c->gs;
+    out->block_threads = c->threads;
+    out->block_sync = c->bsync ? 1 : 0;
     return TAMP_OK;
 }
 
@@ -707,10 +742,20 @@ tamp_status tamp_optimize_step(tamp_ctx* c, int32_t n_steps, void* stream) {
     if (n_steps == 0) return TAMP_OK;
     DeviceGuard g(c->device);
     KArgs A = base_args(c);
-    A.n_steps = n_steps;
-    A.t0 = c->t;
-    CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "optimize");
-    c->t += n_steps;
+    for (int32_t done = 0; done < n_steps;) {
+        const int32_t k = std::min<int32_t>(n_steps - done, kMaxStepsPerLaunch);
+        A.n_steps = k;
+        A.t0 = c->t;
+        for (int i = 0; i < k; ++i) {   // Adam bias corrections (Kingma & Ba): 1 - beta^t, t = t0 + i + 1
+            const double t = (double)(c->t + i + 1);
+            A.bc1[i] = (float)(1.0 - std::pow((double)c->P.beta1, t));
+            A.bc2[i] = (float)(1.0 - std::pow((double)c->P.beta2, t));
+        }
+        CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->bsync, c->threads, c->P, A, c->smem,
+                                 static_cast<cudaStream_t>(stream)), "optimize");
+        c->t += k;
+        done += k;
+    }
     return TAMP_OK;
 }
 
@@ -720,7 +765,7 @@ static tamp_status run_check(tamp_ctx* c, cudaStream_t st) {
     A.out_cost = c->at<float>(c->o_cost);
     A.out_counts = c->at<int32_t>(c->o_counts);
     CUDA_TRY(cudaMemsetAsync(A.out_counts, 0, (TAMP_MAX_TERMS + 2) * 4, st), "check: zero counts");
-    CUDA_TRY(launch_particle(MODE_CHECK, c->gs, c->P, A, c->smem, st), "check");
+    CUDA_TRY(launch_particle(MODE_CHECK, c->gs, c->bsync, c->threads, c->P, A, c->smem, st), "check");
     return TAMP_OK;
 }
 
@@ -788,7 +833,7 @@ tamp_status tamp_eval(tamp_ctx* c, float* J, float* soft, float* Jc, float* grad
     A.out_soft = soft;
     A.out_Jc = Jc;
     A.out_grad = grad;
-    CUDA_TRY(launch_particle(MODE_EVAL, c->gs, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "eval");
+    CUDA_TRY(launch_particle(MODE_EVAL, c->gs, c->bsync, c->threads, c->P, A, c->smem, static_cast<cudaStream_t>(stream)), "eval");
     return TAMP_OK;
 }
 

@@ -331,8 +331,10 @@ __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, T
 // GS = lanes per particle: 8 (one per link frame) or 16 (two per link frame, each with half of the
 // link's spheres; more warps in flight for small particle counts).
 // KM = register-resident Adam moments per lane (coords gl, gl+GS, ...); 0 = moments stay in global memory
-template <int MODE, int KM, int GS>
-__global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
+// BSYNC: phases are block-synchronous (__syncthreads between FK instances / phases) so that all warps of
+// an SM execute the same code region at a time and share the instruction cache (large blocks, one per SM).
+template <int MODE, int KM, int GS, bool BSYNC>
+__global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     extern __shared__ float4 smem4[];
     __shared__ float4 s_osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES];
@@ -355,6 +357,9 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
     float* gT = S + A.off_gT;
     float* gTi = S + A.off_gTi;
     const int D = P.D;
+    auto phase_sync = [&]() {
+        if (BSYNC) __syncthreads(); else __syncwarp();
+    };
     auto ibound = [&](int i) { return *reinterpret_cast<const float4*>(ipose + 16 * i + 12); };
 
     for (int i = threadIdx.x; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += blockDim.x) {
@@ -443,7 +448,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
             if (GRAD && gl < 6) iwr[8 * i + gl] = 0.f;
         }
         if (GRAD) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
-        __syncwarp();
+        phase_sync();
 
         // ---- phase B: robot configurations (Pick/Place confs, knots) ----
         for (int f = 0; f < P.n_fk; ++f) {
@@ -632,6 +637,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                     gs[K.xoff + gl] += dq;
                 }
             }
+            if (BSYNC) __syncthreads();
         }
 
         // ---- phase C: StablePlace (support, containment) and CFreePlace per Place ----
@@ -769,7 +775,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
 
         // ---- phase E: instance wrenches -> placement gradients ----
         if (GRAD) {
-            __syncwarp();
+            phase_sync();
             for (int i = 0; i < P.n_inst; ++i) {
                 const KInst& I = P.inst[i];
                 if (I.xoff < 0) continue;
@@ -781,7 +787,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                     gs[I.xoff + 3] += wr[5] - (tx * wr[1] - ty * wr[0]);
                 }
             }
-            __syncwarp();
+            phase_sync();
         }
 
         if (MODE == MODE_EVAL) {
@@ -805,9 +811,8 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
             for (int d = gl; d < D; d += GS) bad |= !isfinite(gs[d]);
             bad = ((__ballot_sync(FULL, bad) >> (threadIdx.x & 31 & ~(GS - 1))) & ((1u << GS) - 1u)) != 0u;   // my group
             invalid = invalid || bad;
-            const int t = A.t0 + it + 1;
-            const float bc1 = 1.f - powf(P.beta1, (float)t);
-            const float bc2 = 1.f - powf(P.beta2, (float)t);
+            const float bc1 = A.bc1[it];
+            const float bc2 = A.bc2[it];
             if (!invalid) {
                 if (KM > 0) {
 #pragma unroll
@@ -836,7 +841,7 @@ __global__ void __launch_bounds__(128, 6) k_particle(const __grid_constant__ KPr
                     }
                 }
             }
-            __syncwarp();
+            phase_sync();
         }
     }
 
@@ -1039,50 +1044,35 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
 static inline void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-template <int MODE, int KM, int GS>
-static cudaError_t launch_particle_km(const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
-    auto fn = k_particle<MODE, KM, GS>;
+template <int MODE, int GS, bool BSYNC>
+static cudaError_t launch_particle_t(const KProgram& P, const KArgs& A, int threads, size_t smem, cudaStream_t st) {
+    auto fn = k_particle<MODE, 0, GS, BSYNC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int per_block = 128 / GS;
+    const int per_block = threads / GS;
     const int64_t blocks = (A.n + per_block - 1) / per_block;
-    fn<<<(unsigned)blocks, 128, smem, st>>>(P, A);
+    fn<<<(unsigned)blocks, threads, smem, st>>>(P, A);
     counted();
     return cudaGetLastError();
 }
 
-// moments per lane: ceil(D / GS) in {<=3, <=7, <=9} buckets for D <= 72 (GS = 8) / D <= 144 (GS = 16)
-template <int GS>
-static int km_bucket(int D) {
-    (void)D;
-    return 0;      // moments stay in HBM/L2: ~2 x 2 x D x 4 B per particle-step, frees ~2 x D/GS registers
+template <int GS, bool BSYNC>
+static cudaError_t launch_particle_gs(int mode, const KProgram& P, const KArgs& A, int threads, size_t smem,
+                                      cudaStream_t st) {
+    if (mode == MODE_OPT) return launch_particle_t<MODE_OPT, GS, BSYNC>(P, A, threads, smem, st);
+    if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, GS, BSYNC>(P, A, threads, smem, st);
+    return launch_particle_t<MODE_CHECK, GS, BSYNC>(P, A, threads, smem, st);
 }
 
-template <int MODE, int GS>
-static cudaError_t launch_particle_mode(const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
-    if constexpr (MODE != MODE_OPT) {
-        return launch_particle_km<MODE, 1, GS>(P, A, smem, st);
-    } else {
-        switch (km_bucket<GS>(P.D)) {
-            case 3: return launch_particle_km<MODE, 3, GS>(P, A, smem, st);
-            case 7: return launch_particle_km<MODE, 7, GS>(P, A, smem, st);
-            case 9: return launch_particle_km<MODE, 9, GS>(P, A, smem, st);
-            default: return launch_particle_km<MODE, 0, GS>(P, A, smem, st);
-        }
-    }
-}
-
-// gs = lanes per particle (8 or 16); smem must be sized for 128 / gs particles per block
-cudaError_t launch_particle(int mode, int gs, const KProgram& P, const KArgs& A, size_t smem, cudaStream_t st) {
+// gs = lanes per particle (8 or 16); threads = block size (multiple of 32, <= 768); smem sized for
+// threads / gs particles.  bsync = block-synchronous phases.
+cudaError_t launch_particle(int mode, int gs, bool bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
+                            cudaStream_t st) {
     if (A.n <= 0) return cudaSuccess;
-    if (gs == 16) {
-        if (mode == MODE_OPT) return launch_particle_mode<MODE_OPT, 16>(P, A, smem, st);
-        if (mode == MODE_EVAL) return launch_particle_mode<MODE_EVAL, 16>(P, A, smem, st);
-        return launch_particle_mode<MODE_CHECK, 16>(P, A, smem, st);
-    }
-    if (mode == MODE_OPT) return launch_particle_mode<MODE_OPT, 8>(P, A, smem, st);
-    if (mode == MODE_EVAL) return launch_particle_mode<MODE_EVAL, 8>(P, A, smem, st);
-    return launch_particle_mode<MODE_CHECK, 8>(P, A, smem, st);
+    if (gs == 16) return bsync ? launch_particle_gs<16, true>(mode, P, A, threads, smem, st)
+                               : launch_particle_gs<16, false>(mode, P, A, threads, smem, st);
+    return bsync ? launch_particle_gs<8, true>(mode, P, A, threads, smem, st)
+                 : launch_particle_gs<8, false>(mode, P, A, threads, smem, st);
 }
 
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,

@@ -16,6 +16,7 @@ constexpr int kMaxTraj = 32;          // motions carrying knots
 constexpr int kMaxPartners = 1024;    // collision partner instance references
 constexpr int kMaxConstConf = 8;      // constant confs referenced by trajectories (q0)
 constexpr int kGroup = 8;             // lanes per particle: one per link frame (7 joints + tool)
+constexpr int kMaxStepsPerLaunch = 64; // fused Adam steps per particle-kernel launch
 
 // One robot configuration evaluated per particle-step: a Pick/Place conf or a trajectory knot.
 struct KFk {
@@ -118,6 +119,9 @@ struct KArgs {
     int64_t gofs;
     int32_t stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
     int32_t n_steps, t0;
+    // Adam bias corrections 1 - beta^t for the (<= kMaxStepsPerLaunch) steps of this launch, computed on the
+    // host in double precision
+    float bc1[64], bc2[64];
     // MODE_EVAL outputs (nullable)
     float* out_J;
     float* out_soft;

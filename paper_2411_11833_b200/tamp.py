@@ -79,7 +79,7 @@ class ProblemDesc(ctypes.Structure):
                 ("lam_goal", F), ("lam_traj", F), ("eta", F),
                 ("beta1", F), ("beta2", F), ("adam_eps", F),
                 ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F),
-                ("lanes_per_particle", I32)]
+                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32)]
 
 
 class Info(ctypes.Structure):
@@ -87,7 +87,7 @@ class Info(ctypes.Structure):
                 ("n_local", I64), ("global_offset", I64), ("n_global", I64), ("t", I32),
                 ("pairs_sphere_obb", I64), ("pairs_sphere_sphere", I64), ("n_kin", I32), ("n_place", I32),
                 ("n_goal_pairs", I32), ("n_traj_seg", I32), ("n_robot_spheres", I32),
-                ("lanes_per_particle", I32)]
+                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32)]
 
 
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
@@ -147,7 +147,8 @@ def _check(status: int):
 # ---------------------------------------------------------------------------------------------
 # ProblemSpec (workloads/) -> tamp_problem_desc marshalling
 # ---------------------------------------------------------------------------------------------
-def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0) -> ProblemDesc:
+def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block_threads: int = 0,
+               block_sync: int = -1) -> ProblemDesc:
     d = ProblemDesc()
     d.abi_version = ABI_VERSION
     r = spec.robot
@@ -214,6 +215,8 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0) -> Pr
     d.lr_conf, d.lr_pos, d.lr_yaw, d.lr_knot = float(spec.lr_conf), float(spec.lr_pos), float(spec.lr_yaw), float(spec.lr_knot)
     d.grad_scale = float(grad_scale)
     d.lanes_per_particle = int(lanes_per_particle)
+    d.block_threads = int(block_threads)
+    d.block_sync = int(block_sync)
     return d
 
 
@@ -230,7 +233,8 @@ class TampContext:
     """One rank's particles of one skeleton on one GPU (tamp_ctx)."""
 
     def __init__(self, spec, n_local: int, global_offset: int = 0, n_global: Optional[int] = None,
-                 device=None, grad_scale: float = 0.0, lanes_per_particle: int = 0):
+                 device=None, grad_scale: float = 0.0, lanes_per_particle: int = 0, block_threads: int = 0,
+                 block_sync: int = -1):
         self.lib = load()
         if not torch.cuda.is_available():
             raise RuntimeError("TampContext needs a CUDA device (no CPU fallback)")
@@ -238,7 +242,7 @@ class TampContext:
         self.n = int(n_local)
         self.gofs = int(global_offset)
         self.n_global = int(n_global if n_global is not None else n_local)
-        self.desc = build_desc(spec, grad_scale, lanes_per_particle)
+        self.desc = build_desc(spec, grad_scale, lanes_per_particle, block_threads, block_sync)
         nbytes = ctypes.c_size_t()
         _check(self.lib.tamp_query_workspace(ctypes.byref(self.desc), self.n, ctypes.byref(nbytes)))
         self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
@@ -255,6 +259,7 @@ class TampContext:
                          n_traj_seg=info.n_traj_seg, n_robot_spheres=info.n_robot_spheres, n_fk=info.n_fk,
                          D=info.D)
         self.lanes_per_particle = info.lanes_per_particle
+        self.block_threads, self.block_sync = info.block_threads, info.block_sync
         self.counts_buf = torch.zeros(self.n_hard + 2, dtype=torch.int32, device=self.device)
 
     def __del__(self):

@@ -280,3 +280,34 @@ def test_edge_sizes():
     assert decode_records(rec)[2][0] == 0
     ctx.optimize(3)
     assert ctx.t == 3
+
+
+@pytest.mark.parametrize("lanes", [8, 16])
+def test_launch_configuration_invariance_bit_exact(lanes):
+    """Block size and block-synchronous phases change only the schedule: results are bit-identical."""
+    spec = make_config(3, n=300)
+    ref = None
+    for threads, bsync in [(128, 0), (256, 1), (512, 1), (64, 1)]:
+        c = TampContext(spec, 300, lanes_per_particle=lanes, block_threads=threads, block_sync=bsync)
+        c.sample(seed=5)
+        c.optimize(4)
+        counts, _ = c.check()
+        out = (c.get_state()["x"].cpu().numpy(), counts.cpu().numpy())
+        if ref is None:
+            ref = out
+        else:
+            assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
+
+
+def test_long_launch_is_split_and_matches_short_launches():
+    """n_steps > 64 per call is split into launches of <= 64 fused steps with identical results."""
+    spec = make_config(1, n=64)
+    a = TampContext(spec, 64)
+    a.sample(seed=3)
+    a.optimize(100)
+    b2 = TampContext(spec, 64)
+    b2.sample(seed=3)
+    for _ in range(10):
+        b2.optimize(10)
+    assert a.t == b2.t == 100
+    assert np.array_equal(a.get_state()["x"].cpu().numpy(), b2.get_state()["x"].cpu().numpy())
