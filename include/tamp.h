@@ -147,7 +147,11 @@ typedef struct {
     float grad_scale;                     /* <= 0: use 1 / n_global (Eq. 4) */
     int32_t lanes_per_particle;           /* kernel mapping: 8 or 16 lanes per particle; 0 = auto */
     int32_t block_threads;                /* particle-kernel block size (multiple of 32, <= 768); 0 = auto */
-    int32_t block_sync;                   /* block-synchronous phases: 0 off, 1 on, -1 auto */
+    int32_t block_sync;                   /* block-synchronous phases: 0 off, 1 phase boundaries, 2 + every
+                                             FK instance, 3 + inside the FK body; -1 auto (2) */
+    int32_t ik_iters;                     /* conditional IK sampler: damped-least-squares iterations
+                                             per Pick/Place conf inside tamp_sample_particles; 0 = uniform confs */
+    float ik_damping;                     /* DLS damping mu (dq = J^T (J J^T + mu^2 I)^-1 e) */
 } tamp_problem_desc;
 
 /* what the compiled CSP looks like (term order = DESIGN.md "canonical term order") */
@@ -190,7 +194,8 @@ tamp_status tamp_get_info(const tamp_ctx* ctx, tamp_info* out);
 
 /* InitializeParticles (Alg. 1): Philox4x32-10 counter RNG (key = seed, counter =
    (global index, variable id, block)); grasps top-down and frozen, placements uniform on the
-   surface region, confs uniform within joint limits, knots linear interpolation.  Resets Adam
+   surface region, confs uniform within joint limits, then (ik_iters > 0) the conditional IK sampler
+    toward each Pick/Place conf's Kin target, knots linear interpolation.  Resets Adam
    (m = v = 0, t = 0) and the invalid flags. */
 tamp_status tamp_sample_particles(tamp_ctx* ctx, uint64_t seed, void* stream);
 

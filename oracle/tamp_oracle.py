@@ -288,12 +288,47 @@ def build_csp(spec: ProblemSpec) -> CSP:
 # ----------------------------------------------------------------------------------------------
 # Particle initialisation (Algorithm 1 InitializeParticles).  Philox counter RNG.
 # ----------------------------------------------------------------------------------------------
+def ik_dls(robot, q, T_target, iters, damping):
+    """Conditional IK sampler: damped-least-squares iterations on FK(q) = T_target.
+
+    Per iteration (Wampler / Nakamura DLS): e = [t* - t_ee ; rotvec(R* R_ee^T)] (world frame),
+    J = [z_j x (t_ee - o_j) ; z_j]_{j=1..7}, dq = J^T (J J^T + damping^2 I)^-1 e, q <- clamp(q + dq).
+    q [N, 7] float64 (start: the uniform sample), T_target [N, 4, 4].
+    """
+    q = q.copy()
+    lo, hi = robot.joint_lo, robot.joint_hi
+    Tt = torch.as_tensor(T_target, dtype=DT)
+    for _ in range(iters):
+        F = forward_kinematics(robot, torch.as_tensor(q, dtype=DT))
+        Tee = F[:, 8]
+        p = Tee[:, :3, 3]
+        e_p = Tt[:, :3, 3] - p
+        E = Tt[:, :3, :3] @ Tee[:, :3, :3].transpose(-1, -2)
+        w = torch.stack([E[:, 2, 1] - E[:, 1, 2], E[:, 0, 2] - E[:, 2, 0], E[:, 1, 0] - E[:, 0, 1]], -1)
+        wn = torch.linalg.vector_norm(w, dim=-1)
+        th = torch.atan2(wn / 2, (E[:, 0, 0] + E[:, 1, 1] + E[:, 2, 2] - 1) / 2)
+        e_r = torch.where(wn[:, None] > 0, w * (th / torch.where(wn > 0, wn, 1.0))[:, None], torch.zeros_like(w))
+        e = torch.cat([e_p, e_r], -1)                                  # [N, 6]
+        cols = []
+        for j in range(1, 8):
+            z = F[:, j, :3, 2]
+            o = F[:, j, :3, 3]
+            cols.append(torch.cat([torch.linalg.cross(z, p - o), z], -1))
+        J = torch.stack(cols, -1)                                      # [N, 6, 7]
+        A = J @ J.transpose(-1, -2) + damping ** 2 * torch.eye(6, dtype=DT)
+        y = torch.linalg.solve(A, e[..., None])
+        dq = (J.transpose(-1, -2) @ y)[..., 0]
+        q = np.minimum(np.maximum(q + dq.numpy(), lo), hi)
+    return q
+
+
 def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarray):
     """Returns x0 [N, D] float64 and grasps [N, G, 3, 4] float64.
 
     Samplers composed in DAG order: grasps (frozen) -> placements (uniform on the surface
-    region) -> confs (uniform within joint limits = the `Optimization` init) ->
-    knots (linear interpolation).
+    region) -> confs (uniform within joint limits = the `Optimization` init; then, if
+    spec.ik_iters > 0, the conditional IK sampler of P:521 toward each Pick/Place conf's Kin target
+    T(p) T(g)) -> knots (linear interpolation).
     """
     V = spec.variables
     N = len(gidx)
@@ -329,6 +364,20 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
             x[:, off + 1] = s.frame[1] + sn * lx + c * ly
             x[:, off + 2] = s.frame[2]
             x[:, off + 3] = s.frame[3] + lyaw
+    if getattr(spec, "ik_iters", 0) > 0:
+        gslot = {vi: k for k, vi in enumerate(csp.grasp_vars)}
+        bottom = np.zeros((N, 1, 4))
+        bottom[..., 3] = 1.0
+        for a in spec.actions:
+            if a.kind not in (PICK, PLACE) or V[a.q1].const:
+                continue
+            pv = V[a.placement]
+            pval = np.broadcast_to(np.asarray(pv.value, float), (N, 4)) if pv.const else \
+                x[:, csp.offsets[a.placement]:csp.offsets[a.placement] + 4]
+            Tg = np.concatenate([grasps[:, gslot[a.grasp]], bottom], 1)
+            Tt = (pose_xyzyaw(torch.as_tensor(pval)) @ torch.as_tensor(Tg)).numpy()
+            off = csp.offsets[a.q1]
+            x[:, off:off + 7] = ik_dls(spec.robot, x[:, off:off + 7], Tt, spec.ik_iters, spec.ik_damping)
     for a in spec.actions:
         if a.kind in (MOVE_FREE, MOVE_HOLD) and a.traj >= 0 and V[a.traj].n_knots > 0:
             K = V[a.traj].n_knots

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <tuple>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -21,10 +22,13 @@
 #include "tamp_program.h"
 
 namespace tamp {
-cudaError_t launch_particle(int mode, int gs, bool bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
+cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
                             cudaStream_t st);
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
                           cudaStream_t st);
+cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
+                      cudaStream_t st);
+int particle_kernel_regs(int gs);
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
                         cudaStream_t st, unsigned long long** kres, int32_t** pres);
 cudaError_t launch_make_keys(const uint8_t* cls, const float* cost, int64_t n, int64_t gofs, unsigned long long* keys,
@@ -70,8 +74,10 @@ struct tamp_ctx {
     int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
     size_t smem = 0;
     int gs = 8;                  // lanes per particle in the particle kernel
+    int ik_iters = 0;            // conditional IK sampler iterations
+    float ik_damping = 0.1f;
     int threads = 128;           // particle-kernel block size
-    bool bsync = false;          // block-synchronous phases
+    int bsync = 2;               // block-synchronisation level of the particle kernel (0..3)
     int stride_bytes = 0;
     int32_t t = 0;
     bool ready = false;
@@ -131,7 +137,7 @@ static void count_pairs(const tamp_problem_desc& d, Compiled& C) {
     int64_t sb = 0, ss = 0;
     for (int f = 0; f < P.n_fk; ++f) {
         const KFk& K = P.fk[f];
-        if (K.term_cf < 0) continue;
+        if (K.term_cf < 0 || K.ghost) continue;
         int part_sph = 0;
         for (int i = 0; i < K.part_count; ++i) part_sph += P.osph_n[P.inst[P.partners[K.part_begin + i]].obj];
         const int nb = popc(K.obb_mask);
@@ -359,6 +365,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
                 F.held_grasp = (int16_t)hg;
                 F.held_obj = (int16_t)(hg >= 0 ? a.obj : -1);
                 F.obb_mask = all_obb;
+                F.ghost = 0;
                 REQUIRE(add_partners(-1, -1, F.part_begin, F.part_count), TAMP_E_UNSUPPORTED, "too many partners");
             }
             REQUIRE(n_traj < kMaxTraj, TAMP_E_UNSUPPORTED, "too many trajectories");
@@ -392,6 +399,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             F.kin_grasp = (int16_t)gslot[a.grasp];
             F.held_grasp = F.held_obj = -1;
             F.obb_mask = all_obb;
+            F.ghost = 0;
             REQUIRE(add_partners(a.obj, -1, F.part_begin, F.part_count), TAMP_E_UNSUPPORTED, "too many partners");
             if (a.kind == TAMP_PICK) {
                 held = a.obj;
@@ -420,6 +428,36 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         REQUIRE(n_terms < TAMP_MAX_TERMS, TAMP_E_UNSUPPORTED, "too many hard terms (TAMP_MAX_TERMS)");
     }
     P.n_terms = n_terms;
+    // Order the FK instances in pairs of identical structure (same terms, held object or not, partner count,
+    // OBB mask) so that the 16-lane mapping can run the two 8-lane halves of a particle group on two FK
+    // instances with warp-uniform control flow; an unmatched instance is paired with a ghost copy.
+    {
+        auto sig = [&](const KFk& K) {
+            return std::make_tuple(K.term_cf >= 0, K.term_kp >= 0, K.term_kr >= 0, K.term_jl >= 0, K.held_grasp >= 0,
+                                   K.part_count, K.obb_mask);
+        };
+        std::vector<KFk> in(P.fk, P.fk + n_fk), out;
+        std::vector<bool> used(n_fk, false);
+        for (int i = 0; i < n_fk; ++i) {
+            if (used[i]) continue;
+            used[i] = true;
+            int j = -1;
+            for (int k = i + 1; k < n_fk && j < 0; ++k)
+                if (!used[k] && sig(in[k]) == sig(in[i])) j = k;
+            out.push_back(in[i]);
+            if (j >= 0) {
+                used[j] = true;
+                out.push_back(in[j]);
+            } else {
+                KFk g = in[i];
+                g.ghost = 1;
+                out.push_back(g);
+            }
+        }
+        REQUIRE((int)out.size() <= TAMP_MAX_FK, TAMP_E_UNSUPPORTED, "too many robot configurations (TAMP_MAX_FK)");
+        for (size_t i = 0; i < out.size(); ++i) P.fk[i] = out[i];
+        n_fk = (int)out.size();
+    }
     P.n_fk = n_fk;
     P.n_place = n_place;
     P.n_traj = n_traj;
@@ -626,13 +664,25 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     c->pairs_sb = C.pairs_sb;
     c->pairs_ss = C.pairs_ss;
     c->n_robot_spheres = desc->robot.n_spheres;
+    if (desc->ik_iters < 0 || desc->ik_iters > 1000 || !(desc->ik_damping >= 0.f)) {
+        delete c;
+        return fail(TAMP_E_INVALID, "ik_iters must be in [0, 1000] and ik_damping >= 0");
+    }
+    c->ik_iters = desc->ik_iters;
+    c->ik_damping = desc->ik_damping;
     if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 8 && desc->lanes_per_particle != 16) {
         delete c;
         return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 8 or 16");
     }
     // auto: 8 lanes (one per link frame) -- measured faster than 16 on every config, even at 8K particles
     // (profiles/r1: the 16-lane mapping doubles the FK/kin instruction count for little latency gain)
-    c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : 8;
+    {
+        int n_fk_real = 0;
+        for (int f = 0; f < c->P.n_fk; ++f) n_fk_real += !c->P.fk[f].ghost;
+        // 16 lanes (two FK instances at a time) pays off for knot-heavy skeletons (config 4: 48 FK
+        // instances), 8 lanes elsewhere (sweep9)
+        c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : (n_fk_real >= 24 ? 16 : 8);
+    }
     ws_layout(c);
     smem_layout(c);
     {
@@ -654,17 +704,43 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             }
             c->threads = desc->block_threads;
         } else {
-            // measured (profiles/README.md): 256-thread blocks with block-synchronous phases are at or near
-            // the best for every config as long as >= 2 blocks fit an SM's shared memory; otherwise 128
-            const int pp256 = 256 / c->gs;
-            c->threads = (2 * pp256 * c->stride_bytes + 2 * static_smem <= smem_optin) ? 256 : 128;
-            c->threads = std::min(c->threads, std::max(ppw, max_pp) * c->gs);
+            // measured (profiles/README.md, sweeps 8-10):
+            //  - if every particle of the launch is resident at once with one block per SM holding that SM's
+            //    share, that block with phase-level barriers is best (config 2 at 8K);
+            //  - otherwise the block size that maximises resident warps per SM (registers, shared memory),
+            //    ties broken toward 2 blocks per SM, with phase-level barriers (config 3: 608 threads,
+            //    config 1: 384 threads).
+            int64_t pp = (n_local + n_sm - 1) / n_sm;                      // this SM's share
+            pp = ((pp + ppw - 1) / ppw) * ppw;
+            c->bsync = 1;
+            if (pp <= max_pp) {
+                c->threads = (int)std::max<int64_t>(pp, 4 * ppw) * c->gs;
+            } else {
+                const int regs = std::max(32, particle_kernel_regs(c->gs));
+                int best_t = 128, best_score = -1;
+                for (int t = 128; t <= 768; t += 32) {
+                    const int ppb = t / c->gs;
+                    if (ppb % ppw || ppb > max_pp) continue;
+                    const int by_regs = 65536 / (((regs + 7) & ~7) * t);
+                    const int by_smem = (smem_optin + 1024) / (ppb * c->stride_bytes + static_smem + 1024);
+                    const int blocks = std::min(std::min(by_regs, by_smem), 32);
+                    if (blocks < 1) continue;
+                    const int score = 8 * blocks * (t / 32) + (blocks == 2 ? 4 : 0) + (blocks >= 2 ? 2 : 0);
+                    if (score > best_score) { best_score = score; best_t = t; }
+                }
+                c->threads = best_t;
+            }
         }
         if (c->threads / c->gs > max_pp) {
             delete c;
             return fail(TAMP_E_UNSUPPORTED, "block too large for shared memory");
         }
-        c->bsync = desc->block_sync < 0 ? true : desc->block_sync != 0;
+        if (desc->block_sync > 3) {
+            delete c;
+            return fail(TAMP_E_INVALID, "block_sync must be -1 (auto) or 0..3");
+        }
+        if (desc->block_threads && desc->block_sync < 0) c->bsync = 2;
+        if (desc->block_sync >= 0) c->bsync = desc->block_sync;
         c->smem = (size_t)(c->threads / c->gs) * c->stride_bytes;
     }
     if (ws_bytes < c->total) {
@@ -709,7 +785,12 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     out->pairs_sphere_obb = c->pairs_sb;
     out->pairs_sphere_sphere = c->pairs_ss;
     int n_kin = 0, n_seg = 0;
-    for (int f = 0; f < c->P.n_fk; ++f) n_kin += c->P.fk[f].term_kp >= 0;
+    int n_fk_real = 0;
+    for (int f = 0; f < c->P.n_fk; ++f) {
+        n_kin += c->P.fk[f].term_kp >= 0 && !c->P.fk[f].ghost;
+        n_fk_real += !c->P.fk[f].ghost;
+    }
+    out->n_fk = n_fk_real;
     for (int i = 0; i < c->P.n_traj; ++i) n_seg += c->P.traj[i].n_knots + 1;
     out->n_kin = n_kin;
     out->n_place = c->P.n_place;
@@ -718,7 +799,7 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     out->n_robot_spheres = c->n_robot_spheres;
     out->lanes_per_particle = c->gs;
     out->block_threads = c->threads;
-    out->block_sync = c->bsync ? 1 : 0;
+    out->block_sync = c->bsync;
     return TAMP_OK;
 }
 
@@ -727,6 +808,8 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     DeviceGuard g(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(launch_sample(c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, st), "sample");
+    CUDA_TRY(launch_ik(c->P, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->ik_iters, c->ik_damping, st),
+             "sample: IK");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero m");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero v");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_inv, 0, (size_t)c->n, st), "sample: zero invalid");

@@ -306,6 +306,21 @@ __device__ __forceinline__ void flush_partner(Wrench& pw, bool movable, float* d
     }
 }
 
+// phase-B variant: each 8-lane half may work on a different FK instance (so `movable` and `dst` may differ
+// between halves): warp-uniform vote, per-half reduction, halves add one after the other (deterministic).
+template <bool GRAD, int HP>
+__device__ __forceinline__ void flush_partner_b(Wrench& pw, bool movable, float* dst, int ll, int half, bool real) {
+    if (!GRAD) return;
+    if (__any_sync(FULL, movable && pw.nonzero())) {
+        pw.template group_sum<kGroup>();
+#pragma unroll
+        for (int h = 0; h < HP; ++h) {
+            if (half == h && ll == 0 && real && movable) add_wrench(dst, pw);
+            if (HP > 1) __syncwarp();
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------------------
 // K2 / K3 / eval: the fused per-particle kernel
 // ------------------------------------------------------------------------------------------------
@@ -317,7 +332,9 @@ struct TermSink {
 
 template <int MODE>
 __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, TermSink<MODE>& sink, int term,
-                                            float val, int gl, bool active, int64_t p, int* s_counts) {
+                                            float val, int gl, bool active, int64_t p, int* s_counts,
+                                            bool real = true) {
+    if (!real) return;   // ghost FK instance (pair padding)
     sink.J = fmaf(P.term_lam[term], val, sink.J);
     if (MODE == MODE_EVAL) {
         if (gl == 0 && active && A.out_Jc) A.out_Jc[p * P.n_terms + term] = val;
@@ -328,22 +345,23 @@ __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, T
     }
 }
 
-// GS = lanes per particle: 8 (one per link frame) or 16 (two per link frame, each with half of the
-// link's spheres; more warps in flight for small particle counts).
+// GS = lanes per particle: 8 (one per link frame) or 16 (two FK instances at a time, one per 8-lane half:
+// twice the warps in flight for the same particle count, no duplicated work).
 // KM = register-resident Adam moments per lane (coords gl, gl+GS, ...); 0 = moments stay in global memory
-// BSYNC: phases are block-synchronous (__syncthreads between FK instances / phases) so that all warps of
-// an SM execute the same code region at a time and share the instruction cache (large blocks, one per SM).
-template <int MODE, int KM, int GS, bool BSYNC>
+// BSYNC: block-synchronous phases so that all warps of a block execute the same code region at a time and
+// share the instruction cache.  0 = off (warp-level only), 1 = at phase boundaries, 2 = also after every
+// FK instance, 3 = also between collision and Kin inside the FK body.
+template <int MODE, int KM, int GS, int BSYNC>
 __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     extern __shared__ float4 smem4[];
     __shared__ float4 s_osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES];
     __shared__ int s_counts[TAMP_MAX_TERMS + 2];
 
-    constexpr int NS = TAMP_MAX_SPHERES_PER_LINK / (GS / kGroup);   // robot spheres per lane
+    constexpr int NS = TAMP_MAX_SPHERES_PER_LINK;                    // robot spheres per lane (its link's)
     const int gl = threadIdx.x & (GS - 1);          // lane within the particle group
     const int ll = gl & (kGroup - 1);               // link frame owned by this lane
-    const int half = gl / kGroup;                   // which share of the link's spheres
+    const int half = gl / kGroup;                   // GS = 16: which FK instance of the pair
     const int grp = threadIdx.x / GS;
     const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / GS) + grp;
     const bool active = pid < A.n;
@@ -358,7 +376,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
     float* gTi = S + A.off_gTi;
     const int D = P.D;
     auto phase_sync = [&]() {
-        if (BSYNC) __syncthreads(); else __syncwarp();
+        if (BSYNC > 0) __syncthreads(); else __syncwarp();
     };
     auto ibound = [&](int i) { return *reinterpret_cast<const float4*>(ipose + 16 * i + 12); };
 
@@ -381,7 +399,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
         const int l = threadIdx.x / TAMP_MAX_SPHERES_PER_LINK, k = threadIdx.x % TAMP_MAX_SPHERES_PER_LINK;
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3]);
     }
-    const int nsph = P.rsph_n[ll] - half * NS;      // my valid spheres (may be <= 0)
+    const int nsph = P.rsph_n[ll];                  // my link's spheres
     const float jlo = ll < TAMP_NJ ? P.jlo[ll] : 0.f;
     const float jhi = ll < TAMP_NJ ? P.jhi[ll] : 0.f;
 
@@ -451,8 +469,15 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
         phase_sync();
 
         // ---- phase B: robot configurations (Pick/Place confs, knots) ----
-        for (int f = 0; f < P.n_fk; ++f) {
-            const KFk K = P.fk[f];
+        // GS = 16: the two 8-lane halves of a particle group process the two FK instances of a pair of identical
+        // structure concurrently (the compiler pairs them; an unmatched instance is paired with a ghost copy
+        // whose results are discarded), so control flow stays warp-uniform.  GS = 8: ghosts are skipped.
+        constexpr int HP = GS / kGroup;
+        TermSink<MODE> sinkB;                  // this half's share of the phase-B terms
+        for (int f0 = 0; f0 < P.n_fk; f0 += HP) {
+            const KFk K = P.fk[f0 + (HP > 1 ? half : 0)];
+            const bool real = !K.ghost;
+            if (HP == 1 && !real) continue;
             const float q = ll < TAMP_NJ ? xs[K.xoff + ll] : 0.f;
             // A_l = F_l Rz(q_l)
             M34 T;
@@ -484,7 +509,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
             float w[NS][3], gw[NS][3], rr[NS];
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
-                const float4 c4 = s_rsph[ll][half * NS + k];
+                const float4 c4 = s_rsph[ll][k];
                 xform(T, c4.x, c4.y, c4.z, w[k][0], w[k][1], w[k][2]);
                 if (k >= nsph) w[k][0] = w[k][1] = w[k][2] = kFar;      // absent sphere slot
                 rr[k] = c4.w + P.eta;
@@ -503,7 +528,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                     Wrench pw;
                     pw.zero();
                     jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw, pw);
-                    flush_partner<GRAD, GS>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, gl);
+                    flush_partner_b<GRAD, HP>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
                 }
             }
             if (GRAD) {
@@ -511,7 +536,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                 for (int k = 0; k < NS; ++k)
                     link.add_point(w[k][0], w[k][1], w[k][2], gw[k][0], gw[k][1], gw[k][2]);
             }
-            // tool frame to every lane of the group
+            // tool frame to every lane of the half
             const M34 Tee = shfl_m34(T, kGroup - 1);
             // held object at a MoveHold knot: attached spheres T_ee T(g)^-1 c (CFreeTrajHold)
             if (K.held_grasp >= 0 && K.term_cf >= 0) {
@@ -520,9 +545,9 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                 Tobj = compose(Tee, Gi);
                 const int ho = K.held_obj;
                 float h[1][3], gh[1][3] = {{0.f, 0.f, 0.f}}, hr[1];
-                const float4 c = s_osph[ho][gl & (TAMP_MAX_OBJ_SPHERES - 1)];
+                const float4 c = s_osph[ho][ll];
                 xform(Tobj, c.x, c.y, c.z, h[0][0], h[0][1], h[0][2]);
-                if (gl >= P.osph_n[ho]) h[0][0] = h[0][1] = h[0][2] = kFar;
+                if (ll >= P.osph_n[ho]) h[0][0] = h[0][1] = h[0][2] = kFar;
                 hr[0] = c.w + P.eta;
                 for (int b = 0; b < P.n_obb; ++b)
                     if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, 1>(h, hr, P.obb[b], lam_cf, gh);
@@ -531,22 +556,24 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                     Wrench pw;
                     pw.zero();
                     jcf += pairs_vs_instance<GRAD, 1>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh, pw);
-                    flush_partner<GRAD, GS>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, gl);
+                    flush_partner_b<GRAD, HP>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
                 }
-                if (GRAD) {   // held-object wrench acts on the tool link (lane 7)
+                if (GRAD) {   // held-object wrench acts on the tool link (lane 7 of the half)
                     Wrench hw;
                     hw.zero();
                     hw.add_point(h[0][0], h[0][1], h[0][2], gh[0][0], gh[0][1], gh[0][2]);
-                    hw.template group_sum<GS>();
-                    if (gl == kGroup - 1) {
+                    hw.template group_sum<kGroup>();
+                    if (ll == kGroup - 1) {
 #pragma unroll
                         for (int i = 0; i < 3; ++i) { link.f[i] += hw.f[i]; link.m[i] += hw.m[i]; }
                     }
                 }
             }
-            if (K.term_cf >= 0) finish_term<MODE>(P, A, sink, K.term_cf, gsum<GS>(jcf), gl, active, p, s_counts);
+            if (K.term_cf >= 0)
+                finish_term<MODE>(P, A, sinkB, K.term_cf, gsum<kGroup>(jcf), ll, active, p, s_counts, real);
+            if (BSYNC >= 3) __syncthreads();
 
-            // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane (uniform)
+            // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the half
             if (K.term_kp >= 0 || K.term_kr >= 0) {
                 M34 Tp, Tg;
                 load_m34(Tp, ipose + 16 * K.kin_inst);
@@ -567,15 +594,15 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                 const float wn2 = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
                 const float wn = sqrtf(wn2);
                 const float erot = atan2f(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
-                if (K.term_kp >= 0) finish_term<MODE>(P, A, sink, K.term_kp, epos, gl, active, p, s_counts);
-                if (K.term_kr >= 0) finish_term<MODE>(P, A, sink, K.term_kr, erot, gl, active, p, s_counts);
+                if (K.term_kp >= 0) finish_term<MODE>(P, A, sinkB, K.term_kp, epos, ll, active, p, s_counts, real);
+                if (K.term_kr >= 0) finish_term<MODE>(P, A, sinkB, K.term_kr, erot, ll, active, p, s_counts, real);
                 if (GRAD) {
                     Wrench tw;   // on the target placement instance
                     tw.zero();
                     if (K.term_kp >= 0 && epos > 0.f) {
                         const float k = P.term_lam[K.term_kp] / epos;
                         const float fx = dx * k, fy = dy * k, fz = dz * k;      // dJ/dt_ee
-                        if (gl == kGroup - 1) link.add_point(Tee.t[0], Tee.t[1], Tee.t[2], fx, fy, fz);
+                        if (ll == kGroup - 1) link.add_point(Tee.t[0], Tee.t[1], Tee.t[2], fx, fy, fz);
                         tw.add_point(Ts.t[0], Ts.t[1], Ts.t[2], -fx, -fy, -fz);
                     }
                     if (K.term_kr >= 0 && wn > 0.f) {
@@ -584,13 +611,14 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                         const float ux = k * fmaf(Tee.r[0], wx, fmaf(Tee.r[1], wy, Tee.r[2] * wz));
                         const float uy = k * fmaf(Tee.r[3], wx, fmaf(Tee.r[4], wy, Tee.r[5] * wz));
                         const float uz = k * fmaf(Tee.r[6], wx, fmaf(Tee.r[7], wy, Tee.r[8] * wz));
-                        if (gl == kGroup - 1) { link.m[0] -= ux; link.m[1] -= uy; link.m[2] -= uz; }
+                        if (ll == kGroup - 1) { link.m[0] -= ux; link.m[1] -= uy; link.m[2] -= uz; }
                         tw.m[0] += ux; tw.m[1] += uy; tw.m[2] += uz;
                     }
-                    if (gl == 0 && P.inst[K.kin_inst].xoff >= 0) {
-                        float* dst = iwr + 8 * K.kin_inst;
-                        dst[0] += tw.f[0]; dst[1] += tw.f[1]; dst[2] += tw.f[2];
-                        dst[3] += tw.m[0]; dst[4] += tw.m[1]; dst[5] += tw.m[2];
+                    const bool movable = P.inst[K.kin_inst].xoff >= 0;
+#pragma unroll
+                    for (int h = 0; h < HP; ++h) {      // halves add one after the other (deterministic)
+                        if (half == h && ll == 0 && real && movable) add_wrench(iwr + 8 * K.kin_inst, tw);
+                        if (HP > 1) __syncwarp();
                     }
                 }
             }
@@ -598,20 +626,12 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
             // joint limits: dist_from_bounds(q, lo, hi)  (Listing 2; Motion P:1025)
             float ejl = 0.f, jl = 0.f;
             if (K.term_jl >= 0) {
-                ejl = gl < TAMP_NJ ? fmaxf(fmaxf(jlo - q, q - jhi), 0.f) : 0.f;
-                jl = sqrtf(gsum<GS>(ejl * ejl));
-                finish_term<MODE>(P, A, sink, K.term_jl, jl, gl, active, p, s_counts);
+                ejl = ll < TAMP_NJ ? fmaxf(fmaxf(jlo - q, q - jhi), 0.f) : 0.f;
+                jl = sqrtf(gsum<kGroup>(ejl * ejl));
+                finish_term<MODE>(P, A, sinkB, K.term_jl, jl, ll, active, p, s_counts, real);
             }
             if (GRAD) {
-                // sum the link's halves, then suffix sums of link wrenches over lanes >= l:
-                // dJ/dq = z . (M - o x F)
-                if (GS > kGroup) {
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        link.f[i] += __shfl_xor_sync(FULL, link.f[i], kGroup);
-                        link.m[i] += __shfl_xor_sync(FULL, link.m[i], kGroup);
-                    }
-                }
+                // suffix sums of link wrenches over lanes >= l: dJ/dq = z . (M - o x F)
 #pragma unroll
                 for (int d = 1; d < kGroup; d <<= 1) {
                     float v[6];
@@ -625,7 +645,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                         for (int i = 0; i < 3; ++i) { link.f[i] += v[i]; link.m[i] += v[3 + i]; }
                     }
                 }
-                if (gl < TAMP_NJ) {
+                if (ll < TAMP_NJ && real) {
                     const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
                     const float ox = T.t[0], oy = T.t[1], oz = T.t[2];
                     const float mx = link.m[0] - (oy * link.f[2] - oz * link.f[1]);
@@ -634,11 +654,21 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                     float dq = fmaf(zx, mx, fmaf(zy, my, zz * mz));
                     if (K.term_jl >= 0 && jl > 0.f && ejl > 0.f)
                         dq += P.term_lam[K.term_jl] * (q > jhi ? ejl : -ejl) / jl;
-                    gs[K.xoff + gl] += dq;
+                    gs[K.xoff + ll] += dq;
                 }
             }
-            if (BSYNC) __syncthreads();
+            // keep the block's warps in step through the (large) FK loop body (profiles/README.md)
+            if (BSYNC >= 2) __syncthreads();
         }
+        if (BSYNC == 1) phase_sync();   // all warps leave the FK loop before any enters phase C
+        // combine the halves' phase-B terms
+        if (HP > 1) {
+            sinkB.J += __shfl_xor_sync(FULL, sinkB.J, kGroup);
+            const unsigned bal = __ballot_sync(FULL, sinkB.sat);
+            sinkB.sat = ((bal >> (threadIdx.x & 31 & ~(GS - 1))) & ((1u << GS) - 1u)) == ((1u << GS) - 1u);
+        }
+        sink.J += sinkB.J;
+        sink.sat = sink.sat && sinkB.sat;
 
         // ---- phase C: StablePlace (support, containment) and CFreePlace per Place ----
         for (int pl = 0; pl < P.n_place; ++pl) {
@@ -944,6 +974,145 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
 }
 
 // ------------------------------------------------------------------------------------------------
+// K1b: conditional IK sampler -- damped least squares toward each Pick/Place conf's Kin target
+// T(p) T(g), one particle per 8-lane group (lane j = joint j+1, the same FK product scan as K2), then the
+// knots are re-interpolated from the refined endpoint confs.
+//   e = [t* - t_ee ; rotvec(R* R_ee^T)],  J = [z_j x (t_ee - o_j) ; z_j],  dq = J^T (J J^T + mu^2 I)^-1 e
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float y[6]) {
+    // A: packed lower triangle, row-major (i, j <= i) -> index i*(i+1)/2 + j.  In-place Cholesky.
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        float d = A[j * (j + 1) / 2 + j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) d = fmaf(-A[j * (j + 1) / 2 + k], A[j * (j + 1) / 2 + k], d);
+        const float ljj = sqrtf(fmaxf(d, 1e-30f));
+        const float inv = 1.f / ljj;
+        A[j * (j + 1) / 2 + j] = ljj;
+#pragma unroll
+        for (int i = j + 1; i < 6; ++i) {
+            float v = A[i * (i + 1) / 2 + j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v = fmaf(-A[i * (i + 1) / 2 + k], A[j * (j + 1) / 2 + k], v);
+            A[i * (i + 1) / 2 + j] = v * inv;
+        }
+    }
+    float z[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {     // L z = b
+        float v = b[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v = fmaf(-A[i * (i + 1) / 2 + k], z[k], v);
+        z[i] = v / A[i * (i + 1) / 2 + i];
+    }
+#pragma unroll
+    for (int i = 5; i >= 0; --i) {    // L^T y = z
+        float v = z[i];
+#pragma unroll
+        for (int k = i + 1; k < 6; ++k) v = fmaf(-A[k * (k + 1) / 2 + i], y[k], v);
+        y[i] = v / A[i * (i + 1) / 2 + i];
+    }
+}
+
+__global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, float* __restrict__ x,
+                                            const float* __restrict__ grasp, int64_t n, int iters, float damp2) {
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / kGroup) + threadIdx.x / kGroup;
+    const bool active = pid < n;
+    const int64_t p = active ? pid : (n - 1);
+    const int D = P.D;
+    float* xp = x + p * D;
+    M34 F;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        F.r[3 * i] = P.F[gl][4 * i]; F.r[3 * i + 1] = P.F[gl][4 * i + 1];
+        F.r[3 * i + 2] = P.F[gl][4 * i + 2]; F.t[i] = P.F[gl][4 * i + 3];
+    }
+    const float jlo = gl < TAMP_NJ ? P.jlo[gl] : 0.f;
+    const float jhi = gl < TAMP_NJ ? P.jhi[gl] : 0.f;
+    for (int f = 0; f < P.n_fk; ++f) {
+        const KFk K = P.fk[f];
+        if ((K.term_kp < 0 && K.term_kr < 0) || K.ghost) continue;
+        // Kin target T* = T(p) T(g)
+        const KInst& I = P.inst[K.kin_inst];
+        float pp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pp[k] = I.xoff >= 0 ? xp[I.xoff + k] : I.pose[k];
+        float sy, cy;
+        fsincos(pp[3], &sy, &cy);
+        M34 Tp, Tg;
+        Tp.r[0] = cy; Tp.r[1] = -sy; Tp.r[2] = 0.f; Tp.r[3] = sy; Tp.r[4] = cy; Tp.r[5] = 0.f;
+        Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f; Tp.t[0] = pp[0]; Tp.t[1] = pp[1]; Tp.t[2] = pp[2];
+        load_m34(Tg, grasp + (p * P.n_grasp + K.kin_grasp) * 12);
+        const M34 Ts = compose(Tp, Tg);
+        float q = gl < TAMP_NJ ? xp[K.xoff + gl] : 0.f;
+        for (int it = 0; it < iters; ++it) {
+            M34 T;
+            {
+                float s, c;
+                fsincos(q, &s, &c);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    T.r[3 * i] = fmaf(F.r[3 * i], c, F.r[3 * i + 1] * s);
+                    T.r[3 * i + 1] = fmaf(F.r[3 * i + 1], c, -F.r[3 * i] * s);
+                    T.r[3 * i + 2] = F.r[3 * i + 2];
+                    T.t[i] = F.t[i];
+                }
+            }
+#pragma unroll
+            for (int d = 1; d < kGroup; d <<= 1) {
+                const M34 U = shfl_up_m34(T, d);
+                if (gl >= d) T = compose(U, T);
+            }
+            const M34 Tee = shfl_m34(T, kGroup - 1);
+            float e[6];
+            e[0] = Ts.t[0] - Tee.t[0]; e[1] = Ts.t[1] - Tee.t[1]; e[2] = Ts.t[2] - Tee.t[2];
+            float E[9];   // R* R_ee^T
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    E[3 * i + j] = fmaf(Ts.r[3 * i], Tee.r[3 * j], fmaf(Ts.r[3 * i + 1], Tee.r[3 * j + 1], Ts.r[3 * i + 2] * Tee.r[3 * j + 2]));
+            const float wx = E[7] - E[5], wy = E[2] - E[6], wz = E[3] - E[1];
+            const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
+            const float th = atan2f(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
+            const float k = wn > 0.f ? th / wn : 0.f;
+            e[3] = wx * k; e[4] = wy * k; e[5] = wz * k;
+            // Jacobian column of my joint
+            float c[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (gl < TAMP_NJ) {
+                const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
+                const float rx = Tee.t[0] - T.t[0], ry = Tee.t[1] - T.t[1], rz = Tee.t[2] - T.t[2];
+                c[0] = zy * rz - zz * ry; c[1] = zz * rx - zx * rz; c[2] = zx * ry - zy * rx;
+                c[3] = zx; c[4] = zy; c[5] = zz;
+            }
+            float A[21];
+#pragma unroll
+            for (int i = 0; i < 6; ++i)
+#pragma unroll
+                for (int j = 0; j <= i; ++j) A[i * (i + 1) / 2 + j] = gsum<kGroup>(c[i] * c[j]) + (i == j ? damp2 : 0.f);
+            float y[6];
+            chol6_solve(A, e, y);
+            const float dq = fmaf(c[0], y[0], fmaf(c[1], y[1], fmaf(c[2], y[2], fmaf(c[3], y[3], fmaf(c[4], y[4], c[5] * y[5])))));
+            if (gl < TAMP_NJ) q = fminf(fmaxf(q + dq, jlo), jhi);
+        }
+        if (gl < TAMP_NJ && active) xp[K.xoff + gl] = q;
+        __syncwarp();
+    }
+    // knots: linear interpolation between the (refined) endpoint confs
+    for (int tr = 0; tr < P.n_traj; ++tr) {
+        const KTraj& Tj = P.traj[tr];
+        if (gl >= TAMP_NJ || !active) continue;
+        const float qa = Tj.q1_xoff >= 0 ? xp[Tj.q1_xoff + gl] : P.const_conf[Tj.q1_const][gl];
+        const float qb = Tj.q2_xoff >= 0 ? xp[Tj.q2_xoff + gl] : P.const_conf[Tj.q2_const][gl];
+        for (int j = 0; j < Tj.n_knots; ++j) {
+            const float a = (float)(j + 1) / (float)(Tj.n_knots + 1);
+            xp[Tj.knot_xoff + 7 * j + gl] = qa + a * (qb - qa);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // K4 / K5: best-k (key = class | ordered cost | global index)
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t ordered_bits(float f) {
@@ -1044,7 +1213,7 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
 static inline void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-template <int MODE, int GS, bool BSYNC>
+template <int MODE, int GS, int BSYNC>
 static cudaError_t launch_particle_t(const KProgram& P, const KArgs& A, int threads, size_t smem, cudaStream_t st) {
     auto fn = k_particle<MODE, 0, GS, BSYNC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1056,23 +1225,47 @@ static cudaError_t launch_particle_t(const KProgram& P, const KArgs& A, int thre
     return cudaGetLastError();
 }
 
-template <int GS, bool BSYNC>
-static cudaError_t launch_particle_gs(int mode, const KProgram& P, const KArgs& A, int threads, size_t smem,
+template <int GS>
+static cudaError_t launch_particle_gs(int mode, int bsync, const KProgram& P, const KArgs& A, int threads, size_t smem,
                                       cudaStream_t st) {
-    if (mode == MODE_OPT) return launch_particle_t<MODE_OPT, GS, BSYNC>(P, A, threads, smem, st);
-    if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, GS, BSYNC>(P, A, threads, smem, st);
-    return launch_particle_t<MODE_CHECK, GS, BSYNC>(P, A, threads, smem, st);
+    if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, GS, 2>(P, A, threads, smem, st);
+    if (mode == MODE_CHECK) {
+        if (bsync == 0) return launch_particle_t<MODE_CHECK, GS, 0>(P, A, threads, smem, st);
+        return launch_particle_t<MODE_CHECK, GS, 2>(P, A, threads, smem, st);
+    }
+    switch (bsync) {
+        case 0: return launch_particle_t<MODE_OPT, GS, 0>(P, A, threads, smem, st);
+        case 1: return launch_particle_t<MODE_OPT, GS, 1>(P, A, threads, smem, st);
+        case 3: return launch_particle_t<MODE_OPT, GS, 3>(P, A, threads, smem, st);
+        default: return launch_particle_t<MODE_OPT, GS, 2>(P, A, threads, smem, st);
+    }
+}
+
+// registers per thread of the hot kernel (for the launch-configuration policy)
+int particle_kernel_regs(int gs) {
+    cudaFuncAttributes a;
+    cudaError_t e = gs == 16 ? cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 0, 16, 1>)
+                             : cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 0, 8, 1>);
+    if (e != cudaSuccess) { cudaGetLastError(); return 80; }
+    return a.numRegs;
 }
 
 // gs = lanes per particle (8 or 16); threads = block size (multiple of 32, <= 768); smem sized for
-// threads / gs particles.  bsync = block-synchronous phases.
-cudaError_t launch_particle(int mode, int gs, bool bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
+// threads / gs particles.  bsync = block-synchronisation level (see k_particle).
+cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
                             cudaStream_t st) {
     if (A.n <= 0) return cudaSuccess;
-    if (gs == 16) return bsync ? launch_particle_gs<16, true>(mode, P, A, threads, smem, st)
-                               : launch_particle_gs<16, false>(mode, P, A, threads, smem, st);
-    return bsync ? launch_particle_gs<8, true>(mode, P, A, threads, smem, st)
-                 : launch_particle_gs<8, false>(mode, P, A, threads, smem, st);
+    if (gs == 16) return launch_particle_gs<16>(mode, bsync, P, A, threads, smem, st);
+    return launch_particle_gs<8>(mode, bsync, P, A, threads, smem, st);
+}
+
+cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
+                      cudaStream_t st) {
+    if (n <= 0 || iters <= 0) return cudaSuccess;
+    const int per_block = 128 / kGroup;
+    k_ik<<<(unsigned)((n + per_block - 1) / per_block), 128, 0, st>>>(P, x, grasp, n, iters, damping * damping);
+    counted();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,

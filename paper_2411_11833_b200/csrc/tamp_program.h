@@ -29,6 +29,7 @@ struct KFk {
     int16_t held_obj;                 // object id of the held object
     int16_t part_begin, part_count;   // collision partner instances: partners[part_begin ...]
     uint16_t obb_mask;                // OBBs checked against the robot (and held object)
+    int16_t ghost;                    // 1 = padding copy of its pair partner (results discarded)
 };
 
 // An object at a pose: constant (xoff < 0, pose[]) or a placement variable at x[xoff .. xoff+4).

@@ -79,7 +79,8 @@ class ProblemDesc(ctypes.Structure):
                 ("lam_goal", F), ("lam_traj", F), ("eta", F),
                 ("beta1", F), ("beta2", F), ("adam_eps", F),
                 ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F),
-                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32)]
+                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32),
+                ("ik_iters", I32), ("ik_damping", F)]
 
 
 class Info(ctypes.Structure):
@@ -217,6 +218,8 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
     d.lanes_per_particle = int(lanes_per_particle)
     d.block_threads = int(block_threads)
     d.block_sync = int(block_sync)
+    d.ik_iters = int(getattr(spec, "ik_iters", 0))
+    d.ik_damping = float(getattr(spec, "ik_damping", 0.1))
     return d
 
 
