@@ -357,8 +357,18 @@ def main():
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = nsm * 128 * sm_max * 1e6 / 1e12
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        ent = tj.get(f"config{cfg}:{n}")
+        if ent and args.check_every == 10:
+            traffic = ent["dram_read"] + ent["dram_write"]
+    except Exception:
+        pass
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinstr/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "k_particle<MODE_OPT>",
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu, profiles/ncu_traffic.json)",
+            "algorithmic_bytes_per_launch": n * (2 * 3 * ctx.D * 4 + 48 * ctx.n_grasp),
+            "kernel": "k_particle<MODE_OPT>",
             "note": f"FP32-pipe instructions (FFMA=1) of the minimal per-unit evaluation, {instr} per particle-step; "
                     f"peak = {nsm} SM x 128 lanes x {sm_max:.0f} MHz ({src} sm_max_mhz)"}
     if clocks:

@@ -717,18 +717,24 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
                 c->threads = (int)std::max<int64_t>(pp, 4 * ppw) * c->gs;
             } else {
                 const int regs = std::max(32, particle_kernel_regs(c->gs));
-                int best_t = 128, best_score = -1;
-                for (int t = 128; t <= 768; t += 32) {
+                auto blocks_per_sm = [&](int t) {
                     const int ppb = t / c->gs;
-                    if (ppb % ppw || ppb > max_pp) continue;
                     const int by_regs = 65536 / (((regs + 7) & ~7) * t);
                     const int by_smem = (smem_optin + 1024) / (ppb * c->stride_bytes + static_smem + 1024);
-                    const int blocks = std::min(std::min(by_regs, by_smem), 32);
-                    if (blocks < 1) continue;
-                    const int score = 8 * blocks * (t / 32) + (blocks == 2 ? 4 : 0) + (blocks >= 2 ? 2 : 0);
-                    if (score > best_score) { best_score = score; best_t = t; }
+                    return std::min(std::min(by_regs, by_smem), 32);
+                };
+                if (384 / c->gs <= max_pp && blocks_per_sm(384) >= 2) {
+                    c->threads = 384;                                       // config 1 sweet spot
+                } else {                                                    // max resident warps per SM
+                    int best_t = 128, best_w = -1;
+                    for (int t = 128; t <= 768; t += 32) {
+                        const int ppb = t / c->gs;
+                        if (ppb % ppw || ppb > max_pp) continue;
+                        const int w = blocks_per_sm(t) * (t / 32);
+                        if (w >= best_w) { best_w = w; best_t = t; }
+                    }
+                    c->threads = best_t;
                 }
-                c->threads = best_t;
             }
         }
         if (c->threads / c->gs > max_pp) {

@@ -134,7 +134,7 @@ class ProblemSpec:
     # conditional IK sampler in InitializeParticles: damped-least-squares iterations (0 = uniform
     # confs only, the paper's `Optimization` baseline init)
     ik_iters: int = 0
-    ik_damping: float = 0.05
+    ik_damping: float = 0.1
 
 
 DEFAULT_LAM = dict(JL=1.0, CF=1.0, KP=1.0, KR=5.0, SS=2.0, SC=2.0, CP=1.0)
