@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--lanes", type=int, default=0, help="lanes per particle in the particle kernel (0 = auto)")
     p.add_argument("--block-threads", type=int, default=0, help="particle-kernel block size (0 = auto)")
     p.add_argument("--block-sync", type=int, default=-1, help="block-synchronous phases (1/0, -1 = auto)")
-    p.add_argument("--ik-iters", type=int, default=30,
+    p.add_argument("--ik-iters", type=int, default=20,
                    help="conditional IK sampler iterations in InitializeParticles (P:521); 0 = uniform confs")
     return p.parse_args()
 

@@ -234,6 +234,11 @@ tamp_status tamp_get_state(tamp_ctx* ctx, float* x, float* m, float* v, float* g
 tamp_status tamp_set_state(tamp_ctx* ctx, const float* x, const float* m, const float* v,
                            const float* grasp, const uint8_t* invalid, int32_t t, void* stream);
 
+/* Plan-feasibility heuristic (Eq. 5) from the satisfied counts of tamp_check_satisfied (host
+   pointer, all-reduced over ranks): H = (1/n_hard) sum_c h_c, h_c = counts[c] if counts[c] > 0 else
+   penalty (Lambda_penalty, "a large negative penalty").  n_hard = 0 -> 0. */
+double tamp_plan_heuristic(const int32_t* counts, int32_t n_hard, double penalty);
+
 void tamp_destroy(tamp_ctx* ctx);
 
 #ifdef __cplusplus

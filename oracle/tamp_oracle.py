@@ -576,6 +576,14 @@ def check(spec, csp, st: State):
     return cls, counts, J, soft, Jc
 
 
+def plan_heuristic(counts, penalty):
+    """Eq. 5: H = 1/|con| sum_c h(P, c), h = Lambda_penalty if n_satisfying(c) = 0 else n_satisfying(c)."""
+    counts = list(counts)
+    if not counts:
+        return 0.0
+    return sum(penalty if n == 0 else n for n in counts) / len(counts)
+
+
 def best_k(cls, J, soft, gidx, k):
     """Key (class, cost, global index) ascending; cost = soft plan cost if satisfying else J (L19)."""
     cost = np.where(cls == 0, soft, np.where(cls == 1, J, 0.0))

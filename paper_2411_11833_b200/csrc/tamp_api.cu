@@ -975,6 +975,13 @@ tamp_status tamp_set_state(tamp_ctx* c, const float* x, const float* m, const fl
     return TAMP_OK;
 }
 
+double tamp_plan_heuristic(const int32_t* counts, int32_t n_hard, double penalty) {
+    if (!counts || n_hard <= 0) return 0.0;
+    double h = 0.0;
+    for (int32_t c = 0; c < n_hard; ++c) h += counts[c] > 0 ? (double)counts[c] : penalty;
+    return h / n_hard;
+}
+
 void tamp_destroy(tamp_ctx* c) { delete c; }
 
 }  // extern "C"

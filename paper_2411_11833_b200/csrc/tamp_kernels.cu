@@ -1231,6 +1231,7 @@ static cudaError_t launch_particle_gs(int mode, int bsync, const KProgram& P, co
     if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, GS, 2>(P, A, threads, smem, st);
     if (mode == MODE_CHECK) {
         if (bsync == 0) return launch_particle_t<MODE_CHECK, GS, 0>(P, A, threads, smem, st);
+        if (bsync == 1) return launch_particle_t<MODE_CHECK, GS, 1>(P, A, threads, smem, st);
         return launch_particle_t<MODE_CHECK, GS, 2>(P, A, threads, smem, st);
     }
     switch (bsync) {

@@ -94,7 +94,7 @@ class Info(ctypes.Structure):
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
            "tamp_init_problem", "tamp_get_info", "tamp_sample_particles", "tamp_optimize_step",
            "tamp_check_satisfied", "tamp_best_k", "tamp_merge_best_k", "tamp_eval", "tamp_get_state",
-           "tamp_set_state", "tamp_destroy", "tamp_kernel_launches"]
+           "tamp_set_state", "tamp_destroy", "tamp_kernel_launches", "tamp_plan_heuristic"]
 
 _lib = None
 
@@ -125,6 +125,8 @@ def load(path: str = LIB_PATH):
     lib.tamp_set_state.argtypes = [vp, vp, vp, vp, vp, vp, I32, vp]
     lib.tamp_destroy.argtypes = [vp]
     lib.tamp_kernel_launches.restype = ctypes.c_uint64
+    lib.tamp_plan_heuristic.restype = ctypes.c_double
+    lib.tamp_plan_heuristic.argtypes = [vp, I32, ctypes.c_double]
     for name in EXPORTS[4:15]:
         getattr(lib, name).restype = ctypes.c_int
     if lib.tamp_abi_version() != ABI_VERSION:
@@ -332,6 +334,12 @@ class TampContext:
         self._keep = (x, m, v, grasp, invalid)       # host tensors must outlive the async copy
         _check(self.lib.tamp_set_state(self.h, _ptr(x), _ptr(m), _ptr(v), _ptr(grasp), _ptr(invalid), int(t),
                                        _stream(self.device, stream)))
+
+
+def plan_heuristic(counts, n_hard: int, penalty: float = -1e6) -> float:
+    """Eq. 5 plan-feasibility heuristic from (all-reduced) satisfied counts (host)."""
+    c = np.ascontiguousarray(np.asarray(counts if not torch.is_tensor(counts) else counts.cpu().numpy(), dtype=np.int32))
+    return float(load().tamp_plan_heuristic(c.ctypes.data_as(ctypes.c_void_p), int(n_hard), float(penalty)))
 
 
 def kernel_launches() -> int:

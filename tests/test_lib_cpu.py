@@ -6,6 +6,7 @@ import math
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_2411_11833_b200 as pkg
@@ -86,3 +87,12 @@ def test_product_path_fails_loudly_without_library(tmp_path):
             T.load(str(tmp_path / "missing.so"))
         finally:
             T._lib = T._lib_backup
+
+
+def test_plan_heuristic_matches_oracle(lib):
+    from oracle import tamp_oracle as O
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        c = rng.integers(0, 5, size=rng.integers(1, 40))
+        assert pkg.plan_heuristic(c, len(c), -1e3) == pytest.approx(O.plan_heuristic(c, -1e3), rel=1e-12)
+    assert pkg.plan_heuristic([10, 5, 0, 0], 2, -1.0) == 7.5

@@ -402,3 +402,9 @@ def test_ik_initialisation_improves_kin_residuals():
     _, Jc1, _ = _eval(spec, csp, x1, g1)
     assert np.median(Jc1[:, 2]) < 0.1 * np.median(Jc0[:, 2])
     assert ((Jc1[:, 2] <= 5e-3) & (Jc1[:, 3] <= 0.05)).mean() > 0.25
+
+
+def test_plan_heuristic_eq5():
+    """counts [10, 5] -> H = 7.5; a zero count takes the penalty."""
+    assert O.plan_heuristic([10, 5], -100.0) == 7.5
+    assert O.plan_heuristic([10, 0], -100.0) == -45.0
