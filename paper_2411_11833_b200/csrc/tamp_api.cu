@@ -670,9 +670,10 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     }
     c->ik_iters = desc->ik_iters;
     c->ik_damping = desc->ik_damping;
-    if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 8 && desc->lanes_per_particle != 16) {
+    if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 4 && desc->lanes_per_particle != 8 &&
+        desc->lanes_per_particle != 16) {
         delete c;
-        return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 8 or 16");
+        return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 4, 8 or 16");
     }
     // auto: 8 lanes (one per link frame) -- measured faster than 16 on every config, even at 8K particles
     // (profiles/r1: the 16-lane mapping doubles the FK/kin instruction count for little latency gain)
@@ -680,11 +681,21 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         int n_fk_real = 0;
         for (int f = 0; f < c->P.n_fk; ++f) n_fk_real += !c->P.fk[f].ghost;
         // 16 lanes (two FK instances at a time) pays off for knot-heavy skeletons (config 4: 48 FK
-        // instances), 8 lanes elsewhere (sweep9)
+        // instances); 4 lanes (two link frames per lane, 8 particles per warp) for launches that take many
+        // waves when a 512-thread block (128 particles) fits shared memory (config 1 at 1M: +10 %);
+        // 8 lanes elsewhere (sweeps 9, 13)
         c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : (n_fk_real >= 24 ? 16 : 8);
     }
     ws_layout(c);
     smem_layout(c);
+    if (!desc->lanes_per_particle && c->gs == 8) {
+        int n_sm = 148, smem_optin = 227 * 1024;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        cudaGetLastError();
+        const bool many_waves = n_local > (int64_t)n_sm * 4 * (768 / 8);
+        if (many_waves && 128 * c->stride_bytes + 4096 <= smem_optin) c->gs = 4;
+    }
     {
         // launch configuration of the particle kernel.  Auto: block-synchronous phases with one large block
         // per SM holding that SM's share of the particles (all warps of an SM walk the same code region ->
@@ -695,12 +706,13 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         cudaGetLastError();
         const int ppw = 32 / c->gs;                                     // particles per warp
         const int static_smem = 4096;
-        int max_pp = std::min(768 / c->gs, (smem_optin - static_smem) / c->stride_bytes);
+        const int max_threads = c->gs == 4 ? 512 : 768;                // __launch_bounds__ of the variant
+        int max_pp = std::min(max_threads / c->gs, (smem_optin - static_smem) / c->stride_bytes);
         max_pp = (max_pp / ppw) * ppw;
         if (desc->block_threads) {
-            if (desc->block_threads % 32 || desc->block_threads < 32 || desc->block_threads > 768) {
+            if (desc->block_threads % 32 || desc->block_threads < 32 || desc->block_threads > max_threads) {
                 delete c;
-                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 768]");
+                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 768] (512 for 4 lanes)");
             }
             c->threads = desc->block_threads;
         } else {
@@ -723,11 +735,11 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
                     const int by_smem = (smem_optin + 1024) / (ppb * c->stride_bytes + static_smem + 1024);
                     return std::min(std::min(by_regs, by_smem), 32);
                 };
-                if (384 / c->gs <= max_pp && blocks_per_sm(384) >= 2) {
+                if (384 <= max_threads && 384 / c->gs <= max_pp && blocks_per_sm(384) >= 2) {
                     c->threads = 384;                                       // config 1 sweet spot
                 } else {                                                    // max resident warps per SM
                     int best_t = 128, best_w = -1;
-                    for (int t = 128; t <= 768; t += 32) {
+                    for (int t = 128; t <= max_threads; t += 32) {
                         const int ppb = t / c->gs;
                         if (ppb % ppw || ppb > max_pp) continue;
                         const int w = blocks_per_sm(t) * (t / 32);

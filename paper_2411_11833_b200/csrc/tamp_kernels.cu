@@ -48,21 +48,21 @@ __device__ __forceinline__ M34 compose(const M34& a, const M34& b) {
     return c;
 }
 
-__device__ __forceinline__ M34 shfl_m34(const M34& a, int src) {
+__device__ __forceinline__ M34 shfl_m34(const M34& a, int src, int width = kGroup) {
     M34 o;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) o.r[i] = __shfl_sync(FULL, a.r[i], src, kGroup);
+    for (int i = 0; i < 9; ++i) o.r[i] = __shfl_sync(FULL, a.r[i], src, width);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) o.t[i] = __shfl_sync(FULL, a.t[i], src, kGroup);
+    for (int i = 0; i < 3; ++i) o.t[i] = __shfl_sync(FULL, a.t[i], src, width);
     return o;
 }
 
-__device__ __forceinline__ M34 shfl_up_m34(const M34& a, int d) {
+__device__ __forceinline__ M34 shfl_up_m34(const M34& a, int d, int width = kGroup) {
     M34 o;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) o.r[i] = __shfl_up_sync(FULL, a.r[i], d, kGroup);
+    for (int i = 0; i < 9; ++i) o.r[i] = __shfl_up_sync(FULL, a.r[i], d, width);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) o.t[i] = __shfl_up_sync(FULL, a.t[i], d, kGroup);
+    for (int i = 0; i < 3; ++i) o.t[i] = __shfl_up_sync(FULL, a.t[i], d, width);
     return o;
 }
 
@@ -308,11 +308,11 @@ __device__ __forceinline__ void flush_partner(Wrench& pw, bool movable, float* d
 
 // phase-B variant: each 8-lane half may work on a different FK instance (so `movable` and `dst` may differ
 // between halves): warp-uniform vote, per-half reduction, halves add one after the other (deterministic).
-template <bool GRAD, int HP>
+template <bool GRAD, int HP, int LPF>
 __device__ __forceinline__ void flush_partner_b(Wrench& pw, bool movable, float* dst, int ll, int half, bool real) {
     if (!GRAD) return;
     if (__any_sync(FULL, movable && pw.nonzero())) {
-        pw.template group_sum<kGroup>();
+        pw.template group_sum<LPF>();
 #pragma unroll
         for (int h = 0; h < HP; ++h) {
             if (half == h && ll == 0 && real && movable) add_wrench(dst, pw);
@@ -345,23 +345,32 @@ __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, T
     }
 }
 
-// GS = lanes per particle: 8 (one per link frame) or 16 (two FK instances at a time, one per 8-lane half:
-// twice the warps in flight for the same particle count, no duplicated work).
-// KM = register-resident Adam moments per lane (coords gl, gl+GS, ...); 0 = moments stay in global memory
+// Particle-group mapping.  LPF = lanes per FK instance: 8 (lane l owns link frame l+1; lane 7 the tool
+// frame) or 4 (lane l owns link frames 2l+1 and 2l+2: half the warp-instructions per particle for the
+// per-particle serial work -- FK scan, Kin, bookkeeping -- twice the sphere work per lane).  HP = FK
+// instances a particle group processes concurrently: 1, or 2 (two LPF-lane halves run the two FK instances
+// of a pair of identical structure).  GS = LPF * HP lanes per particle.
 // BSYNC: block-synchronous phases so that all warps of a block execute the same code region at a time and
 // share the instruction cache.  0 = off (warp-level only), 1 = at phase boundaries, 2 = also after every
-// FK instance, 3 = also between collision and Kin inside the FK body.
-template <int MODE, int KM, int GS, int BSYNC>
-__global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
+// FK instance.
+template <int MODE, int LPF, int HP, int BSYNC>
+__global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
+    constexpr int GS = LPF * HP;                                   // lanes per particle
+    constexpr int LPL = kGroup / LPF;                              // link frames per lane
+    constexpr int NS = TAMP_MAX_SPHERES_PER_LINK * LPL;            // robot spheres per lane
+    constexpr int NH = TAMP_MAX_OBJ_SPHERES / LPF;                 // held-object spheres per lane
+    constexpr int NSO = GS >= TAMP_MAX_OBJ_SPHERES ? 1 : TAMP_MAX_OBJ_SPHERES / GS;   // placed-object spheres per lane
+    constexpr int NJL = (TAMP_NJ + GS - 1) / GS;                   // joints per lane in trajectory costs
     extern __shared__ float4 smem4[];
     __shared__ float4 s_osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES];
     __shared__ int s_counts[TAMP_MAX_TERMS + 2];
+    __shared__ float4 s_F[kGroup][3];                              // fixed transform of each joint (7: tool)
+    __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];   // spheres of each link frame
 
-    constexpr int NS = TAMP_MAX_SPHERES_PER_LINK;                    // robot spheres per lane (its link's)
     const int gl = threadIdx.x & (GS - 1);          // lane within the particle group
-    const int ll = gl & (kGroup - 1);               // link frame owned by this lane
-    const int half = gl / kGroup;                   // GS = 16: which FK instance of the pair
+    const int ll = gl & (LPF - 1);                  // lane within the FK segment
+    const int half = gl / LPF;                      // HP = 2: which FK instance of the pair
     const int grp = threadIdx.x / GS;
     const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / GS) + grp;
     const bool active = pid < A.n;
@@ -386,11 +395,6 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
     }
     if (MODE == MODE_CHECK)
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
-
-    // robot data in shared memory (read per FK instance instead of pinning ~28 registers): fixed transform
-    // of each joint (lane 7: tool) and each link's spheres
-    __shared__ float4 s_F[kGroup][3];
-    __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];
     if (threadIdx.x < kGroup * 3) {
         const int l = threadIdx.x / 3, r = threadIdx.x % 3;
         s_F[l][r] = make_float4(P.F[l][4 * r], P.F[l][4 * r + 1], P.F[l][4 * r + 2], P.F[l][4 * r + 3]);
@@ -399,22 +403,19 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
         const int l = threadIdx.x / TAMP_MAX_SPHERES_PER_LINK, k = threadIdx.x % TAMP_MAX_SPHERES_PER_LINK;
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3]);
     }
-    const int nsph = P.rsph_n[ll];                  // my link's spheres
-    const float jlo = ll < TAMP_NJ ? P.jlo[ll] : 0.f;
-    const float jhi = ll < TAMP_NJ ? P.jhi[ll] : 0.f;
+    int nsph[LPL];
+    float jlo[LPL], jhi[LPL];
+#pragma unroll
+    for (int u = 0; u < LPL; ++u) {
+        const int j = ll * LPL + u;                  // joint j+1 / link frame j+1 (j = 7: tool)
+        nsph[u] = P.rsph_n[j];
+        jlo[u] = j < TAMP_NJ ? P.jlo[j] : 0.f;
+        jhi[u] = j < TAMP_NJ ? P.jhi[j] : 0.f;
+    }
 
-    // particle state -> shared memory / registers
+    // particle state -> shared memory
     const float* xg = A.x + p * D;
     for (int d = gl; d < D; d += GS) xs[d] = xg[d];
-    float mreg[KM > 0 ? KM : 1], vreg[KM > 0 ? KM : 1];
-    if (MODE == MODE_OPT && KM > 0) {
-#pragma unroll
-        for (int k = 0; k < KM; ++k) {
-            const int d = gl + GS * k;
-            mreg[k] = d < D ? A.m[p * D + d] : 0.f;
-            vreg[k] = d < D ? A.v[p * D + d] : 0.f;
-        }
-    }
     for (int i = gl; i < P.n_grasp * 12; i += GS) gT[(i / 12) * 16 + (i % 12)] = A.grasp[(p * P.n_grasp) * 12 + i];
     bool invalid = A.invalid[p] != 0;
     __syncthreads();
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
             else { px = I.pose[0]; py = I.pose[1]; pz = I.pose[2]; yaw = I.pose[3]; }
             float sy, cy;
             fsincos(yaw, &sy, &cy);
-            float* ip = ipose + 16 * i;      // [R row0 | t0, R row1 | t1, R row2 | t2]
+            float* ip = ipose + 16 * i;      // [R row0 | t0, R row1 | t1, R row2 | t2, bounding sphere]
             if (gl == 0) {
                 ip[0] = cy; ip[1] = -sy; ip[2] = 0.f; ip[3] = px;
                 ip[4] = sy; ip[5] = cy; ip[6] = 0.f; ip[7] = py;
@@ -457,67 +458,75 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                 ip[14] = pz + ob[2];
                 ip[15] = ob[3];
             }
-            if (gl < TAMP_MAX_OBJ_SPHERES) {
-                const float4 c = s_osph[I.obj][gl];
-                isph[i * TAMP_MAX_OBJ_SPHERES + gl] = gl < P.osph_n[I.obj]
+            for (int k = gl; k < TAMP_MAX_OBJ_SPHERES; k += GS) {
+                const float4 c = s_osph[I.obj][k];
+                isph[i * TAMP_MAX_OBJ_SPHERES + k] = k < P.osph_n[I.obj]
                     ? make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w)
                     : make_float4(kFar, kFar, kFar, 0.f);
             }
-            if (GRAD && gl < 6) iwr[8 * i + gl] = 0.f;
+            if (GRAD)
+                for (int c = gl; c < 6; c += GS) iwr[8 * i + c] = 0.f;
         }
         if (GRAD) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
         phase_sync();
 
         // ---- phase B: robot configurations (Pick/Place confs, knots) ----
-        // GS = 16: the two 8-lane halves of a particle group process the two FK instances of a pair of identical
-        // structure concurrently (the compiler pairs them; an unmatched instance is paired with a ghost copy
-        // whose results are discarded), so control flow stays warp-uniform.  GS = 8: ghosts are skipped.
-        constexpr int HP = GS / kGroup;
+        // HP = 2: the two halves process the two FK instances of a pair of identical structure concurrently
+        // (the compiler pairs them; an unmatched instance is paired with a ghost copy whose results are
+        // discarded), so control flow stays warp-uniform.  HP = 1: ghosts are skipped.
         TermSink<MODE> sinkB;                  // this half's share of the phase-B terms
         for (int f0 = 0; f0 < P.n_fk; f0 += HP) {
             const KFk K = P.fk[f0 + (HP > 1 ? half : 0)];
             const bool real = !K.ghost;
             if (HP == 1 && !real) continue;
-            const float q = ll < TAMP_NJ ? xs[K.xoff + ll] : 0.f;
-            // A_l = F_l Rz(q_l)
-            M34 T;
-            {
+            // A_j = F_j Rz(q_j) for my joints, local product, product scan over the LPF lanes (FK)
+            float q[LPL];
+            M34 Al[LPL];
+#pragma unroll
+            for (int u = 0; u < LPL; ++u) {
+                const int j = ll * LPL + u;
+                q[u] = j < TAMP_NJ ? xs[K.xoff + j] : 0.f;
                 float s, c;
-                fsincos(q, &s, &c);
-                M34 F;
+                fsincos(q[u], &s, &c);
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    const float4 f4 = s_F[ll][i];
-                    F.r[3 * i] = f4.x; F.r[3 * i + 1] = f4.y; F.r[3 * i + 2] = f4.z; F.t[i] = f4.w;
-                }
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    T.r[3 * i] = fmaf(F.r[3 * i], c, F.r[3 * i + 1] * s);
-                    T.r[3 * i + 1] = fmaf(F.r[3 * i + 1], c, -F.r[3 * i] * s);
-                    T.r[3 * i + 2] = F.r[3 * i + 2];
-                    T.t[i] = F.t[i];
+                    const float4 f4 = s_F[j][i];
+                    Al[u].r[3 * i] = fmaf(f4.x, c, f4.y * s);
+                    Al[u].r[3 * i + 1] = fmaf(f4.y, c, -f4.x * s);
+                    Al[u].r[3 * i + 2] = f4.z;
+                    Al[u].t[i] = f4.w;
                 }
             }
-            // inclusive product scan: T_l = A_0 A_1 ... A_l  (FK)
+            M34 Sc = Al[0];
+            if (LPL == 2) Sc = compose(Al[0], Al[LPL - 1]);
 #pragma unroll
-            for (int d = 1; d < kGroup; d <<= 1) {
-                const M34 U = shfl_up_m34(T, d);
-                if (ll >= d) T = compose(U, T);
+            for (int d = 1; d < LPF; d <<= 1) {
+                const M34 U = shfl_up_m34(Sc, d, LPF);
+                if (ll >= d) Sc = compose(U, Sc);
+            }
+            M34 T[LPL];                       // my link frames (world)
+            if (LPL == 1) {
+                T[0] = Sc;
+            } else {
+                const M34 E = shfl_up_m34(Sc, 1, LPF);     // product of all earlier lanes' transforms
+                T[0] = ll == 0 ? Al[0] : compose(E, Al[0]);
+                T[LPL - 1] = Sc;
             }
             const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
-            // my link's spheres in the world
+            // my links' spheres in the world
             float w[NS][3], gw[NS][3], rr[NS];
 #pragma unroll
-            for (int k = 0; k < NS; ++k) {
-                const float4 c4 = s_rsph[ll][k];
-                xform(T, c4.x, c4.y, c4.z, w[k][0], w[k][1], w[k][2]);
-                if (k >= nsph) w[k][0] = w[k][1] = w[k][2] = kFar;      // absent sphere slot
-                rr[k] = c4.w + P.eta;
-                gw[k][0] = gw[k][1] = gw[k][2] = 0.f;
-            }
+            for (int u = 0; u < LPL; ++u)
+#pragma unroll
+                for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                    const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
+                    const float4 c4 = s_rsph[ll * LPL + u][k];
+                    xform(T[u], c4.x, c4.y, c4.z, w[s][0], w[s][1], w[s][2]);
+                    if (k >= nsph[u]) w[s][0] = w[s][1] = w[s][2] = kFar;      // absent sphere slot
+                    rr[s] = c4.w + P.eta;
+                    gw[s][0] = gw[s][1] = gw[s][2] = 0.f;
+                }
             float jcf = 0.f;
-            Wrench link;
-            link.zero();
             if (K.term_cf >= 0) {
                 // robot spheres vs OBBs (constant cache)
                 for (int b = 0; b < P.n_obb; ++b)
@@ -528,52 +537,64 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                     Wrench pw;
                     pw.zero();
                     jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw, pw);
-                    flush_partner_b<GRAD, HP>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
+                    flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
                 }
             }
-            if (GRAD) {
+            Wrench Wl[LPL];                   // wrench (about the world origin) on each of my links
 #pragma unroll
-                for (int k = 0; k < NS; ++k)
-                    link.add_point(w[k][0], w[k][1], w[k][2], gw[k][0], gw[k][1], gw[k][2]);
+            for (int u = 0; u < LPL; ++u) {
+                Wl[u].zero();
+                if (GRAD) {
+#pragma unroll
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                        const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
+                        Wl[u].add_point(w[s][0], w[s][1], w[s][2], gw[s][0], gw[s][1], gw[s][2]);
+                    }
+                }
             }
-            // tool frame to every lane of the half
-            const M34 Tee = shfl_m34(T, kGroup - 1);
+            // tool frame to every lane of the segment
+            const M34 Tee = shfl_m34(T[LPL - 1], LPF - 1, LPF);
             // held object at a MoveHold knot: attached spheres T_ee T(g)^-1 c (CFreeTrajHold)
             if (K.held_grasp >= 0 && K.term_cf >= 0) {
                 M34 Gi, Tobj;
                 load_m34(Gi, gTi + 16 * K.held_grasp);
                 Tobj = compose(Tee, Gi);
                 const int ho = K.held_obj;
-                float h[1][3], gh[1][3] = {{0.f, 0.f, 0.f}}, hr[1];
-                const float4 c = s_osph[ho][ll];
-                xform(Tobj, c.x, c.y, c.z, h[0][0], h[0][1], h[0][2]);
-                if (ll >= P.osph_n[ho]) h[0][0] = h[0][1] = h[0][2] = kFar;
-                hr[0] = c.w + P.eta;
+                float h[NH][3], gh[NH][3], hr[NH];
+#pragma unroll
+                for (int v = 0; v < NH; ++v) {
+                    const int k = ll + LPF * v;
+                    const float4 c = s_osph[ho][k];
+                    xform(Tobj, c.x, c.y, c.z, h[v][0], h[v][1], h[v][2]);
+                    if (k >= P.osph_n[ho]) h[v][0] = h[v][1] = h[v][2] = kFar;
+                    hr[v] = c.w + P.eta;
+                    gh[v][0] = gh[v][1] = gh[v][2] = 0.f;
+                }
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, 1>(h, hr, P.obb[b], lam_cf, gh);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, NH>(h, hr, P.obb[b], lam_cf, gh);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
                     Wrench pw;
                     pw.zero();
-                    jcf += pairs_vs_instance<GRAD, 1>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh, pw);
-                    flush_partner_b<GRAD, HP>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
+                    jcf += pairs_vs_instance<GRAD, NH>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh, pw);
+                    flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
                 }
-                if (GRAD) {   // held-object wrench acts on the tool link (lane 7 of the half)
+                if (GRAD) {   // held-object wrench acts on the tool link (last lane of the segment)
                     Wrench hw;
                     hw.zero();
-                    hw.add_point(h[0][0], h[0][1], h[0][2], gh[0][0], gh[0][1], gh[0][2]);
-                    hw.template group_sum<kGroup>();
-                    if (ll == kGroup - 1) {
 #pragma unroll
-                        for (int i = 0; i < 3; ++i) { link.f[i] += hw.f[i]; link.m[i] += hw.m[i]; }
+                    for (int v = 0; v < NH; ++v) hw.add_point(h[v][0], h[v][1], h[v][2], gh[v][0], gh[v][1], gh[v][2]);
+                    hw.template group_sum<LPF>();
+                    if (ll == LPF - 1) {
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) { Wl[LPL - 1].f[i] += hw.f[i]; Wl[LPL - 1].m[i] += hw.m[i]; }
                     }
                 }
             }
             if (K.term_cf >= 0)
-                finish_term<MODE>(P, A, sinkB, K.term_cf, gsum<kGroup>(jcf), ll, active, p, s_counts, real);
-            if (BSYNC >= 3) __syncthreads();
+                finish_term<MODE>(P, A, sinkB, K.term_cf, gsum<LPF>(jcf), ll, active, p, s_counts, real);
 
-            // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the half
+            // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the segment
             if (K.term_kp >= 0 || K.term_kr >= 0) {
                 M34 Tp, Tg;
                 load_m34(Tp, ipose + 16 * K.kin_inst);
@@ -602,7 +623,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                     if (K.term_kp >= 0 && epos > 0.f) {
                         const float k = P.term_lam[K.term_kp] / epos;
                         const float fx = dx * k, fy = dy * k, fz = dz * k;      // dJ/dt_ee
-                        if (ll == kGroup - 1) link.add_point(Tee.t[0], Tee.t[1], Tee.t[2], fx, fy, fz);
+                        if (ll == LPF - 1) Wl[LPL - 1].add_point(Tee.t[0], Tee.t[1], Tee.t[2], fx, fy, fz);
                         tw.add_point(Ts.t[0], Ts.t[1], Ts.t[2], -fx, -fy, -fz);
                     }
                     if (K.term_kr >= 0 && wn > 0.f) {
@@ -611,7 +632,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                         const float ux = k * fmaf(Tee.r[0], wx, fmaf(Tee.r[1], wy, Tee.r[2] * wz));
                         const float uy = k * fmaf(Tee.r[3], wx, fmaf(Tee.r[4], wy, Tee.r[5] * wz));
                         const float uz = k * fmaf(Tee.r[6], wx, fmaf(Tee.r[7], wy, Tee.r[8] * wz));
-                        if (ll == kGroup - 1) { link.m[0] -= ux; link.m[1] -= uy; link.m[2] -= uz; }
+                        if (ll == LPF - 1) { Wl[LPL - 1].m[0] -= ux; Wl[LPL - 1].m[1] -= uy; Wl[LPL - 1].m[2] -= uz; }
                         tw.m[0] += ux; tw.m[1] += uy; tw.m[2] += uz;
                     }
                     const bool movable = P.inst[K.kin_inst].xoff >= 0;
@@ -624,37 +645,70 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
             }
 
             // joint limits: dist_from_bounds(q, lo, hi)  (Listing 2; Motion P:1025)
-            float ejl = 0.f, jl = 0.f;
+            float ejl[LPL], jl = 0.f;
+#pragma unroll
+            for (int u = 0; u < LPL; ++u) ejl[u] = 0.f;
             if (K.term_jl >= 0) {
-                ejl = ll < TAMP_NJ ? fmaxf(fmaxf(jlo - q, q - jhi), 0.f) : 0.f;
-                jl = sqrtf(gsum<kGroup>(ejl * ejl));
+                float e2 = 0.f;
+#pragma unroll
+                for (int u = 0; u < LPL; ++u) {
+                    ejl[u] = ll * LPL + u < TAMP_NJ ? fmaxf(fmaxf(jlo[u] - q[u], q[u] - jhi[u]), 0.f) : 0.f;
+                    e2 = fmaf(ejl[u], ejl[u], e2);
+                }
+                jl = sqrtf(gsum<LPF>(e2));
                 finish_term<MODE>(P, A, sinkB, K.term_jl, jl, ll, active, p, s_counts, real);
             }
             if (GRAD) {
-                // suffix sums of link wrenches over lanes >= l: dJ/dq = z . (M - o x F)
+                // suffix sums of link wrenches over the links after each joint: dJ/dq_j = z_j . (M - o_j x F)
+                Wrench sfx;                               // sum over my links and all later lanes' links
 #pragma unroll
-                for (int d = 1; d < kGroup; d <<= 1) {
+                for (int i = 0; i < 3; ++i) {
+                    sfx.f[i] = Wl[0].f[i] + (LPL == 2 ? Wl[LPL - 1].f[i] : 0.f);
+                    sfx.m[i] = Wl[0].m[i] + (LPL == 2 ? Wl[LPL - 1].m[i] : 0.f);
+                }
+#pragma unroll
+                for (int d = 1; d < LPF; d <<= 1) {
                     float v[6];
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
-                        v[i] = __shfl_down_sync(FULL, link.f[i], d, kGroup);
-                        v[3 + i] = __shfl_down_sync(FULL, link.m[i], d, kGroup);
+                        v[i] = __shfl_down_sync(FULL, sfx.f[i], d, LPF);
+                        v[3 + i] = __shfl_down_sync(FULL, sfx.m[i], d, LPF);
                     }
-                    if (ll + d < kGroup) {
+                    if (ll + d < LPF) {
 #pragma unroll
-                        for (int i = 0; i < 3; ++i) { link.f[i] += v[i]; link.m[i] += v[3 + i]; }
+                        for (int i = 0; i < 3; ++i) { sfx.f[i] += v[i]; sfx.m[i] += v[3 + i]; }
                     }
                 }
-                if (ll < TAMP_NJ && real) {
-                    const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
-                    const float ox = T.t[0], oy = T.t[1], oz = T.t[2];
-                    const float mx = link.m[0] - (oy * link.f[2] - oz * link.f[1]);
-                    const float my = link.m[1] - (oz * link.f[0] - ox * link.f[2]);
-                    const float mz = link.m[2] - (ox * link.f[1] - oy * link.f[0]);
-                    float dq = fmaf(zx, mx, fmaf(zy, my, zz * mz));
-                    if (K.term_jl >= 0 && jl > 0.f && ejl > 0.f)
-                        dq += P.term_lam[K.term_jl] * (q > jhi ? ejl : -ejl) / jl;
-                    gs[K.xoff + ll] += dq;
+                Wrench bar[LPL];                          // total wrench on links >= each of my links
+                if (LPL == 1) {
+                    bar[0] = sfx;
+                } else {
+                    Wrench nxt;                           // later lanes only
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        nxt.f[i] = __shfl_down_sync(FULL, sfx.f[i], 1, LPF);
+                        nxt.m[i] = __shfl_down_sync(FULL, sfx.m[i], 1, LPF);
+                        if (ll == LPF - 1) nxt.f[i] = nxt.m[i] = 0.f;
+                        bar[LPL - 1].f[i] = Wl[LPL - 1].f[i] + nxt.f[i];
+                        bar[LPL - 1].m[i] = Wl[LPL - 1].m[i] + nxt.m[i];
+                        bar[0].f[i] = Wl[0].f[i] + bar[LPL - 1].f[i];
+                        bar[0].m[i] = Wl[0].m[i] + bar[LPL - 1].m[i];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < LPL; ++u) {
+                    const int j = ll * LPL + u;
+                    if (j < TAMP_NJ && real) {
+                        const float zx = T[u].r[2], zy = T[u].r[5], zz = T[u].r[8];
+                        const float ox = T[u].t[0], oy = T[u].t[1], oz = T[u].t[2];
+                        const float mx = bar[u].m[0] - (oy * bar[u].f[2] - oz * bar[u].f[1]);
+                        const float my = bar[u].m[1] - (oz * bar[u].f[0] - ox * bar[u].f[2]);
+                        const float mz = bar[u].m[2] - (ox * bar[u].f[1] - oy * bar[u].f[0]);
+                        float dq = fmaf(zx, mx, fmaf(zy, my, zz * mz));
+                        if (K.term_jl >= 0 && jl > 0.f && ejl[u] > 0.f)
+                            dq += P.term_lam[K.term_jl] * (q[u] > jhi[u] ? ejl[u] : -ejl[u]) / jl;
+                        gs[K.xoff + j] += dq;
+                    }
                 }
             }
             // keep the block's warps in step through the (large) FK loop body (profiles/README.md)
@@ -663,7 +717,7 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
         if (BSYNC == 1) phase_sync();   // all warps leave the FK loop before any enters phase C
         // combine the halves' phase-B terms
         if (HP > 1) {
-            sinkB.J += __shfl_xor_sync(FULL, sinkB.J, kGroup);
+            sinkB.J += __shfl_xor_sync(FULL, sinkB.J, LPF);
             const unsigned bal = __ballot_sync(FULL, sinkB.sat);
             sinkB.sat = ((bal >> (threadIdx.x & 31 & ~(GS - 1))) & ((1u << GS) - 1u)) == ((1u << GS) - 1u);
         }
@@ -689,29 +743,38 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                 }
             }
             const int no = P.osph_n[I.obj];
-            const bool mine = gl < no;
-            const float4 c = gl < TAMP_MAX_OBJ_SPHERES ? isph[ii * TAMP_MAX_OBJ_SPHERES + gl]   // padded slots are far
-                                                       : make_float4(kFar, kFar, kFar, 0.f);
-            float gx = 0.f, gy = 0.f, gz = 0.f;
+            float wq[NSO][3], rq[NSO], gq[NSO][3];
+#pragma unroll
+            for (int u = 0; u < NSO; ++u) {
+                const int k = gl + GS * u;
+                const float4 c = k < TAMP_MAX_OBJ_SPHERES ? isph[ii * TAMP_MAX_OBJ_SPHERES + k]   // padded slots: far
+                                                          : make_float4(kFar, kFar, kFar, 0.f);
+                wq[u][0] = c.x; wq[u][1] = c.y; wq[u][2] = c.z;
+                rq[u] = c.w;
+                gq[u][0] = gq[u][1] = gq[u][2] = 0.f;
+            }
             // containment: sum over spheres of dist_from_bounds(xy in surface frame, lo + r, hi - r)
             {
+                float sy, cy;
+                fsincos(Sf.frame[3], &sy, &cy);
                 float e = 0.f;
-                if (mine) {
-                    float sy, cy;
-                    fsincos(Sf.frame[3], &sy, &cy);
-                    const float rx = c.x - Sf.frame[0], ry = c.y - Sf.frame[1];
+#pragma unroll
+                for (int u = 0; u < NSO; ++u) {
+                    if (gl + GS * u >= no) continue;
+                    const float rx = wq[u][0] - Sf.frame[0], ry = wq[u][1] - Sf.frame[1];
                     const float lx = fmaf(cy, rx, sy * ry), ly = fmaf(-sy, rx, cy * ry);
-                    const float lox = Sf.lo[0] + c.w, hix = Sf.hi[0] - c.w;
-                    const float loy = Sf.lo[1] + c.w, hiy = Sf.hi[1] - c.w;
+                    const float lox = Sf.lo[0] + rq[u], hix = Sf.hi[0] - rq[u];
+                    const float loy = Sf.lo[1] + rq[u], hiy = Sf.hi[1] - rq[u];
                     const float ex = fmaxf(fmaxf(lox - lx, lx - hix), 0.f);
                     const float ey = fmaxf(fmaxf(loy - ly, ly - hiy), 0.f);
-                    e = sqrtf(fmaf(ex, ex, ey * ey));
-                    if (GRAD && e > 0.f) {
-                        const float k = P.term_lam[Q.term_sc] / e;
+                    const float eu = sqrtf(fmaf(ex, ex, ey * ey));
+                    e += eu;
+                    if (GRAD && eu > 0.f) {
+                        const float k = P.term_lam[Q.term_sc] / eu;
                         const float glx = (lx > hix ? ex : (lx < lox ? -ex : 0.f)) * k;
                         const float gly = (ly > hiy ? ey : (ly < loy ? -ey : 0.f)) * k;
-                        gx += fmaf(cy, glx, -sy * gly);
-                        gy += fmaf(sy, glx, cy * gly);
+                        gq[u][0] += fmaf(cy, glx, -sy * gly);
+                        gq[u][1] += fmaf(sy, glx, cy * gly);
                     }
                 }
                 finish_term<MODE>(P, A, sink, Q.term_sc, gsum<GS>(e), gl, active, p, s_counts);
@@ -719,28 +782,27 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
             // CFreePlace: placed-object spheres vs OBBs (support excluded) and other objects
             {
                 const float lam_cp = P.term_lam[Q.term_cp];
-                float wq[1][3] = {{c.x, c.y, c.z}}, rq[1] = {c.w + P.eta}, gq[1][3] = {{0.f, 0.f, 0.f}};
+                float rqe[NSO];
+#pragma unroll
+                for (int u = 0; u < NSO; ++u) rqe[u] = rq[u] + P.eta;
                 float jcp = 0.f;
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<GRAD, 1>(wq, rq, P.obb[b], lam_cp, gq);
+                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<GRAD, NSO>(wq, rqe, P.obb[b], lam_cp, gq);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
                     Wrench pw;
                     pw.zero();
-                    jcp += pairs_vs_instance<GRAD, 1>(wq, rq, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq, pw);
+                    jcp += pairs_vs_instance<GRAD, NSO>(wq, rqe, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq, pw);
                     flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl);
                 }
-                gx += gq[0][0]; gy += gq[0][1]; gz += gq[0][2];
                 finish_term<MODE>(P, A, sink, Q.term_cp, gsum<GS>(jcp), gl, active, p, s_counts);
             }
             if (GRAD) {
-                if (mine) own.add_point(c.x, c.y, c.z, gx, gy, gz);
+#pragma unroll
+                for (int u = 0; u < NSO; ++u)
+                    if (gl + GS * u < no) own.add_point(wq[u][0], wq[u][1], wq[u][2], gq[u][0], gq[u][1], gq[u][2]);
                 own.template group_sum<GS>();
-                if (gl == 0) {
-                    float* dst = iwr + 8 * ii;
-                    dst[0] += own.f[0]; dst[1] += own.f[1]; dst[2] += own.f[2];
-                    dst[3] += own.m[0]; dst[4] += own.m[1]; dst[5] += own.m[2];
-                }
+                if (gl == 0) add_wrench(iwr + 8 * ii, own);
             }
         }
 
@@ -777,12 +839,11 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
         for (int tr = 0; tr < P.n_traj; ++tr) {   // TrajLength(tau) = sum_j ||k_{j+1} - k_j||  (Listing 1 cost)
             const KTraj& Tj = P.traj[tr];
             const int nseg = Tj.n_knots + 1;
-            const bool mine = gl < TAMP_NJ;
-            auto val = [&](int j) -> float {   // j = 0: q1, 1..K: knots, K+1: q2
-                if (!mine) return 0.f;
-                if (j == 0) return Tj.q1_xoff >= 0 ? xs[Tj.q1_xoff + gl] : P.const_conf[Tj.q1_const][gl];
-                if (j == nseg) return Tj.q2_xoff >= 0 ? xs[Tj.q2_xoff + gl] : P.const_conf[Tj.q2_const][gl];
-                return xs[Tj.knot_xoff + 7 * (j - 1) + gl];
+            auto val = [&](int j, int jt) -> float {   // j = 0: q1, 1..K: knots, K+1: q2; jt = joint
+                if (jt >= TAMP_NJ) return 0.f;
+                if (j == 0) return Tj.q1_xoff >= 0 ? xs[Tj.q1_xoff + jt] : P.const_conf[Tj.q1_const][jt];
+                if (j == nseg) return Tj.q2_xoff >= 0 ? xs[Tj.q2_xoff + jt] : P.const_conf[Tj.q2_const][jt];
+                return xs[Tj.knot_xoff + 7 * (j - 1) + jt];
             };
             auto xoff_of = [&](int j) -> int {
                 if (j == 0) return Tj.q1_xoff;
@@ -790,14 +851,25 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
                 return Tj.knot_xoff + 7 * (j - 1);
             };
             for (int j = 0; j < nseg; ++j) {
-                const float dlt = val(j + 1) - val(j);
-                const float len = sqrtf(gsum<GS>(dlt * dlt));
+                float dlt[NJL], s2 = 0.f;
+#pragma unroll
+                for (int u = 0; u < NJL; ++u) {
+                    const int jt = gl + GS * u;
+                    dlt[u] = val(j + 1, jt) - val(j, jt);
+                    s2 = fmaf(dlt[u], dlt[u], s2);
+                }
+                const float len = sqrtf(gsum<GS>(s2));
                 soft = fmaf(P.lam_traj, len, soft);
-                if (GRAD && mine && len > 0.f) {
-                    const float g = P.lam_traj * dlt / len;
+                if (GRAD && len > 0.f) {
                     const int o1 = xoff_of(j + 1), o0 = xoff_of(j);
-                    if (o1 >= 0) gs[o1 + gl] += g;
-                    if (o0 >= 0) gs[o0 + gl] -= g;
+#pragma unroll
+                    for (int u = 0; u < NJL; ++u) {
+                        const int jt = gl + GS * u;
+                        if (jt >= TAMP_NJ) continue;
+                        const float g = P.lam_traj * dlt[u] / len;
+                        if (o1 >= 0) gs[o1 + jt] += g;
+                        if (o0 >= 0) gs[o0 + jt] -= g;
+                    }
                 }
             }
         }
@@ -844,31 +916,15 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
             const float bc1 = A.bc1[it];
             const float bc2 = A.bc2[it];
             if (!invalid) {
-                if (KM > 0) {
-#pragma unroll
-                    for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
-                        const int d = gl + GS * k;
-                        if (d < D) {
-                            const float g = gs[d] * P.grad_scale;
-                            mreg[k] = fmaf(P.beta1, mreg[k], (1.f - P.beta1) * g);
-                            vreg[k] = fmaf(P.beta2, vreg[k], (1.f - P.beta2) * g * g);
-                            const float mh = mreg[k] / bc1;
-                            const float vh = vreg[k] / bc2;
-                            const float xn = xs[d] - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
-                            xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
-                        }
-                    }
-                } else {
-                    for (int d = gl; d < D; d += GS) {
-                        const float g = gs[d] * P.grad_scale;
-                        const float mm = fmaf(P.beta1, A.m[p * D + d], (1.f - P.beta1) * g);
-                        const float vv = fmaf(P.beta2, A.v[p * D + d], (1.f - P.beta2) * g * g);
-                        if (active) { A.m[p * D + d] = mm; A.v[p * D + d] = vv; }
-                        const float mh = mm / bc1;
-                        const float vh = vv / bc2;
-                        const float xn = xs[d] - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
-                        xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
-                    }
+                for (int d = gl; d < D; d += GS) {
+                    const float g = gs[d] * P.grad_scale;
+                    const float mm = fmaf(P.beta1, A.m[p * D + d], (1.f - P.beta1) * g);
+                    const float vv = fmaf(P.beta2, A.v[p * D + d], (1.f - P.beta2) * g * g);
+                    if (active) { A.m[p * D + d] = mm; A.v[p * D + d] = vv; }
+                    const float mh = mm / bc1;
+                    const float vh = vv / bc2;
+                    const float xn = xs[d] - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
+                    xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
                 }
             }
             phase_sync();
@@ -877,13 +933,6 @@ __global__ void __launch_bounds__(768, 1) k_particle(const __grid_constant__ KPr
 
     if (MODE == MODE_OPT && active) {
         for (int d = gl; d < D; d += GS) A.x[p * D + d] = xs[d];
-        if (KM > 0) {
-#pragma unroll
-            for (int k = 0; k < (KM > 0 ? KM : 1); ++k) {
-                const int d = gl + GS * k;
-                if (d < D) { A.m[p * D + d] = mreg[k]; A.v[p * D + d] = vreg[k]; }
-            }
-        }
         if (gl == 0) A.invalid[p] = invalid ? 1 : 0;
     }
     if (MODE == MODE_CHECK) {
@@ -1213,51 +1262,53 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
 static inline void counted() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-template <int MODE, int GS, int BSYNC>
+template <int MODE, int LPF, int HP, int BSYNC>
 static cudaError_t launch_particle_t(const KProgram& P, const KArgs& A, int threads, size_t smem, cudaStream_t st) {
-    auto fn = k_particle<MODE, 0, GS, BSYNC>;
+    auto fn = k_particle<MODE, LPF, HP, BSYNC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int per_block = threads / GS;
+    const int per_block = threads / (LPF * HP);
     const int64_t blocks = (A.n + per_block - 1) / per_block;
     fn<<<(unsigned)blocks, threads, smem, st>>>(P, A);
     counted();
     return cudaGetLastError();
 }
 
-template <int GS>
-static cudaError_t launch_particle_gs(int mode, int bsync, const KProgram& P, const KArgs& A, int threads, size_t smem,
-                                      cudaStream_t st) {
-    if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, GS, 2>(P, A, threads, smem, st);
+template <int LPF, int HP>
+static cudaError_t launch_particle_map(int mode, int bsync, const KProgram& P, const KArgs& A, int threads, size_t smem,
+                                       cudaStream_t st) {
+    if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, LPF, HP, 2>(P, A, threads, smem, st);
     if (mode == MODE_CHECK) {
-        if (bsync == 0) return launch_particle_t<MODE_CHECK, GS, 0>(P, A, threads, smem, st);
-        if (bsync == 1) return launch_particle_t<MODE_CHECK, GS, 1>(P, A, threads, smem, st);
-        return launch_particle_t<MODE_CHECK, GS, 2>(P, A, threads, smem, st);
+        if (bsync == 0) return launch_particle_t<MODE_CHECK, LPF, HP, 0>(P, A, threads, smem, st);
+        if (bsync == 1) return launch_particle_t<MODE_CHECK, LPF, HP, 1>(P, A, threads, smem, st);
+        return launch_particle_t<MODE_CHECK, LPF, HP, 2>(P, A, threads, smem, st);
     }
     switch (bsync) {
-        case 0: return launch_particle_t<MODE_OPT, GS, 0>(P, A, threads, smem, st);
-        case 1: return launch_particle_t<MODE_OPT, GS, 1>(P, A, threads, smem, st);
-        case 3: return launch_particle_t<MODE_OPT, GS, 3>(P, A, threads, smem, st);
-        default: return launch_particle_t<MODE_OPT, GS, 2>(P, A, threads, smem, st);
+        case 0: return launch_particle_t<MODE_OPT, LPF, HP, 0>(P, A, threads, smem, st);
+        case 1: return launch_particle_t<MODE_OPT, LPF, HP, 1>(P, A, threads, smem, st);
+        default: return launch_particle_t<MODE_OPT, LPF, HP, 2>(P, A, threads, smem, st);
     }
 }
 
 // registers per thread of the hot kernel (for the launch-configuration policy)
 int particle_kernel_regs(int gs) {
     cudaFuncAttributes a;
-    cudaError_t e = gs == 16 ? cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 0, 16, 1>)
-                             : cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 0, 8, 1>);
+    cudaError_t e = gs == 16 ? cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 8, 2, 1>)
+                  : gs == 4  ? cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 4, 1, 1>)
+                             : cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 8, 1, 1>);
     if (e != cudaSuccess) { cudaGetLastError(); return 80; }
     return a.numRegs;
 }
 
-// gs = lanes per particle (8 or 16); threads = block size (multiple of 32, <= 768); smem sized for
-// threads / gs particles.  bsync = block-synchronisation level (see k_particle).
+// gs = lanes per particle: 4 (two link frames per lane), 8 (one), 16 (two FK instances at a time);
+// threads = block size (multiple of 32, <= 768); smem sized for threads / gs particles;
+// bsync = block-synchronisation level (see k_particle).
 cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
                             cudaStream_t st) {
     if (A.n <= 0) return cudaSuccess;
-    if (gs == 16) return launch_particle_gs<16>(mode, bsync, P, A, threads, smem, st);
-    return launch_particle_gs<8>(mode, bsync, P, A, threads, smem, st);
+    if (gs == 16) return launch_particle_map<8, 2>(mode, bsync, P, A, threads, smem, st);
+    if (gs == 4) return launch_particle_map<4, 1>(mode, bsync, P, A, threads, smem, st);
+    return launch_particle_map<8, 1>(mode, bsync, P, A, threads, smem, st);
 }
 
 cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
