@@ -119,6 +119,22 @@ __device__ __forceinline__ void fsincos(float x, float* s, float* c) {
     *c = ((q + 1) & 2) ? -cv : cv;
 }
 
+// atan2(y, x) for y >= 0 (an angle in [0, pi]): octant reduction, cephes atanf reduction at tan(pi/8) and its
+// single-precision polynomial (max |err| 2.7e-7 rad over [0, pi], ~1 ulp; verified on the host against
+// libm atan2); branch-free and shorter than atan2f
+__device__ __forceinline__ float fatan2_pos(float y, float x) {
+    const float ax = fabsf(x);
+    const float mx = fmaxf(ax, y), mn = fminf(ax, y);
+    const float a = mx > 0.f ? mn / mx : 0.f;
+    const bool big = a > 0.41421356f;
+    const float t = big ? (a - 1.f) / (a + 1.f) : a;
+    const float z = t * t;
+    const float p = fmaf(fmaf(fmaf(8.05374449538e-2f, z, -1.38776856032e-1f), z, 1.99777106478e-1f), z, -3.33329491539e-1f);
+    float r = fmaf(p * z, t, t) + (big ? 0.785398163397f : 0.f);
+    r = y > ax ? 1.57079632679f - r : r;
+    return x < 0.f ? 3.14159265359f - r : r;
+}
+
 struct Wrench {
     float f[3];
     float m[3];
@@ -214,9 +230,9 @@ constexpr float kFar = 1e18f;   // position of padded (absent) spheres: never wi
 // broadcast to the group).  Fast path: branch-free test of all NS x 8 pairs (d^2 - (ra+rb)^2 < 0 ?), no
 // square roots; only if some pair of the warp is active are the hinges and gradients evaluated.
 // Returns the hinge sum; if GRAD accumulates dJ/dw_a (x lam) into g and the partner's wrench into pw.
-template <bool GRAD, int NS>
+template <bool GRAD, int NS, class OnWrench>
 __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], const float (&rr)[NS], const float4* Bs,
-                                                   const float4 bound, float lam, float (&g)[NS][3], Wrench& pw) {
+                                                   const float4 bound, float lam, float (&g)[NS][3], OnWrench&& on_wrench) {
     // broad phase: skip the instance unless some query sphere of the warp reaches its bounding sphere
     float mb = 1.f;
 #pragma unroll
@@ -226,7 +242,10 @@ __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], cons
         mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
     }
     if (!__any_sync(FULL, mb < 0.f)) return 0.f;
-    float mn = 1.f;
+    // narrow phase, branch-free: which of the NS x 8 pairs reach (d^2 < (ra + rb)^2)?
+    uint32_t act[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) act[k] = 0u;
 #pragma unroll
     for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
         const float4 B = Bs[b];
@@ -235,16 +254,24 @@ __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], cons
             const float dx = w[k][0] - B.x, dy = w[k][1] - B.y, dz = w[k][2] - B.z;
             const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
             const float R = rr[k] + B.w;
-            mn = fminf(mn, fmaf(-R, R, d2));
+            act[k] |= (fmaf(-R, R, d2) < 0.f ? 1u : 0u) << b;
         }
     }
-    float j = 0.f;
-    if (__any_sync(FULL, mn < 0.f)) {
-#pragma unroll 1
-        for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
-            const float4 B = Bs[b];
+    uint32_t any = 0u;
 #pragma unroll
-            for (int k = 0; k < NS; ++k) {
+    for (int k = 0; k < NS; ++k) any |= act[k];
+    float j = 0.f;
+    if (__any_sync(FULL, any != 0u)) {
+        // hinges and gradients of the active pairs only
+        Wrench pw;
+        pw.zero();
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            uint32_t m = act[k];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1u;
+                const float4 B = Bs[b];
                 float ux, uy, uz;
                 j += sphere_sphere<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, ux, uy, uz);
                 if (GRAD) {
@@ -253,6 +280,7 @@ __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], cons
                 }
             }
         }
+        on_wrench(pw);   // warp-uniform: reduce / store the partner's wrench
     }
     return j;
 }
@@ -442,6 +470,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
         // ---- phase A: object instances (poses, world sphere centres), zero accumulators ----
         for (int i = 0; i < P.n_inst; ++i) {
             const KInst& I = P.inst[i];
+            if (I.xoff < 0 && it > 0) continue;      // constant instances: set up once per launch
             float px, py, pz, yaw;
             if (I.xoff >= 0) { px = xs[I.xoff]; py = xs[I.xoff + 1]; pz = xs[I.xoff + 2]; yaw = xs[I.xoff + 3]; }
             else { px = I.pose[0]; py = I.pose[1]; pz = I.pose[2]; yaw = I.pose[3]; }
@@ -534,10 +563,8 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    Wrench pw;
-                    pw.zero();
-                    jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw, pw);
-                    flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
+                    jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw,
+                        [&](Wrench& pw) { flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); });
                 }
             }
             Wrench Wl[LPL];                   // wrench (about the world origin) on each of my links
@@ -574,10 +601,8 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                     if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, NH>(h, hr, P.obb[b], lam_cf, gh);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    Wrench pw;
-                    pw.zero();
-                    jcf += pairs_vs_instance<GRAD, NH>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh, pw);
-                    flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real);
+                    jcf += pairs_vs_instance<GRAD, NH>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh,
+                        [&](Wrench& pw) { flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); });
                 }
                 if (GRAD) {   // held-object wrench acts on the tool link (last lane of the segment)
                     Wrench hw;
@@ -614,7 +639,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                 const float wx = Mm[7] - Mm[5], wy = Mm[2] - Mm[6], wz = Mm[3] - Mm[1];
                 const float wn2 = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
                 const float wn = sqrtf(wn2);
-                const float erot = atan2f(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
+                const float erot = fatan2_pos(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
                 if (K.term_kp >= 0) finish_term<MODE>(P, A, sinkB, K.term_kp, epos, ll, active, p, s_counts, real);
                 if (K.term_kr >= 0) finish_term<MODE>(P, A, sinkB, K.term_kr, erot, ll, active, p, s_counts, real);
                 if (GRAD) {
@@ -790,10 +815,8 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                     if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<GRAD, NSO>(wq, rqe, P.obb[b], lam_cp, gq);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
-                    Wrench pw;
-                    pw.zero();
-                    jcp += pairs_vs_instance<GRAD, NSO>(wq, rqe, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq, pw);
-                    flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl);
+                    jcp += pairs_vs_instance<GRAD, NSO>(wq, rqe, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq,
+                        [&](Wrench& pw) { flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl); });
                 }
                 finish_term<MODE>(P, A, sink, Q.term_cp, gsum<GS>(jcp), gl, active, p, s_counts);
             }
