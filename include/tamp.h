@@ -52,7 +52,7 @@ extern "C" {
 #define TAMP_MAX_ACTIONS 64
 #define TAMP_MAX_GOAL 8
 #define TAMP_MAX_D 384                /* optimised floats per particle */
-#define TAMP_MAX_TERMS 160            /* hard constraint terms */
+#define TAMP_MAX_TERMS 256            /* hard constraint terms */
 #define TAMP_MAX_FK 64                /* robot configurations evaluated per particle (confs + knots) */
 #define TAMP_MAX_GRASPS 8
 #define TAMP_MAX_KNOTS 8
@@ -73,9 +73,10 @@ enum { TAMP_MOVE_FREE = 0, TAMP_PICK = 1, TAMP_MOVE_HOLD = 2, TAMP_PLACE = 3 };
 /* hard-constraint term kinds (SURVEY §8(c) term table):
    JL joint limits (Motion); CF robot collision (CFreeTraj/CFreeHold/CFreeTrajHold,
    P:1029-1031); KP/KR kinematics position/rotation (Kin); SS/SC stable-place support /
-   containment; CP CFreePlace. */
+   containment; CP CFreePlace; SELF robot self-collision ("does not cause
+   robot self-collisions", tolerance 0 P:1132; enabled by desc.self_collision). */
 enum { TAMP_TERM_JL = 0, TAMP_TERM_CF = 1, TAMP_TERM_KP = 2, TAMP_TERM_KR = 3,
-       TAMP_TERM_SS = 4, TAMP_TERM_SC = 5, TAMP_TERM_CP = 6, TAMP_N_TERM_KINDS = 7 };
+       TAMP_TERM_SS = 4, TAMP_TERM_SC = 5, TAMP_TERM_CP = 6, TAMP_TERM_SELF = 7, TAMP_N_TERM_KINDS = 8 };
 
 /* Serial 7-DOF arm, modified (Craig) DH: frame_j = frame_{j-1} Rx(alpha_{j-1}) Tx(a_{j-1}) Tz(d_j) Rz(q_j);
    tool/TCP = frame_7 Tz(flange_d) Rz(tcp_yaw) Tz(tcp_d); frame_0 = Trans(base xyz) Rz(base yaw).
@@ -89,6 +90,8 @@ typedef struct {
     int32_t n_spheres;
     float sphere[TAMP_MAX_ROBOT_SPHERES][4];
     int32_t sphere_link[TAMP_MAX_ROBOT_SPHERES];
+    uint32_t self_mask[TAMP_MAX_ROBOT_SPHERES];   /* bit j of self_mask[i]: sphere pair (i, j) is checked by
+                                                     the SELF term (symmetric; typically non-adjacent links) */
 } tamp_robot_desc;
 
 /* static oriented box: centre, yaw about world z, half extents > 0 */
@@ -149,6 +152,7 @@ typedef struct {
     int32_t block_threads;                /* particle-kernel block size (multiple of 32, <= 768); 0 = auto */
     int32_t block_sync;                   /* block-synchronous phases: 0 off, 1 phase boundaries, 2 + every
                                              FK instance, 3 + inside the FK body; -1 auto (2) */
+    int32_t self_collision;               /* 1: add a SELF term after every CF term */
     int32_t ik_iters;                     /* conditional IK sampler: damped-least-squares iterations
                                              per Pick/Place conf inside tamp_sample_particles; 0 = uniform confs */
     float ik_damping;                     /* DLS damping mu (dq = J^T (J J^T + mu^2 I)^-1 e) */

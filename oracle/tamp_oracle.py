@@ -28,7 +28,7 @@ from workloads.scenes import (ProblemSpec, CONF, PLACEMENT, GRASP, TRAJ,
 from .philox import uniforms
 
 DT = torch.float64
-HARD_KINDS = ("JL", "CF", "KP", "KR", "SS", "SC", "CP")
+HARD_KINDS = ("JL", "CF", "KP", "KR", "SS", "SC", "CP", "SELF")
 
 
 # ----------------------------------------------------------------------------------------------
@@ -255,6 +255,8 @@ def build_csp(spec: ProblemSpec) -> CSP:
                     terms.append(Term("JL", conf=("knot", a.traj, j)))
                     terms.append(Term("CF", conf=("knot", a.traj, j), scene=scene,
                                       excl=((a.obj,) if hv else ()), held=hv))
+                    if spec.self_collision:   # "... does not cause robot self-collisions"
+                        terms.append(Term("SELF", conf=("knot", a.traj, j)))
                 trajs.append((a.q1, a.traj, a.q2))
         elif a.kind == PICK:
             scene = {o: p for o, p in pose.items()}
@@ -263,6 +265,8 @@ def build_csp(spec: ProblemSpec) -> CSP:
             # Kin(q, o, g, p) (KP, KR)
             terms.append(Term("JL", conf=c))
             terms.append(Term("CF", conf=c, scene=scene, excl=(a.obj,)))
+            if spec.self_collision:
+                terms.append(Term("SELF", conf=c))
             terms.append(Term("KP", conf=c, obj=a.obj, grasp=a.grasp, placement=a.placement))
             terms.append(Term("KR", conf=c, obj=a.obj, grasp=a.grasp, placement=a.placement))
             held = (a.obj, a.grasp)
@@ -272,6 +276,8 @@ def build_csp(spec: ProblemSpec) -> CSP:
             c = ("var", a.q1)
             terms.append(Term("JL", conf=c))
             terms.append(Term("CF", conf=c, scene=scene, excl=(a.obj,)))
+            if spec.self_collision:
+                terms.append(Term("SELF", conf=c))
             terms.append(Term("KP", conf=c, obj=a.obj, grasp=a.grasp, placement=a.placement))
             terms.append(Term("KR", conf=c, obj=a.obj, grasp=a.grasp, placement=a.placement))
             # StablePlace(o, p, s): support + containment; CFreePlace(o, p)
@@ -466,6 +472,12 @@ def evaluate(spec: ProblemSpec, csp: CSP, x: torch.Tensor, grasps: torch.Tensor)
                 wo, ro = obj_spheres(o, T_obj)
                 j = j + scene_cost(wo, ro, t.scene, {o}, spec.obbs)
             Jc.append(j)
+        elif t.kind == "SELF":  # robot self-collision: hinge over the robot's sphere pairs
+            w = robot_sphere_centers(rob, fk(t.conf))
+            ii = torch.as_tensor([a for a, _ in rob.self_pairs], dtype=torch.long)
+            jj = torch.as_tensor([b for _, b in rob.self_pairs], dtype=torch.long)
+            d = torch.linalg.vector_norm(w[:, ii] - w[:, jj], dim=-1)
+            Jc.append((r_rob[ii] + r_rob[jj] + eta - d).clamp(min=0.0).sum(-1))
         elif t.kind in ("KP", "KR"):   # Kin(q, o, g, p): FK(q) = p . g
             target = placement_T(t.placement) @ G[:, gslot[t.grasp]]
             e_pos, e_rot = pose_error(fk(t.conf)[:, 8], target)

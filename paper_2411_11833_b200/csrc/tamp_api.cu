@@ -71,7 +71,7 @@ struct tamp_ctx {
     size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, total;
     int64_t n_keys = 0;
     // shared-memory layout of the particle kernel (floats per particle)
-    int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
+    int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi, off_rsw;
     size_t smem = 0;
     int gs = 8;                  // lanes per particle in the particle kernel
     int ik_iters = 0;            // conditional IK sampler iterations
@@ -203,6 +203,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         }
         H34 tool = h_mul(h_mul(h_tr(0, 0, R.flange_d), h_rz(R.tcp_yaw)), h_tr(0, 0, R.tcp_d));
         h_store(tool, P.F[kGroup - 1]);
+        int packed[TAMP_MAX_ROBOT_SPHERES];
         for (int s = 0; s < R.n_spheres; ++s) {
             const int l = R.sphere_link[s];
             REQUIRE(l >= 1 && l <= 8, TAMP_E_INVALID, "sphere_link must be in 1..8");
@@ -210,7 +211,18 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             const int lane = l - 1;
             REQUIRE(P.rsph_n[lane] < TAMP_MAX_SPHERES_PER_LINK, TAMP_E_UNSUPPORTED, "more than 4 spheres on a link");
             for (int c = 0; c < 4; ++c) P.rsph[lane][P.rsph_n[lane]][c] = R.sphere[s][c];
+            packed[s] = lane * TAMP_MAX_SPHERES_PER_LINK + P.rsph_n[lane];
             P.rsph_n[lane]++;
+        }
+        // self-collision pairs in packed sphere ids
+        if (d.self_collision) {
+            P.has_self = 1;
+            for (int i = 0; i < R.n_spheres; ++i)
+                for (int j = 0; j < R.n_spheres; ++j) {
+                    if (!((R.self_mask[i] >> j) & 1u)) continue;
+                    REQUIRE(i != j && ((R.self_mask[j] >> i) & 1u), TAMP_E_INVALID, "self_mask must be symmetric, no diagonal");
+                    P.self_mask[packed[i]] |= 1u << packed[j];
+                }
         }
     }
     // world
@@ -360,6 +372,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
                 F.xoff = (int16_t)(xoff[a.traj] + 7 * j);
                 F.term_jl = add_term(TAMP_TERM_JL);
                 F.term_cf = add_term(TAMP_TERM_CF);
+                F.term_self = d.self_collision ? add_term(TAMP_TERM_SELF) : (int16_t)-1;
                 F.term_kp = F.term_kr = -1;
                 F.kin_inst = F.kin_grasp = -1;
                 F.held_grasp = (int16_t)hg;
@@ -393,6 +406,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             F.xoff = (int16_t)xoff[a.q1];
             F.term_jl = add_term(TAMP_TERM_JL);
             F.term_cf = add_term(TAMP_TERM_CF);
+            F.term_self = d.self_collision ? add_term(TAMP_TERM_SELF) : (int16_t)-1;
             F.term_kp = add_term(TAMP_TERM_KP);
             F.term_kr = add_term(TAMP_TERM_KR);
             F.kin_inst = (int16_t)inst_of[a.placement];
@@ -434,7 +448,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
     {
         auto sig = [&](const KFk& K) {
             return std::make_tuple(K.term_cf >= 0, K.term_kp >= 0, K.term_kr >= 0, K.term_jl >= 0, K.held_grasp >= 0,
-                                   K.part_count, K.obb_mask);
+                                   K.part_count, K.obb_mask, K.term_self >= 0);
         };
         std::vector<KFk> in(P.fk, P.fk + n_fk), out;
         std::vector<bool> used(n_fk, false);
@@ -536,6 +550,8 @@ static void smem_layout(tamp_ctx* c) {
     off += 16 * P.n_grasp;
     c->off_gTi = off;
     off += 16 * P.n_grasp;
+    c->off_rsw = off;                                 // robot sphere centres for the SELF term (2 FK halves)
+    off += P.has_self ? 2 * 4 * kGroup * TAMP_MAX_SPHERES_PER_LINK : 0;
     // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
     int stride = ((off + 31) / 32) * 32 + 8;
     c->stride = stride;
@@ -609,6 +625,7 @@ static KArgs base_args(tamp_ctx* c) {
     A.off_iwr = c->off_iwr;
     A.off_gT = c->off_gT;
     A.off_gTi = c->off_gTi;
+    A.off_rsw = c->off_rsw;
     return A;
 }
 

@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
     __shared__ int s_counts[TAMP_MAX_TERMS + 2];
     __shared__ float4 s_F[kGroup][3];                              // fixed transform of each joint (7: tool)
     __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];   // spheres of each link frame
+    __shared__ uint32_t s_selfmask[kGroup * TAMP_MAX_SPHERES_PER_LINK];
 
     const int gl = threadIdx.x & (GS - 1);          // lane within the particle group
     const int ll = gl & (LPF - 1);                  // lane within the FK segment
@@ -430,7 +431,9 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
     if (threadIdx.x < kGroup * TAMP_MAX_SPHERES_PER_LINK) {
         const int l = threadIdx.x / TAMP_MAX_SPHERES_PER_LINK, k = threadIdx.x % TAMP_MAX_SPHERES_PER_LINK;
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3]);
+        s_selfmask[threadIdx.x] = P.self_mask[threadIdx.x];
     }
+    float4* rsw = reinterpret_cast<float4*>(S + A.off_rsw) + (HP > 1 ? half : 0) * kGroup * TAMP_MAX_SPHERES_PER_LINK;
     int nsph[LPL];
     float jlo[LPL], jhi[LPL];
 #pragma unroll
@@ -566,6 +569,32 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                     jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw,
                         [&](Wrench& pw) { flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); });
                 }
+            }
+            // robot self-collision: every lane tests its own spheres against their pair
+            // partners (sphere centres shared through shared memory), keeping only its own spheres' gradient;
+            // each pair's hinge is counted once, by the lower sphere id.
+            if (K.term_self >= 0) {
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    rsw[ll * NS + s] = make_float4(w[s][0], w[s][1], w[s][2], rr[s] - P.eta);
+                __syncwarp();
+                float js = 0.f;
+                const float lam_self = P.term_lam[K.term_self];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    const int sid = ll * NS + s;
+                    uint32_t m = s_selfmask[sid];
+                    while (m) {
+                        const int t = __ffs(m) - 1;
+                        m &= m - 1u;
+                        float ux, uy, uz;
+                        const float pen = sphere_sphere<GRAD>(w[s][0], w[s][1], w[s][2], rr[s], rsw[t], lam_self, ux, uy, uz);
+                        if (sid < t) js += pen;
+                        if (GRAD) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
+                    }
+                }
+                finish_term<MODE>(P, A, sinkB, K.term_self, gsum<LPF>(js), ll, active, p, s_counts, real);
+                __syncwarp();
             }
             Wrench Wl[LPL];                   // wrench (about the world origin) on each of my links
 #pragma unroll

@@ -30,6 +30,7 @@ struct KFk {
     int16_t part_begin, part_count;   // collision partner instances: partners[part_begin ...]
     uint16_t obb_mask;                // OBBs checked against the robot (and held object)
     int16_t ghost;                    // 1 = padding copy of its pair partner (results discarded)
+    int16_t term_self;                // robot self-collision term (-1 none)
 };
 
 // An object at a pose: constant (xoff < 0, pose[]) or a placement variable at x[xoff .. xoff+4).
@@ -81,6 +82,9 @@ struct KProgram {
     float osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES][4];
     int32_t osph_n[TAMP_MAX_OBJECTS];
     float obound[TAMP_MAX_OBJECTS][4];   // bounding sphere of each object's spheres (object frame xyz, radius)
+    // self-collision: bit t of self_mask[s] = check robot spheres s, t (packed ids: link lane * 4 + k)
+    uint32_t self_mask[kGroup * TAMP_MAX_SPHERES_PER_LINK];
+    int32_t has_self;
 };
 
 // Particle-initialisation program (K1).
@@ -118,7 +122,7 @@ struct KArgs {
     const float* hi;       // [D]
     int64_t n;
     int64_t gofs;
-    int32_t stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi;
+    int32_t stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi, off_rsw;
     int32_t n_steps, t0;
     // Adam bias corrections 1 - beta^t for the (<= kMaxStepsPerLaunch) steps of this launch, computed on the
     // host in double precision

@@ -28,9 +28,9 @@ MAX_SURFACES = 8
 MAX_VARS = 96
 MAX_ACTIONS = 64
 MAX_GOAL = 8
-MAX_TERMS = 160
-N_TERM_KINDS = 7
-TERM_NAMES = ("JL", "CF", "KP", "KR", "SS", "SC", "CP")
+MAX_TERMS = 256
+N_TERM_KINDS = 8
+TERM_NAMES = ("JL", "CF", "KP", "KR", "SS", "SC", "CP", "SELF")
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_CUDA", 3: "E_NOMEM", 4: "E_STATE", 5: "E_UNSUPPORTED"}
 
 F = ctypes.c_float
@@ -41,7 +41,8 @@ I64 = ctypes.c_int64
 class RobotDesc(ctypes.Structure):
     _fields_ = [("dh", F * 3 * NJ), ("flange_d", F), ("tcp_yaw", F), ("tcp_d", F), ("base", F * 4),
                 ("joint_lo", F * NJ), ("joint_hi", F * NJ), ("n_spheres", I32),
-                ("sphere", F * 4 * MAX_ROBOT_SPHERES), ("sphere_link", I32 * MAX_ROBOT_SPHERES)]
+                ("sphere", F * 4 * MAX_ROBOT_SPHERES), ("sphere_link", I32 * MAX_ROBOT_SPHERES),
+                ("self_mask", ctypes.c_uint32 * MAX_ROBOT_SPHERES)]
 
 
 class ObbDesc(ctypes.Structure):
@@ -80,7 +81,7 @@ class ProblemDesc(ctypes.Structure):
                 ("beta1", F), ("beta2", F), ("adam_eps", F),
                 ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F),
                 ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32),
-                ("ik_iters", I32), ("ik_damping", F)]
+                ("self_collision", I32), ("ik_iters", I32), ("ik_damping", F)]
 
 
 class Info(ctypes.Structure):
@@ -168,6 +169,9 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
         for k in range(4):
             d.robot.sphere[s][k] = float(r.spheres[s][k])
         d.robot.sphere_link[s] = int(r.sphere_link[s])
+    for i, j in getattr(r, "self_pairs", []):
+        d.robot.self_mask[i] |= 1 << j
+        d.robot.self_mask[j] |= 1 << i
     d.n_obb = len(spec.obbs)
     for b, o in enumerate(spec.obbs):
         for k in range(3):
@@ -220,6 +224,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
     d.lanes_per_particle = int(lanes_per_particle)
     d.block_threads = int(block_threads)
     d.block_sync = int(block_sync)
+    d.self_collision = int(bool(getattr(spec, "self_collision", False)))
     d.ik_iters = int(getattr(spec, "ik_iters", 0))
     d.ik_damping = float(getattr(spec, "ik_damping", 0.1))
     return d

@@ -12,9 +12,10 @@ GRAD_RTOL = 1e-3
 STEP_RTOL = 1e-3
 
 
-def oracle_inputs(cfg, n, seed, gofs=0):
+def oracle_inputs(cfg, n, seed, gofs=0, self_collision=False):
     """Oracle-sampled particles rounded to fp32: the common starting state of both sides."""
     spec = make_config(cfg, n=n)
+    spec.self_collision = self_collision
     csp = O.build_csp(spec)
     x, g = O.initialize_particles(spec, csp, seed, np.arange(gofs, gofs + n))
     x32, g32 = x.astype(np.float32), g.astype(np.float32)

@@ -357,3 +357,32 @@ def test_ik_sampler_converged_particles_match_oracle():
     ok_gpu = ((Jc[:, 2] <= 5e-3) & (Jc[:, 3] <= 0.05)).mean()
     ok_or = ((Jco[:, 2] <= 5e-3) & (Jco[:, 3] <= 0.05)).mean()
     assert abs(ok_gpu - ok_or) < 0.05
+
+
+@pytest.mark.parametrize("lanes", [4, 8, 16])
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_self_collision_term_matches_oracle(cfg, lanes):
+    """the SELF term (robot sphere pairs) -- cost, per-term values, gradient
+    and one Adam step against the oracle."""
+    n = 97 if cfg != 4 else 40
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=90 + cfg, self_collision=True)
+    assert "SELF" in [t.kind for t in csp.terms]
+    ctx = _ctx(spec, n, x32, g32, lanes=lanes, n_global=1000)
+    assert ctx.term_kinds == [t.kind for t in csp.terms]
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    selfc = np.array([t.kind == "SELF" for t in csp.terms])
+    assert (Jco[:, selfc] > 0).any()
+    ok = grad_ok(grad, grado)
+    kinks = kink_mask(spec, csp, x32.astype(np.float64), g32.astype(np.float64), grado,
+                      np.random.default_rng(0)) if not ok.all() else ~ok
+    assert np.all(ok | kinks) and kinks.mean() < 0.1
+    ctx.optimize(1)
+    x1 = ctx.get_state()["x"].cpu().numpy()
+    so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
+    O.optimize(spec, csp, so, 1, 1.0 / 1000)
+    unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
+    close = np.abs(x1 - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
+    assert np.all(close | unstable | kinks[:, None])

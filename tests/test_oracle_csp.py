@@ -216,12 +216,16 @@ def test_permutation_and_batch_split_invariance():
     np.testing.assert_array_equal(gr2, gr[2:3])
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, "1s"])
 def test_gradient_vs_central_fd(cfg):
     """Autograd gradient of Eq. 2 against central finite differences, excluding
-    coordinates whose FD is unstable between h and h/10 (kink neighbourhoods, "1e-4-wide")."""
+    coordinates whose FD is unstable between h and h/10 (kink neighbourhoods, "1e-4-wide").
+    "1s" = config 1 with the self-collision term."""
+    selfc = cfg == "1s"
+    cfg = 1 if selfc else cfg
     n = 3 if cfg != 4 else 2
     spec = make_config(cfg, n=n)
+    spec.self_collision = selfc
     csp = O.build_csp(spec)
     x, g = O.initialize_particles(spec, csp, 100 + cfg, np.arange(n))
     _, _, _, gr = O.cost_and_grad(spec, csp, x, g)
@@ -408,3 +412,31 @@ def test_plan_heuristic_eq5():
     """counts [10, 5] -> H = 7.5; a zero count takes the penalty."""
     assert O.plan_heuristic([10, 5], -100.0) == 7.5
     assert O.plan_heuristic([10, 0], -100.0) == -45.0
+
+
+def test_self_collision_term():
+    """SELF: 0 at the home pose; equals a brute-force loop over the robot's
+    sphere pairs on non-adjacent links; emitted after every CF term."""
+    from workloads.scenes import Q_HOME
+    spec = make_config(1, n=4)
+    spec.self_collision = True
+    csp = O.build_csp(spec)
+    assert [t.kind for t in csp.terms][:5] == ["JL", "CF", "SELF", "KP", "KR"]
+    rob = spec.robot
+    rng = np.random.default_rng(4)
+    q = rng.uniform(rob.joint_lo, rob.joint_hi, (64, 7))
+    q[0] = Q_HOME
+    x = np.zeros((64, csp.D))
+    off = csp.offsets[csp.terms[2].conf[1]]
+    x[:, off:off + 7] = q
+    g = np.tile(np.eye(3, 4)[None, None], (64, 1, 1, 1))
+    _, Jc, _ = _eval(spec, csp, x, g)
+    W = O.robot_sphere_centers(rob, O.forward_kinematics(rob, torch.tensor(q))).numpy()
+    r = rob.spheres[:, 3]
+    ref = np.zeros(64)
+    for i in range(len(r)):
+        for j in range(i + 1, len(r)):
+            if abs(int(rob.sphere_link[i]) - int(rob.sphere_link[j])) >= 2 and (i, j) != (7, 12):
+                ref += np.maximum(0.0, r[i] + r[j] - np.linalg.norm(W[:, i] - W[:, j], axis=-1))
+    np.testing.assert_allclose(Jc[:, 2], ref, rtol=1e-12, atol=1e-15)
+    assert Jc[0, 2] == 0.0 and (ref > 0).mean() > 0.2

@@ -42,6 +42,8 @@ class Robot:
     spheres: np.ndarray       # (S, 4)
     sphere_link: np.ndarray   # (S,) int in 1..8
     base: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(4))
+    # self-collision sphere pairs (i < j) checked by the SELF term
+    self_pairs: List[tuple] = dataclasses.field(default_factory=list)
 
 
 @dataclasses.dataclass
@@ -129,6 +131,7 @@ class ProblemSpec:
     lr_pos: float = 0.005
     lr_yaw: float = 0.01
     lr_knot: float = 0.01
+    self_collision: bool = False      # robot self-collision term per conf / knot
     n_particles: int = 256
     n_steps: int = 100
     # conditional IK sampler in InitializeParticles: damped-least-squares iterations (0 = uniform
@@ -137,8 +140,8 @@ class ProblemSpec:
     ik_damping: float = 0.1
 
 
-DEFAULT_LAM = dict(JL=1.0, CF=1.0, KP=1.0, KR=5.0, SS=2.0, SC=2.0, CP=1.0)
-DEFAULT_EPS = dict(JL=0.0, CF=1e-3, KP=5e-3, KR=0.05, SS=1e-2, SC=1e-3, CP=1e-3)
+DEFAULT_LAM = dict(JL=1.0, CF=1.0, KP=1.0, KR=5.0, SS=2.0, SC=2.0, CP=1.0, SELF=1.0)
+DEFAULT_EPS = dict(JL=0.0, CF=1e-3, KP=5e-3, KR=0.05, SS=1e-2, SC=1e-3, CP=1e-3, SELF=0.0)
 
 
 def _line_spheres(p0, p1, r, n=4):
@@ -180,9 +183,14 @@ def panda_robot() -> Robot:
     # tool frame (TCP, z = approach): hand + two finger pads
     add([[0, 0.05, -0.065, 0.03], [0, -0.05, -0.065, 0.03],
          [0, 0.042, -0.01, 0.012], [0, -0.042, -0.01, 0.012]], 8)
+    # self-collision pairs: spheres on non-adjacent links, minus the structural overlap of the sphere model
+    # (pair (7, 12) overlaps in 100 % of uniformly sampled confs; tools/gen_self_pairs.py)
+    ignore = {(7, 12)}
+    pairs = [(i, j) for i in range(len(sph)) for j in range(i + 1, len(sph))
+             if abs(link[i] - link[j]) >= 2 and (i, j) not in ignore]
     return Robot(dh=dh, flange_d=0.107, tcp_yaw=-math.pi / 4, tcp_d=0.1034,
                  joint_lo=lo, joint_hi=hi, spheres=np.array(sph, float),
-                 sphere_link=np.array(link, np.int32))
+                 sphere_link=np.array(link, np.int32), self_pairs=pairs)
 
 
 Q_HOME = np.array([0.0, -math.pi / 4, 0.0, -3 * math.pi / 4, 0.0, math.pi / 2, math.pi / 4])
