@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--lanes", type=int, default=0, help="lanes per particle in the particle kernel (0 = auto)")
     p.add_argument("--block-threads", type=int, default=0, help="particle-kernel block size (0 = auto)")
     p.add_argument("--block-sync", type=int, default=-1, help="block-synchronous phases (1/0, -1 = auto)")
+    p.add_argument("--self-collision", action="store_true", help="add the SELF term (SURVEY §8(f) f2)")
     p.add_argument("--ik-iters", type=int, default=20,
                    help="conditional IK sampler iterations in InitializeParticles (P:521); 0 = uniform confs")
     return p.parse_args()
@@ -313,6 +314,7 @@ def main():
         n = 131072 // 8                              # config 4: 128K particles over 8 GPUs (per-rank share)
     spec = make_config(cfg, n=n)
     spec.ik_iters = args.ik_iters
+    spec.self_collision = args.self_collision
     n_global = n * world
     ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes,
                       block_threads=args.block_threads, block_sync=args.block_sync)
@@ -416,7 +418,7 @@ def main():
                            "particles_per_gpu": n, "particles_global": n_global, "D": ctx.D,
                            "hard_terms": ctx.n_hard, "adam_steps_per_step": args.adam_steps,
                            "check_every": args.check_every, "best_k": args.k, "l2": "flushed between steps",
-                           "ik_iters": args.ik_iters,
+                           "ik_iters": args.ik_iters, "self_collision": args.self_collision,
                            "lanes_per_particle": ctx.lanes_per_particle, "block_threads": ctx.block_threads,
                            "block_sync": ctx.block_sync,
                            "parallelism": f"dp{world}"},

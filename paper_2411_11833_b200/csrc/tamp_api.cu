@@ -743,7 +743,7 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             pp = ((pp + ppw - 1) / ppw) * ppw;
             c->bsync = 1;
             if (pp <= max_pp) {
-                c->threads = (int)std::max<int64_t>(pp, 4 * ppw) * c->gs;
+                c->threads = (int)std::min<int64_t>(std::max<int64_t>(pp, 4 * ppw), std::max(max_pp, ppw)) * c->gs;
             } else {
                 const int regs = std::max(32, particle_kernel_regs(c->gs));
                 auto blocks_per_sm = [&](int t) {
