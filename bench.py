@@ -94,7 +94,7 @@ W_ADAM = 12         # per coordinate
 def algorithmic_instr(w):
     n_fk, S = w["n_fk"], w["n_robot_spheres"]
     return (n_fk * (W_FK + S * (W_SPH_XFORM + W_SPH_BWD) + W_LINK_BWD + W_JL)
-            + W_PAIR_SB * w["pairs_sphere_obb"] + W_PAIR_SS * w["pairs_sphere_sphere"]
+            + W_PAIR_SB * w["pairs_sphere_obb"] + W_PAIR_SS * (w["pairs_sphere_sphere"] + w.get("pairs_self", 0))
             + W_KIN * w["n_kin"] + W_PLACE * w["n_place"] + W_GOAL_PAIR * w["n_goal_pairs"]
             + W_SEG * w["n_traj_seg"] + W_ADAM * w["D"])
 

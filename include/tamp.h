@@ -173,6 +173,7 @@ typedef struct {
     int32_t n_kin, n_place, n_goal_pairs, n_traj_seg, n_robot_spheres;
     int32_t lanes_per_particle;           /* mapping chosen for the particle kernel */
     int32_t block_threads, block_sync;    /* launch configuration chosen for the particle kernel */
+    int64_t pairs_self;                   /* robot self-collision sphere pairs per particle-step */
 } tamp_info;
 
 typedef struct tamp_ctx tamp_ctx;

@@ -214,6 +214,19 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             packed[s] = lane * TAMP_MAX_SPHERES_PER_LINK + P.rsph_n[lane];
             P.rsph_n[lane]++;
         }
+        // link bounding spheres (self-collision broad phase)
+        for (int l = 0; l < kGroup; ++l) {
+            double c[3] = {0, 0, 0}, rad = 0;
+            const int ns = P.rsph_n[l];
+            for (int k = 0; k < ns; ++k)
+                for (int a = 0; a < 3; ++a) c[a] += P.rsph[l][k][a] / ns;
+            for (int k = 0; k < ns; ++k) {
+                const double dx = P.rsph[l][k][0] - c[0], dy = P.rsph[l][k][1] - c[1], dz = P.rsph[l][k][2] - c[2];
+                rad = std::max(rad, std::sqrt(dx * dx + dy * dy + dz * dz) + P.rsph[l][k][3]);
+            }
+            for (int a = 0; a < 3; ++a) P.lbound[l][a] = (float)c[a];
+            P.lbound[l][3] = ns ? (float)(rad * (1.0 + 1e-5) + 1e-6) : 0.f;   // no spheres: no pairs either
+        }
         // self-collision pairs in packed sphere ids
         if (d.self_collision) {
             P.has_self = 1;
@@ -551,7 +564,7 @@ static void smem_layout(tamp_ctx* c) {
     c->off_gTi = off;
     off += 16 * P.n_grasp;
     c->off_rsw = off;                                 // robot sphere centres for the SELF term (2 FK halves)
-    off += P.has_self ? 2 * 4 * kGroup * TAMP_MAX_SPHERES_PER_LINK : 0;
+    off += P.has_self ? 2 * 4 * (kGroup * TAMP_MAX_SPHERES_PER_LINK + kGroup) : 0;   // + link bounding spheres
     // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
     int stride = ((off + 31) / 32) * 32 + 8;
     c->stride = stride;
@@ -835,6 +848,12 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     out->lanes_per_particle = c->gs;
     out->block_threads = c->threads;
     out->block_sync = c->bsync;
+    {
+        int64_t per_conf = 0, n_self = 0;
+        for (int i = 0; i < kGroup * TAMP_MAX_SPHERES_PER_LINK; ++i) per_conf += __builtin_popcount(c->P.self_mask[i]);
+        for (int f = 0; f < c->P.n_fk; ++f) n_self += c->P.fk[f].term_self >= 0 && !c->P.fk[f].ghost;
+        out->pairs_self = per_conf / 2 * n_self;
+    }
     return TAMP_OK;
 }
 

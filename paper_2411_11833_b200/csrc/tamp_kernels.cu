@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3]);
         s_selfmask[threadIdx.x] = P.self_mask[threadIdx.x];
     }
-    float4* rsw = reinterpret_cast<float4*>(S + A.off_rsw) + (HP > 1 ? half : 0) * kGroup * TAMP_MAX_SPHERES_PER_LINK;
+    float4* rsw = reinterpret_cast<float4*>(S + A.off_rsw) + (HP > 1 ? half : 0) * (kGroup * TAMP_MAX_SPHERES_PER_LINK + kGroup);
+    float4* rlb = rsw + kGroup * TAMP_MAX_SPHERES_PER_LINK;       // world bounding sphere of each link frame
     int nsph[LPL];
     float jlo[LPL], jhi[LPL];
 #pragma unroll
@@ -577,20 +578,41 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
                     rsw[ll * NS + s] = make_float4(w[s][0], w[s][1], w[s][2], rr[s] - P.eta);
+#pragma unroll
+                for (int u = 0; u < LPL; ++u) {
+                    const float* lb = P.lbound[ll * LPL + u];
+                    float bx, by, bz;
+                    xform(T[u], lb[0], lb[1], lb[2], bx, by, bz);
+                    rlb[ll * LPL + u] = make_float4(bx, by, bz, lb[3] + P.eta);
+                }
                 __syncwarp();
                 float js = 0.f;
                 const float lam_self = P.term_lam[K.term_self];
 #pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    const int sid = ll * NS + s;
-                    uint32_t m = s_selfmask[sid];
-                    while (m) {
-                        const int t = __ffs(m) - 1;
-                        m &= m - 1u;
-                        float ux, uy, uz;
-                        const float pen = sphere_sphere<GRAD>(w[s][0], w[s][1], w[s][2], rr[s], rsw[t], lam_self, ux, uy, uz);
-                        if (sid < t) js += pen;
-                        if (GRAD) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
+                for (int u = 0; u < LPL; ++u) {
+                    // broad phase: links whose bounding spheres overlap this link's
+                    const float4 a4 = rlb[ll * LPL + u];
+                    uint32_t near = 0u;
+#pragma unroll
+                    for (int m = 0; m < kGroup; ++m) {
+                        const float4 b4 = rlb[m];
+                        const float dx = a4.x - b4.x, dy = a4.y - b4.y, dz = a4.z - b4.z;
+                        const float R = a4.w + b4.w;
+                        near |= (fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f ? 0xFu : 0u) << (4 * m);
+                    }
+#pragma unroll
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                        const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
+                        const int sid = ll * NS + s;
+                        uint32_t m = s_selfmask[sid] & near;
+                        while (m) {
+                            const int t = __ffs(m) - 1;
+                            m &= m - 1u;
+                            float ux, uy, uz;
+                            const float pen = sphere_sphere<GRAD>(w[s][0], w[s][1], w[s][2], rr[s], rsw[t], lam_self, ux, uy, uz);
+                            if (sid < t) js += pen;
+                            if (GRAD) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
+                        }
                     }
                 }
                 finish_term<MODE>(P, A, sinkB, K.term_self, gsum<LPF>(js), ll, active, p, s_counts, real);
@@ -765,10 +787,11 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                     }
                 }
             }
-            // keep the block's warps in step through the (large) FK loop body (profiles/README.md)
-            if (BSYNC >= 2) __syncthreads();
+            // keep the block's warps in step through the (large) FK loop body (profiles/README.md):
+            // every FK instance (2) or every other one (3)
+            if (BSYNC == 2 || (BSYNC == 3 && ((f0 / HP) & 1))) __syncthreads();
         }
-        if (BSYNC == 1) phase_sync();   // all warps leave the FK loop before any enters phase C
+        if (BSYNC == 1 || BSYNC == 3) phase_sync();   // all warps leave the FK loop before phase C
         // combine the halves' phase-B terms
         if (HP > 1) {
             sinkB.J += __shfl_xor_sync(FULL, sinkB.J, LPF);
@@ -1338,6 +1361,7 @@ static cudaError_t launch_particle_map(int mode, int bsync, const KProgram& P, c
     switch (bsync) {
         case 0: return launch_particle_t<MODE_OPT, LPF, HP, 0>(P, A, threads, smem, st);
         case 1: return launch_particle_t<MODE_OPT, LPF, HP, 1>(P, A, threads, smem, st);
+        case 3: return launch_particle_t<MODE_OPT, LPF, HP, 3>(P, A, threads, smem, st);
         default: return launch_particle_t<MODE_OPT, LPF, HP, 2>(P, A, threads, smem, st);
     }
 }

@@ -84,6 +84,7 @@ struct KProgram {
     float obound[TAMP_MAX_OBJECTS][4];   // bounding sphere of each object's spheres (object frame xyz, radius)
     // self-collision: bit t of self_mask[s] = check robot spheres s, t (packed ids: link lane * 4 + k)
     uint32_t self_mask[kGroup * TAMP_MAX_SPHERES_PER_LINK];
+    float lbound[kGroup][4];             // bounding sphere of each link frame's spheres (link frame xyz, radius)
     int32_t has_self;
 };
 

@@ -89,7 +89,7 @@ class Info(ctypes.Structure):
                 ("n_local", I64), ("global_offset", I64), ("n_global", I64), ("t", I32),
                 ("pairs_sphere_obb", I64), ("pairs_sphere_sphere", I64), ("n_kin", I32), ("n_place", I32),
                 ("n_goal_pairs", I32), ("n_traj_seg", I32), ("n_robot_spheres", I32),
-                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32)]
+                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32), ("pairs_self", I64)]
 
 
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
@@ -267,7 +267,7 @@ class TampContext:
         self.work = dict(pairs_sphere_obb=info.pairs_sphere_obb, pairs_sphere_sphere=info.pairs_sphere_sphere,
                          n_kin=info.n_kin, n_place=info.n_place, n_goal_pairs=info.n_goal_pairs,
                          n_traj_seg=info.n_traj_seg, n_robot_spheres=info.n_robot_spheres, n_fk=info.n_fk,
-                         D=info.D)
+                         D=info.D, pairs_self=info.pairs_self)
         self.lanes_per_particle = info.lanes_per_particle
         self.block_threads, self.block_sync = info.block_threads, info.block_sync
         self.counts_buf = torch.zeros(self.n_hard + 2, dtype=torch.int32, device=self.device)
