@@ -98,11 +98,14 @@ typedef struct {
 typedef struct { float center[3]; float yaw; float half[3]; } tamp_obb_desc;
 
 /* movable object as spheres in its frame (origin = bottom centre, L15); sampler parameters:
-   footprint = radius shrinking placement regions; top-down grasp TCP at (u*grasp_xy, v*grasp_xy, grasp_z) */
+   footprint = radius shrinking placement regions; top-down grasp TCP at (u*grasp_xy, v*grasp_xy, grasp_z);
+   grasp_mode 0 = top-down 4-DOF, 1 = 6-DOF (top or one of the 4 sides, approach through the vertical axis
+   at height grasp_z; "top-down 4-DOF or 6-DOF poses") */
 typedef struct {
     int32_t n_spheres;
     float sphere[TAMP_MAX_OBJ_SPHERES][4];
     float footprint, grasp_xy, grasp_z;
+    int32_t grasp_mode;
 } tamp_object_desc;
 
 /* placement surface: frame (x, y, z_top, yaw) in the world, rectangle lo/hi in that frame;
@@ -153,6 +156,9 @@ typedef struct {
     int32_t block_sync;                   /* block-synchronous phases: 0 off, 1 phase boundaries, 2 + every
                                              FK instance, 3 + inside the FK body; -1 auto (2) */
     int32_t self_collision;               /* 1: add a SELF term after every CF term */
+    int32_t collision_smooth;             /* 1: CHOMP-smooth collision cost instead of the hinge:
+                                             p - eta/2 (p > eta), p^2/(2 eta) (0 < p <= eta), p = r + eta - sd;
+                                             needs eta > 0 */
     int32_t ik_iters;                     /* conditional IK sampler: damped-least-squares iterations
                                              per Pick/Place conf inside tamp_sample_particles; 0 = uniform confs */
     float ik_damping;                     /* DLS damping mu (dq = J^T (J J^T + mu^2 I)^-1 e) */

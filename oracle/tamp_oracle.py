@@ -56,6 +56,15 @@ def rot_z(a):
                         torch.stack([z, z, o, z], -1), torch.stack([z, z, z, o], -1)], -2)
 
 
+def rot_y(a):
+    """Ry(a) as [..., 4, 4]."""
+    a = _t(a)
+    c, s = torch.cos(a), torch.sin(a)
+    z, o = torch.zeros_like(a), torch.ones_like(a)
+    return torch.stack([torch.stack([c, z, s, z], -1), torch.stack([z, o, z, z], -1),
+                        torch.stack([-s, z, c, z], -1), torch.stack([z, z, z, o], -1)], -2)
+
+
 def trans(x, y, z):
     """Translation as [..., 4, 4]."""
     x, y, z = _t(x), _t(y), _t(z)
@@ -132,20 +141,29 @@ def obb_arrays(obb):
     return _t(obb.center), R, _t(obb.half)
 
 
-def sphere_obb_cost(w, r, obbs, eta):
+def collision_cost(p, eta, smooth=False):
+    """Cost of a penetration depth p = r + eta - sd.  Hinge max(0, p) (L1); with `smooth` the CHOMP obstacle
+    cost (Zucker et al. 2013; the "smooth gradients" of P:490): p - eta/2 for p > eta,
+    p^2 / (2 eta) for 0 < p <= eta, 0 otherwise (continuously differentiable; needs eta > 0)."""
+    if not smooth:
+        return p.clamp(min=0.0)
+    return torch.where(p > eta, p - eta / 2, torch.where(p > 0, p * p / (2 * eta), torch.zeros_like(p)))
+
+
+def sphere_obb_cost(w, r, obbs, eta, smooth=False):
     """Sum over (sphere, box) pairs of max(0, r + eta - sd)  (L1 hinge, L2 sum)."""
     tot = torch.zeros(w.shape[0], dtype=DT)
     for obb in obbs:
         c, R, h = obb_arrays(obb)
         sd = box_signed_distance(w, c, R, h)
-        tot = tot + (r + eta - sd).clamp(min=0.0).sum(-1)
+        tot = tot + collision_cost(r + eta - sd, eta, smooth).sum(-1)
     return tot
 
 
-def sphere_sphere_cost(wa, ra, wb, rb, eta):
+def sphere_sphere_cost(wa, ra, wb, rb, eta, smooth=False):
     """Sum over sphere pairs of max(0, ra + rb + eta - ||wa - wb||)."""
     d = torch.linalg.vector_norm(wa[:, :, None, :] - wb[:, None, :, :], dim=-1)
-    return (ra[:, None] + rb[None, :] + eta - d).clamp(min=0.0).sum((-1, -2))
+    return collision_cost(ra[:, None] + rb[None, :] + eta - d, eta, smooth).sum((-1, -2))
 
 
 def dist_from_bounds(vals, lower, upper):
@@ -179,6 +197,22 @@ def pose_error(Ta, Tb):
     """Kin residuals (Listing 2 curobo_pose_error P:1570-1589): (||t_a - t_b||, angle(R_a, R_b)) (L4, L5)."""
     return (torch.linalg.vector_norm(Ta[..., :3, 3] - Tb[..., :3, 3], dim=-1),
             rotation_angle(Ta[..., :3, :3], Tb[..., :3, :3]))
+
+
+def six_dof_grasp(face, gx, gy, gz, gamma):
+    """6-DOF grasp (P:629 "top-down 4-DOF or 6-DOF poses"; SURVEY f4, PROPOSAL): face 0 = top-down as above;
+    faces 1-4 approach the object's +x, -x, +y, -y side horizontally at height gz through its vertical axis:
+    T(g) = Trans(0, 0, gz) R_face Rz(gamma), R_face turning the approach (TCP z) axis to -n_face."""
+    top = top_down_grasp(gx, gy, gz, gamma)
+    zero = torch.zeros_like(_t(gamma))
+    faces = [None, rot_y(zero - math.pi / 2), rot_y(zero + math.pi / 2), rot_x(zero + math.pi / 2),
+             rot_x(zero - math.pi / 2)]
+    side = [None] + [trans(zero, zero, gz) @ Rf @ rot_z(gamma) for Rf in faces[1:]]
+    face = torch.as_tensor(face)
+    out = top.clone()
+    for f in range(1, 5):
+        out = torch.where((face == f)[:, None, None], side[f], out)
+    return out
 
 
 def top_down_grasp(gx, gy, gz, gamma):
@@ -342,6 +376,16 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
     grasps = np.zeros((N, len(csp.grasp_vars), 3, 4))
     for gi, vi in enumerate(csp.grasp_vars):
         o = spec.objects[V[vi].obj]
+        if getattr(o, "grasp_mode", 0) == 1:     # 6-DOF: face, gx, gy, gamma
+            u = uniforms(seed, gidx, vi, 4)
+            face = np.minimum(np.floor(u[:, 0] * 5), 4).astype(np.int64)
+            gx = -o.grasp_xy + 2 * o.grasp_xy * u[:, 1]
+            gy = -o.grasp_xy + 2 * o.grasp_xy * u[:, 2]
+            gamma = -math.pi + 2 * math.pi * u[:, 3]
+            T = six_dof_grasp(face, torch.as_tensor(gx), torch.as_tensor(gy),
+                              torch.full((N,), o.grasp_z, dtype=DT), torch.as_tensor(gamma))
+            grasps[:, gi] = T[:, :3, :].numpy()
+            continue
         u = uniforms(seed, gidx, vi, 3)
         gx = -o.grasp_xy + 2 * o.grasp_xy * u[:, 0]
         gy = -o.grasp_xy + 2 * o.grasp_xy * u[:, 1]
@@ -414,6 +458,7 @@ def evaluate(spec: ProblemSpec, csp: CSP, x: torch.Tensor, grasps: torch.Tensor)
     rob = spec.robot
     N = x.shape[0]
     eta = spec.eta
+    smooth = bool(getattr(spec, "collision_smooth", False))
     bottom = torch.zeros(1, 1, 1, 4, dtype=DT)
     bottom[..., 3] = 1.0
     G = torch.cat([grasps, bottom.expand(N, grasps.shape[1], 1, 4)], dim=-2)   # [N, G, 4, 4]
@@ -450,12 +495,12 @@ def evaluate(spec: ProblemSpec, csp: CSP, x: torch.Tensor, grasps: torch.Tensor)
         return transform_points(T, _t(s[:, :3])), _t(s[:, 3])
 
     def scene_cost(w, r, scene, skip_objs, obbs):
-        tot = sphere_obb_cost(w, r, obbs, eta)
+        tot = sphere_obb_cost(w, r, obbs, eta, smooth)
         for o, pv in scene.items():
             if o in skip_objs:
                 continue
             wo, ro = obj_spheres(o, placement_T(pv))
-            tot = tot + sphere_sphere_cost(w, r, wo, ro, eta)
+            tot = tot + sphere_sphere_cost(w, r, wo, ro, eta, smooth)
         return tot
 
     Jc = []
@@ -477,7 +522,7 @@ def evaluate(spec: ProblemSpec, csp: CSP, x: torch.Tensor, grasps: torch.Tensor)
             ii = torch.as_tensor([a for a, _ in rob.self_pairs], dtype=torch.long)
             jj = torch.as_tensor([b for _, b in rob.self_pairs], dtype=torch.long)
             d = torch.linalg.vector_norm(w[:, ii] - w[:, jj], dim=-1)
-            Jc.append((r_rob[ii] + r_rob[jj] + eta - d).clamp(min=0.0).sum(-1))
+            Jc.append(collision_cost(r_rob[ii] + r_rob[jj] + eta - d, eta, smooth).sum(-1))
         elif t.kind in ("KP", "KR"):   # Kin(q, o, g, p): FK(q) = p . g
             target = placement_T(t.placement) @ G[:, gslot[t.grasp]]
             e_pos, e_rot = pose_error(fk(t.conf)[:, 8], target)

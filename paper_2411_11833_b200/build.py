@@ -4,11 +4,15 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRCS = [os.path.join(HERE, "csrc", f) for f in ("tamp_api.cu", "tamp_kernels.cu")]
-HDRS = [os.path.join(HERE, "csrc", "tamp_program.h"), os.path.join(ROOT, "include", "tamp.h")]
+# one translation unit per instantiation group so the (slow) k_particle variants compile in parallel
+SRCS = [os.path.join(HERE, "csrc", f) for f in ("tamp_api.cu", "tamp_kernels.cu", "tamp_particle_hinge.cu",
+                                                 "tamp_particle_smooth.cu")]
+HDRS = [os.path.join(HERE, "csrc", "tamp_program.h"), os.path.join(HERE, "csrc", "particle.cuh"),
+        os.path.join(ROOT, "include", "tamp.h")]
 LIB = os.path.join(HERE, "libtamp.so")
+OBJ_DIR = os.path.join(HERE, "csrc", "build")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc():
@@ -29,15 +33,27 @@ def build(force=False, verbose=False):
     """Compile csrc/*.cu into paper_2411_11833_b200/libtamp.so (sm_100a).  Returns the path."""
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + SRCS
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    objs = [os.path.join(OBJ_DIR, os.path.basename(s)[:-3] + ".o") for s in SRCS]
+    procs = [subprocess.Popen([nvcc()] + NVCC_FLAGS + ["-c", "-o", o, s], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for s, o in zip(SRCS, objs)]
+    logs, failed = [], []
+    for s, p in zip(SRCS, procs):
+        out, err = p.communicate()
+        logs.append(f"== {os.path.basename(s)}\n{out}{err}")
+        if p.returncode != 0:
+            failed.append(s)
+    if failed:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(logs))
+    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"]
+                         + objs, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     os.replace(LIB + ".tmp", LIB)
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+        f.write("\n".join(logs))
     if verbose:
-        print(res.stderr)
+        print("\n".join(logs))
     return LIB
 
 

@@ -496,6 +496,8 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
     }
     P.grad_scale = d.grad_scale > 0.f ? d.grad_scale : (float)(1.0 / (double)n_global);
     P.eta = d.eta;
+    REQUIRE(!d.collision_smooth || d.eta > 0.f, TAMP_E_INVALID, "collision_smooth needs eta > 0");
+    P.smooth = d.collision_smooth ? d.eta : 0.f;
     P.beta1 = d.beta1;
     P.beta2 = d.beta2;
     P.adam_eps = d.adam_eps;
@@ -516,6 +518,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             S.kind = KS_GRASP;
             S.a[0] = d.object[V.obj].grasp_xy;
             S.a[1] = d.object[V.obj].grasp_z;
+            S.a[2] = d.object[V.obj].grasp_mode == 1 ? 1.f : 0.f;
         } else if (V.kind == TAMP_VAR_PLACEMENT) {
             const tamp_surface_desc& Sf = d.surface[V.surface];
             S.kind = KS_PLACEMENT;
@@ -783,9 +786,9 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             delete c;
             return fail(TAMP_E_UNSUPPORTED, "block too large for shared memory");
         }
-        if (desc->block_sync > 3) {
+        if (desc->block_sync > 2) {
             delete c;
-            return fail(TAMP_E_INVALID, "block_sync must be -1 (auto) or 0..3");
+            return fail(TAMP_E_INVALID, "block_sync must be -1 (auto) or 0..2");
         }
         if (desc->block_threads && desc->block_sync < 0) c->bsync = 2;
         if (desc->block_sync >= 0) c->bsync = desc->block_sync;

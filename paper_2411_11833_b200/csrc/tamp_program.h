@@ -61,6 +61,7 @@ struct KObb { float R[9]; float c[3]; float h[3]; float rad; };   // rad = |h| (
 struct KProgram {
     int32_t D, n_terms, n_fk, n_inst, n_place, n_traj, n_goal, n_grasp, n_obb;
     float grad_scale, eta, beta1, beta2, adam_eps, lam_goal, lam_traj;
+    float smooth;                        // CHOMP-smooth collision cost width (= eta) or 0 = hinge
     KFk fk[TAMP_MAX_FK];
     KInst inst[kMaxInst];
     KPlace place[kMaxPlace];

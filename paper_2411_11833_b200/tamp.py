@@ -51,7 +51,7 @@ class ObbDesc(ctypes.Structure):
 
 class ObjectDesc(ctypes.Structure):
     _fields_ = [("n_spheres", I32), ("sphere", F * 4 * MAX_OBJ_SPHERES), ("footprint", F), ("grasp_xy", F),
-                ("grasp_z", F)]
+                ("grasp_z", F), ("grasp_mode", I32)]
 
 
 class SurfaceDesc(ctypes.Structure):
@@ -81,7 +81,7 @@ class ProblemDesc(ctypes.Structure):
                 ("beta1", F), ("beta2", F), ("adam_eps", F),
                 ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F),
                 ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32),
-                ("self_collision", I32), ("ik_iters", I32), ("ik_damping", F)]
+                ("self_collision", I32), ("collision_smooth", I32), ("ik_iters", I32), ("ik_damping", F)]
 
 
 class Info(ctypes.Structure):
@@ -187,6 +187,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
         d.object[i].footprint = float(o.footprint)
         d.object[i].grasp_xy = float(o.grasp_xy)
         d.object[i].grasp_z = float(o.grasp_z)
+        d.object[i].grasp_mode = int(getattr(o, "grasp_mode", 0))
     d.n_surfaces = len(spec.surfaces)
     for i, s in enumerate(spec.surfaces):
         for k in range(4):
@@ -225,6 +226,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
     d.block_threads = int(block_threads)
     d.block_sync = int(block_sync)
     d.self_collision = int(bool(getattr(spec, "self_collision", False)))
+    d.collision_smooth = int(bool(getattr(spec, "collision_smooth", False)))
     d.ik_iters = int(getattr(spec, "ik_iters", 0))
     d.ik_damping = float(getattr(spec, "ik_damping", 0.1))
     return d

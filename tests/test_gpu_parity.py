@@ -30,11 +30,15 @@ def _ctx(spec, n, x32, g32, gofs=0, n_global=None, lanes=0):
 
 
 # ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("grasp_mode", [0, 1])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4])
-def test_sampler_matches_oracle(cfg):
-    """K1 (Philox + samplers) vs the oracle's InitializeParticles; ragged N, nonzero global offset."""
+def test_sampler_matches_oracle(cfg, grasp_mode):
+    """K1 (Philox + samplers) vs the oracle's InitializeParticles; ragged N, nonzero global offset;
+    top-down (0) and 6-DOF (1) grasp samplers."""
     n, gofs = 301, 1000
     spec = make_config(cfg, n=n)
+    for o in spec.objects:
+        o.grasp_mode = grasp_mode
     csp = O.build_csp(spec)
     ctx = TampContext(spec, n, global_offset=gofs, n_global=4096)
     ctx.sample(seed=77 + cfg)
@@ -375,6 +379,33 @@ def test_self_collision_term_matches_oracle(cfg, lanes):
     np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
     selfc = np.array([t.kind == "SELF" for t in csp.terms])
     assert (Jco[:, selfc] > 0).any()
+    ok = grad_ok(grad, grado)
+    kinks = kink_mask(spec, csp, x32.astype(np.float64), g32.astype(np.float64), grado,
+                      np.random.default_rng(0)) if not ok.all() else ~ok
+    assert np.all(ok | kinks) and kinks.mean() < 0.1
+    ctx.optimize(1)
+    x1 = ctx.get_state()["x"].cpu().numpy()
+    so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
+    O.optimize(spec, csp, so, 1, 1.0 / 1000)
+    unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
+    close = np.abs(x1 - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
+    assert np.all(close | unstable | kinks[:, None])
+
+
+@pytest.mark.parametrize("lanes", [4, 8, 16])
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_smooth_collision_matches_oracle(cfg, lanes):
+    """CHOMP-smooth collision cost (eta = 2 cm) on CF / CP / SELF -- cost, per-term values,
+    gradient and one Adam step against the oracle."""
+    n = 97
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=110 + cfg, self_collision=True)
+    spec.collision_smooth = True
+    spec.eta = float(np.float32(0.02))
+    ctx = _ctx(spec, n, x32, g32, lanes=lanes, n_global=1000)
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
     ok = grad_ok(grad, grado)
     kinks = kink_mask(spec, csp, x32.astype(np.float64), g32.astype(np.float64), grado,
                       np.random.default_rng(0)) if not ok.all() else ~ok

@@ -440,3 +440,52 @@ def test_self_collision_term():
                 ref += np.maximum(0.0, r[i] + r[j] - np.linalg.norm(W[:, i] - W[:, j], axis=-1))
     np.testing.assert_allclose(Jc[:, 2], ref, rtol=1e-12, atol=1e-15)
     assert Jc[0, 2] == 0.0 and (ref > 0).mean() > 0.2
+
+
+def test_smooth_collision_cost_shape():
+    """CHOMP-smooth cost: 0 below contact, quadratic up to eta, linear beyond; C^1 at 0
+    and eta; the hinge minus eta/2 deep inside."""
+    eta = 0.02
+    p = torch.tensor([-0.01, 0.0, 0.005, 0.02, 0.05], dtype=DT, requires_grad=True)
+    c = O.collision_cost(p, eta, smooth=True)
+    np.testing.assert_allclose(c.detach().numpy(), [0.0, 0.0, 0.005 ** 2 / 0.04, 0.01, 0.04], atol=1e-15)
+    c.sum().backward()
+    np.testing.assert_allclose(p.grad.numpy(), [0.0, 0.0, 0.25, 1.0, 1.0], atol=1e-12)
+    np.testing.assert_allclose(O.collision_cost(p.detach(), eta).numpy(), [0, 0, 0.005, 0.02, 0.05], atol=1e-15)
+
+
+def test_smooth_collision_gradient_vs_fd():
+    spec = make_config(2, n=3)
+    spec.collision_smooth = True
+    spec.eta = 0.02
+    spec.self_collision = True
+    csp = O.build_csp(spec)
+    x, g = O.initialize_particles(spec, csp, 5, np.arange(3))
+    _, _, _, gr = O.cost_and_grad(spec, csp, x, g)
+    h = 1e-6
+    for d in range(0, csp.D, 5):
+        xp, xm = x.copy(), x.copy()
+        xp[:, d] += h
+        xm[:, d] -= h
+        fd = (_eval(spec, csp, xp, g)[0] - _eval(spec, csp, xm, g)[0]) / (2 * h)
+        np.testing.assert_allclose(gr[:, d], fd, rtol=1e-4, atol=1e-5)
+
+
+def test_six_dof_grasp_sampler():
+    """6-DOF grasps: proper rotations whose approach axis is -z (top) or horizontal into one
+    of the four sides, faces roughly uniform; top-down mode unchanged."""
+    spec = make_config(1, n=2000)
+    spec.objects[0].grasp_mode = 1
+    csp = O.build_csp(spec)
+    _, g = O.initialize_particles(spec, csp, 3, np.arange(2000))
+    R = g[:, 0, :, :3]
+    np.testing.assert_allclose(R @ R.transpose(0, 2, 1), np.tile(np.eye(3), (2000, 1, 1)), atol=1e-12)
+    np.testing.assert_allclose(np.linalg.det(R), 1.0, atol=1e-12)
+    a = R[:, :, 2]
+    dirs = np.array([[0, 0, -1], [-1, 0, 0], [1, 0, 0], [0, -1, 0], [0, 1, 0]], float)
+    face = np.argmax(a @ dirs.T, axis=1)
+    np.testing.assert_allclose(a, dirs[face], atol=1e-12)
+    h = np.bincount(face, minlength=5)
+    assert ((h - 400.0) ** 2 / 400.0).sum() < 18.5          # chi^2, 4 dof, p = 0.001
+    side = face > 0
+    np.testing.assert_allclose(g[side, 0, :2, 3], 0.0, atol=1e-15)

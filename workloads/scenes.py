@@ -64,6 +64,7 @@ class Obj:
     footprint: float          # radius used to shrink placement sampling regions
     grasp_xy: float           # top-down grasp sampler: TCP xy uniform in [-grasp_xy, grasp_xy]^2 (object frame)
     grasp_z: float            # TCP height above the object bottom
+    grasp_mode: int = 0       # 0: top-down 4-DOF grasps; 1: 6-DOF grasps (top or one of the four sides)
 
 
 @dataclasses.dataclass
@@ -132,6 +133,7 @@ class ProblemSpec:
     lr_yaw: float = 0.01
     lr_knot: float = 0.01
     self_collision: bool = False      # robot self-collision term per conf / knot
+    collision_smooth: bool = False    # CHOMP-smooth collision cost (needs eta > 0)
     n_particles: int = 256
     n_steps: int = 100
     # conditional IK sampler in InitializeParticles: damped-least-squares iterations (0 = uniform
