@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TAMP_ABI_VERSION 1
+#define TAMP_ABI_VERSION 2
 
 /* compiled limits of the sm_100a kernels (exceeding one returns TAMP_E_UNSUPPORTED) */
 #define TAMP_NJ 7                     /* 7-DOF arm */
@@ -68,15 +68,26 @@ typedef enum {
 
 /* variable kinds */
 enum { TAMP_VAR_CONF = 0, TAMP_VAR_PLACEMENT = 1, TAMP_VAR_GRASP = 2, TAMP_VAR_TRAJ = 3 };
-/* actions of Listing 1 */
-enum { TAMP_MOVE_FREE = 0, TAMP_PICK = 1, TAMP_MOVE_HOLD = 2, TAMP_PLACE = 3 };
+/* actions of Listing 1 and of the Stick Button domain:
+   PressButton(b, p, q): hand empty; `obj` = the robot's virtual fingertip object (an object with no
+     constant initial placement: never in the scene), `grasp` = its grasp variable (TCP pose in the
+     fingertip frame), `placement` = the press pose p (a placement variable of the fingertip object),
+     `surface` = the button's top face (support_obb = the button); conf q1.
+   PressButtonStick(b, o, g, p, q): stick o held with grasp g; `placement` = the stick's pose p while
+     pressing (a placement variable of o), `surface` = the button's top face; conf q1.  o stays held. */
+enum { TAMP_MOVE_FREE = 0, TAMP_PICK = 1, TAMP_MOVE_HOLD = 2, TAMP_PLACE = 3, TAMP_PRESS = 4,
+       TAMP_PRESS_STICK = 5 };
 /* hard-constraint term kinds (SURVEY §8(c) term table):
    JL joint limits (Motion); CF robot collision (CFreeTraj/CFreeHold/CFreeTrajHold,
    P:1029-1031); KP/KR kinematics position/rotation (Kin); SS/SC stable-place support /
    containment; CP CFreePlace; SELF robot self-collision ("does not cause
-   robot self-collisions", tolerance 0 P:1132; enabled by desc.self_collision). */
+   robot self-collisions", tolerance 0 P:1132; enabled by desc.self_collision);
+   PC press contact (ValidPress / ValidStickPress, R8): min over the pressing
+   object's spheres of dist_from_bounds(xy in the button-face frame, lo, hi); with SS (the object's bottom
+   at the face height) it says "some point of the fingertip / stick touches the button's top face". */
 enum { TAMP_TERM_JL = 0, TAMP_TERM_CF = 1, TAMP_TERM_KP = 2, TAMP_TERM_KR = 3,
-       TAMP_TERM_SS = 4, TAMP_TERM_SC = 5, TAMP_TERM_CP = 6, TAMP_TERM_SELF = 7, TAMP_N_TERM_KINDS = 8 };
+       TAMP_TERM_SS = 4, TAMP_TERM_SC = 5, TAMP_TERM_CP = 6, TAMP_TERM_SELF = 7, TAMP_TERM_PC = 8,
+       TAMP_N_TERM_KINDS = 9 };
 
 /* Serial 7-DOF arm, modified (Craig) DH: frame_j = frame_{j-1} Rx(alpha_{j-1}) Tx(a_{j-1}) Tz(d_j) Rz(q_j);
    tool/TCP = frame_7 Tz(flange_d) Rz(tcp_yaw) Tz(tcp_d); frame_0 = Trans(base xyz) Rz(base yaw).
@@ -98,14 +109,18 @@ typedef struct {
 typedef struct { float center[3]; float yaw; float half[3]; } tamp_obb_desc;
 
 /* movable object as spheres in its frame (origin = bottom centre, L15); sampler parameters:
-   footprint = radius shrinking placement regions; top-down grasp TCP at (u*grasp_xy, v*grasp_xy, grasp_z);
+   footprint = radius shrinking placement regions; top-down grasp TCP at (u*grasp_xy, v*grasp_y, grasp_z),
+   u, v uniform in [-1, 1] (grasp_y < 0: grasp_y = grasp_xy);
    grasp_mode 0 = top-down 4-DOF, 1 = 6-DOF (top or one of the 4 sides, approach through the vertical axis
-   at height grasp_z; "top-down 4-DOF or 6-DOF poses") */
+   at height grasp_z; "top-down 4-DOF or 6-DOF poses").  An object with no constant initial
+   placement variable is virtual (the fingertip of PressButton): never in the scene, never a collision
+   partner. */
 typedef struct {
     int32_t n_spheres;
     float sphere[TAMP_MAX_OBJ_SPHERES][4];
     float footprint, grasp_xy, grasp_z;
     int32_t grasp_mode;
+    float grasp_y;
 } tamp_object_desc;
 
 /* placement surface: frame (x, y, z_top, yaw) in the world, rectangle lo/hi in that frame;

@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from workloads.scenes import (ProblemSpec, CONF, PLACEMENT, GRASP, TRAJ,
-                              MOVE_FREE, PICK, MOVE_HOLD, PLACE)
+                              MOVE_FREE, PICK, MOVE_HOLD, PLACE, PRESS, PRESS_STICK)
 from .philox import uniforms
 
 DT = torch.float64
@@ -226,10 +226,11 @@ def top_down_grasp(gx, gy, gz, gamma):
 # ----------------------------------------------------------------------------------------------
 @dataclasses.dataclass
 class Term:
-    kind: str                       # JL CF KP KR SS SC CP
+    kind: str                       # JL CF KP KR SS SC CP SELF PC
     conf: Optional[tuple] = None    # ("var", v) or ("knot", traj_var, j)
     scene: Optional[Dict[int, int]] = None   # object -> pose variable, objects present (not held)
     excl: Tuple[int, ...] = ()      # objects excluded from the robot check
+    excl_obb: Tuple[int, ...] = ()  # OBBs excluded from the robot check (the button being pressed)
     held: Optional[Tuple[int, int]] = None   # (obj, grasp var) attached at a knot (MoveHold)
     obj: int = -1
     grasp: int = -1
@@ -320,6 +321,27 @@ def build_csp(spec: ProblemSpec) -> CSP:
             terms.append(Term("CP", obj=a.obj, placement=a.placement, surface=a.surface, scene=scene))
             pose[a.obj] = a.placement
             held = None
+        elif a.kind in (PRESS, PRESS_STICK):
+            # PressButton(b, p, q): con Kin(q, b, p), ValidPress(b, p, q); pre HandEmpty.
+            # PressButtonStick(b, o, g, p, q): con Kin(q, o, g, p), ValidStickPress(o, g, p, b); pre
+            # Holding(o, g).  Kin targets T(p) T(g) with p the pose of the pressing object
+            # (fingertip / stick); ValidPress = the object's bottom at the face height (SS) + some sphere of
+            # it over the face (PC); the held stick is also CFreePlace-checked at p except against the
+            # button (CP).  The robot's CF at q ignores the button (it touches it).  DESIGN.md R8.
+            s_ = spec.surfaces[a.surface]
+            scene = {o: p for o, p in pose.items()}
+            c = ("var", a.q1)
+            btn = (s_.support_obb,) if s_.support_obb >= 0 else ()
+            terms.append(Term("JL", conf=c))
+            terms.append(Term("CF", conf=c, scene=scene, excl=(a.obj,), excl_obb=btn))
+            if spec.self_collision:
+                terms.append(Term("SELF", conf=c))
+            terms.append(Term("KP", conf=c, obj=a.obj, grasp=a.grasp, placement=a.placement))
+            terms.append(Term("KR", conf=c, obj=a.obj, grasp=a.grasp, placement=a.placement))
+            terms.append(Term("SS", obj=a.obj, placement=a.placement, surface=a.surface))
+            terms.append(Term("PC", obj=a.obj, placement=a.placement, surface=a.surface))
+            if a.kind == PRESS_STICK:
+                terms.append(Term("CP", obj=a.obj, placement=a.placement, surface=a.surface, scene=scene))
     goal = {o: pose[o] for o in spec.goal_objs}
     return CSP(terms=terms, traj_costs=trajs, goal=goal, offsets=offsets, D=D, grasp_vars=grasp_vars,
                lo=np.array(lo, float), hi=np.array(hi, float), lr=np.array(lr, float))
@@ -376,11 +398,12 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
     grasps = np.zeros((N, len(csp.grasp_vars), 3, 4))
     for gi, vi in enumerate(csp.grasp_vars):
         o = spec.objects[V[vi].obj]
+        o = dataclasses.replace(o, grasp_y=o.grasp_xy if getattr(o, "grasp_y", -1.0) < 0 else o.grasp_y)
         if getattr(o, "grasp_mode", 0) == 1:     # 6-DOF: face, gx, gy, gamma
             u = uniforms(seed, gidx, vi, 4)
             face = np.minimum(np.floor(u[:, 0] * 5), 4).astype(np.int64)
             gx = -o.grasp_xy + 2 * o.grasp_xy * u[:, 1]
-            gy = -o.grasp_xy + 2 * o.grasp_xy * u[:, 2]
+            gy = -o.grasp_y + 2 * o.grasp_y * u[:, 2]
             gamma = -math.pi + 2 * math.pi * u[:, 3]
             T = six_dof_grasp(face, torch.as_tensor(gx), torch.as_tensor(gy),
                               torch.full((N,), o.grasp_z, dtype=DT), torch.as_tensor(gamma))
@@ -388,7 +411,7 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
             continue
         u = uniforms(seed, gidx, vi, 3)
         gx = -o.grasp_xy + 2 * o.grasp_xy * u[:, 0]
-        gy = -o.grasp_xy + 2 * o.grasp_xy * u[:, 1]
+        gy = -o.grasp_y + 2 * o.grasp_y * u[:, 1]
         gamma = -math.pi + 2 * math.pi * u[:, 2]
         T = top_down_grasp(torch.as_tensor(gx), torch.as_tensor(gy), torch.full((N,), o.grasp_z, dtype=DT),
                            torch.as_tensor(gamma))
@@ -403,6 +426,8 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
         elif v.kind == PLACEMENT:
             s = spec.surfaces[v.surface]
             f = spec.objects[v.obj].footprint
+            if any(a.kind in (PRESS, PRESS_STICK) and a.placement == vi for a in spec.actions):
+                f = 0.0     # press pose: uniform on the whole button face (R8)
             u = uniforms(seed, gidx, vi, 3)
             wx = max(s.hi[0] - s.lo[0] - 2 * f, 0.0)
             wy = max(s.hi[1] - s.lo[1] - 2 * f, 0.0)
@@ -419,7 +444,7 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
         bottom = np.zeros((N, 1, 4))
         bottom[..., 3] = 1.0
         for a in spec.actions:
-            if a.kind not in (PICK, PLACE) or V[a.q1].const:
+            if a.kind not in (PICK, PLACE, PRESS, PRESS_STICK) or V[a.q1].const:
                 continue
             pv = V[a.placement]
             pval = np.broadcast_to(np.asarray(pv.value, float), (N, 4)) if pv.const else \
@@ -510,7 +535,8 @@ def evaluate(spec: ProblemSpec, csp: CSP, x: torch.Tensor, grasps: torch.Tensor)
         elif t.kind == "CF":    # CFreeTraj / CFreeHold / CFreeTrajHold
             frames = fk(t.conf)
             w = robot_sphere_centers(rob, frames)
-            j = scene_cost(w, r_rob, t.scene, set(t.excl), spec.obbs)
+            obbs = [b for i, b in enumerate(spec.obbs) if i not in t.excl_obb]
+            j = scene_cost(w, r_rob, t.scene, set(t.excl), obbs)
             if t.held is not None:
                 o, gv = t.held
                 T_obj = frames[:, 8] @ inverse(G[:, gslot[gv]])
@@ -539,6 +565,15 @@ def evaluate(spec: ProblemSpec, csp: CSP, x: torch.Tensor, grasps: torch.Tensor)
             lower = _t(s.lo)[None, :] + r[:, None]
             upper = _t(s.hi)[None, :] - r[:, None]
             Jc.append(dist_from_bounds(loc, lower, upper).sum(-1))
+        elif t.kind == "PC":   # ValidPress / ValidStickPress contact (R8): the sphere of the
+            # pressing object closest to the button face region, dist_from_bounds on the unshrunk face
+            s = spec.surfaces[t.surface]
+            w, r = obj_spheres(t.obj, placement_T(t.placement))
+            c, sn = math.cos(s.frame[3]), math.sin(s.frame[3])
+            dx, dy = w[..., 0] - s.frame[0], w[..., 1] - s.frame[1]
+            loc = torch.stack([c * dx + sn * dy, -sn * dx + c * dy], -1)
+            e = dist_from_bounds(loc, _t(s.lo), _t(s.hi))                 # [N, m]
+            Jc.append(e.min(-1).values)
         elif t.kind == "CP":   # CFreePlace(o, p): support excluded (L3)
             s = spec.surfaces[t.surface]
             w, r = obj_spheres(t.obj, placement_T(t.placement))

@@ -818,7 +818,8 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
             const float pz = xs[I.xoff + 2];
             Wrench own;
             own.zero();
-            // support: |z_bottom - z_top|  (L6; object frame origin at its bottom, L15)
+            // support: |z_bottom - z_top|  (L6; object frame origin at its bottom, L15); for a press the
+            // pressing object's bottom at the button-face height (R8)
             {
                 const float e = fabsf(pz - Sf.frame[2]);
                 finish_term<MODE>(P, A, sink, Q.term_ss, e, gl, active, p, s_counts);
@@ -839,7 +840,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                 gq[u][0] = gq[u][1] = gq[u][2] = 0.f;
             }
             // containment: sum over spheres of dist_from_bounds(xy in surface frame, lo + r, hi - r)
-            {
+            if (Q.term_sc >= 0) {
                 float sy, cy;
                 fsincos(Sf.frame[3], &sy, &cy);
                 float e = 0.f;
@@ -864,8 +865,48 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                 }
                 finish_term<MODE>(P, A, sink, Q.term_sc, gsum<GS>(e), gl, active, p, s_counts);
             }
+            // press contact (ValidPress / ValidStickPress, R8): min over the object's spheres of
+            // dist_from_bounds(xy in the face frame, lo, hi); the subgradient goes to the arg-min sphere
+            // (lowest index on ties)
+            if (Q.term_pc >= 0) {
+                float sy, cy;
+                fsincos(Sf.frame[3], &sy, &cy);
+                float emin = kFar, glx_min = 0.f, gly_min = 0.f;
+                int kmin = TAMP_MAX_OBJ_SPHERES;
+#pragma unroll
+                for (int u = 0; u < NSO; ++u) {
+                    if (gl + GS * u >= no) continue;
+                    const float rx = wq[u][0] - Sf.frame[0], ry = wq[u][1] - Sf.frame[1];
+                    const float lx = fmaf(cy, rx, sy * ry), ly = fmaf(-sy, rx, cy * ry);
+                    const float ex = fmaxf(fmaxf(Sf.lo[0] - lx, lx - Sf.hi[0]), 0.f);
+                    const float ey = fmaxf(fmaxf(Sf.lo[1] - ly, ly - Sf.hi[1]), 0.f);
+                    const float eu = sqrtf(fmaf(ex, ex, ey * ey));
+                    if (eu < emin) {
+                        emin = eu;
+                        kmin = gl + GS * u;
+                        glx_min = eu > 0.f ? (lx > Sf.hi[0] ? ex : (lx < Sf.lo[0] ? -ex : 0.f)) / eu : 0.f;
+                        gly_min = eu > 0.f ? (ly > Sf.hi[1] ? ey : (ly < Sf.lo[1] ? -ey : 0.f)) / eu : 0.f;
+                    }
+                }
+#pragma unroll
+                for (int o = GS / 2; o > 0; o >>= 1) {
+                    const float e2 = __shfl_xor_sync(FULL, emin, o, GS);
+                    const int k2 = __shfl_xor_sync(FULL, kmin, o, GS);
+                    if (e2 < emin || (e2 == emin && k2 < kmin)) { emin = e2; kmin = k2; }
+                }
+                finish_term<MODE>(P, A, sink, Q.term_pc, emin, gl, active, p, s_counts);
+                if (GRAD && emin > 0.f) {
+                    const float lam = P.term_lam[Q.term_pc];
+#pragma unroll
+                    for (int u = 0; u < NSO; ++u)
+                        if (gl + GS * u == kmin) {
+                            gq[u][0] += lam * fmaf(cy, glx_min, -sy * gly_min);
+                            gq[u][1] += lam * fmaf(sy, glx_min, cy * gly_min);
+                        }
+                }
+            }
             // CFreePlace: placed-object spheres vs OBBs (support excluded) and other objects
-            {
+            if (Q.term_cp >= 0) {
                 const float lam_cp = P.term_lam[Q.term_cp];
                 float rqe[NSO];
 #pragma unroll

@@ -147,6 +147,7 @@ static void count_pairs(const tamp_problem_desc& d, Compiled& C) {
     }
     for (int q = 0; q < P.n_place; ++q) {
         const KPlace& Q = P.place[q];
+        if (Q.term_cp < 0) continue;
         int part_sph = 0;
         for (int i = 0; i < Q.part_count; ++i) part_sph += P.osph_n[P.inst[P.partners[Q.part_begin + i]].obj];
         const int no = P.osph_n[P.inst[Q.inst].obj];
@@ -340,11 +341,11 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         inst_of[v] = n_inst++;
     }
     P.n_inst = n_inst;
-    for (int o = 0; o < d.n_objects; ++o)
-        REQUIRE(init_inst[o] >= 0, TAMP_E_INVALID, "every object needs a constant initial placement variable");
 
-    // symbolic simulation along the skeleton
-    std::vector<int> pose(init_inst);     // object -> instance, -1 = held
+    // symbolic simulation along the skeleton.  An object without a constant initial placement is virtual
+    // (the PressButton fingertip): never in the scene.
+    std::vector<int> pose(d.n_objects);   // object -> instance, -1 = held, -2 = virtual (absent)
+    for (int o = 0; o < d.n_objects; ++o) pose[o] = init_inst[o] >= 0 ? init_inst[o] : -2;
     int held = -1;
     int n_terms = 0, n_fk = 0, n_place = 0, n_traj = 0, n_part = 0;
     auto add_term = [&](int kind) -> int16_t {
@@ -408,6 +409,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
                     d.var[a.placement].obj == a.obj, TAMP_E_INVALID, "pick/place placement must belong to the object");
             if (a.kind == TAMP_PICK) {
                 REQUIRE(held < 0, TAMP_E_INVALID, "Pick: hand not empty");
+                REQUIRE(pose[a.obj] != -2, TAMP_E_INVALID, "Pick: virtual object (no initial placement)");
                 REQUIRE(pose[a.obj] == inst_of[a.placement], TAMP_E_INVALID, "Pick: object is not at that placement");
             } else {
                 REQUIRE(held == a.obj, TAMP_E_INVALID, "Place: object not held");
@@ -439,6 +441,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
                 Q.term_ss = add_term(TAMP_TERM_SS);
                 Q.term_sc = add_term(TAMP_TERM_SC);
                 Q.term_cp = add_term(TAMP_TERM_CP);
+                Q.term_pc = -1;
                 Q.surface = (int16_t)a.surface;
                 Q.obb_mask = (uint16_t)(all_obb & ~(S.support_obb >= 0 ? (1u << S.support_obb) : 0u));
                 REQUIRE(add_partners(a.obj, S.support_obj, Q.part_begin, Q.part_count), TAMP_E_UNSUPPORTED,
@@ -449,6 +452,51 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
                 pose[a.obj] = inst_of[a.placement];
                 held = -1;
             }
+        } else if (a.kind == TAMP_PRESS || a.kind == TAMP_PRESS_STICK) {
+            // PressButton(b, p, q) / PressButtonStick(b, o, g, p, q) (R8):
+            // JL(q), CF(q) [button excluded; held stick covered by CP], [SELF], KP(q), KR(q) vs T(p) T(g),
+            // SS(p) + PC(p) on the button face, and for the stick CP(p) [button excluded].
+            REQUIRE(a.obj >= 0 && a.obj < d.n_objects, TAMP_E_INVALID, "press object out of range");
+            REQUIRE(conf_ok(a.q1) && !d.var[a.q1].is_const, TAMP_E_UNSUPPORTED, "press conf must be a free conf");
+            REQUIRE(a.grasp >= 0 && a.grasp < d.n_vars && gslot[a.grasp] >= 0 && d.var[a.grasp].obj == a.obj,
+                    TAMP_E_INVALID, "press grasp must be a grasp variable of the pressing object");
+            REQUIRE(a.placement >= 0 && a.placement < d.n_vars && inst_of[a.placement] >= 0 &&
+                    d.var[a.placement].obj == a.obj && !d.var[a.placement].is_const, TAMP_E_INVALID,
+                    "press pose must be a free placement variable of the pressing object");
+            REQUIRE(a.surface >= 0 && a.surface < d.n_surfaces, TAMP_E_INVALID, "press: button face out of range");
+            if (a.kind == TAMP_PRESS) {
+                REQUIRE(held < 0, TAMP_E_INVALID, "PressButton: hand not empty");
+                REQUIRE(pose[a.obj] == -2, TAMP_E_INVALID, "PressButton: object must be virtual (the fingertip)");
+            } else {
+                REQUIRE(held == a.obj, TAMP_E_INVALID, "PressButtonStick: stick not held");
+            }
+            const tamp_surface_desc& S = d.surface[a.surface];
+            const uint16_t no_button = (uint16_t)(all_obb & ~(S.support_obb >= 0 ? (1u << S.support_obb) : 0u));
+            REQUIRE(n_fk < TAMP_MAX_FK, TAMP_E_UNSUPPORTED, "too many robot configurations (TAMP_MAX_FK)");
+            KFk& F = P.fk[n_fk++];
+            F.xoff = (int16_t)xoff[a.q1];
+            F.term_jl = add_term(TAMP_TERM_JL);
+            F.term_cf = add_term(TAMP_TERM_CF);
+            F.term_self = d.self_collision ? add_term(TAMP_TERM_SELF) : (int16_t)-1;
+            F.term_kp = add_term(TAMP_TERM_KP);
+            F.term_kr = add_term(TAMP_TERM_KR);
+            F.kin_inst = (int16_t)inst_of[a.placement];
+            F.kin_grasp = (int16_t)gslot[a.grasp];
+            F.held_grasp = F.held_obj = -1;
+            F.obb_mask = no_button;
+            F.ghost = 0;
+            REQUIRE(add_partners(a.obj, -1, F.part_begin, F.part_count), TAMP_E_UNSUPPORTED, "too many partners");
+            REQUIRE(n_place < kMaxPlace, TAMP_E_UNSUPPORTED, "too many Place / press actions");
+            KPlace& Q = P.place[n_place++];
+            Q.inst = (int16_t)inst_of[a.placement];
+            Q.term_ss = add_term(TAMP_TERM_SS);
+            Q.term_sc = -1;
+            Q.term_pc = add_term(TAMP_TERM_PC);
+            Q.term_cp = a.kind == TAMP_PRESS_STICK ? add_term(TAMP_TERM_CP) : (int16_t)-1;
+            Q.surface = (int16_t)a.surface;
+            Q.obb_mask = no_button;
+            REQUIRE(add_partners(a.obj, S.support_obj, Q.part_begin, Q.part_count), TAMP_E_UNSUPPORTED,
+                    "too many partners");
         } else {
             return fail(TAMP_E_INVALID, "bad action kind");
         }
@@ -519,11 +567,17 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             S.a[0] = d.object[V.obj].grasp_xy;
             S.a[1] = d.object[V.obj].grasp_z;
             S.a[2] = d.object[V.obj].grasp_mode == 1 ? 1.f : 0.f;
+            S.a[3] = d.object[V.obj].grasp_y < 0.f ? d.object[V.obj].grasp_xy : d.object[V.obj].grasp_y;
         } else if (V.kind == TAMP_VAR_PLACEMENT) {
             const tamp_surface_desc& Sf = d.surface[V.surface];
             S.kind = KS_PLACEMENT;
             S.a[0] = Sf.lo[0]; S.a[1] = Sf.lo[1]; S.a[2] = Sf.hi[0]; S.a[3] = Sf.hi[1];
-            S.a[4] = d.object[V.obj].footprint;
+            // a press pose is sampled on the whole button face (R8): contact needs only some point over it
+            bool press = false;
+            for (int ai = 0; ai < d.n_actions; ++ai)
+                press |= (d.action[ai].kind == TAMP_PRESS || d.action[ai].kind == TAMP_PRESS_STICK) &&
+                         d.action[ai].placement == v;
+            S.a[4] = press ? 0.f : d.object[V.obj].footprint;
             S.a[5] = Sf.frame[0]; S.a[6] = Sf.frame[1]; S.a[7] = Sf.frame[2]; S.a[8] = Sf.frame[3];
         } else if (V.kind == TAMP_VAR_CONF) {
             S.kind = KS_CONF;

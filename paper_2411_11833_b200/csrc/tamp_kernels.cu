@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
             const int face = six ? min((int)floorf(u[0] * 5.f), 4) : 0;
             const float* uu = six ? u + 1 : u;          // 6-DOF: u0 picks the face
             const float gx = -gxy + 2.f * gxy * uu[0];
-            const float gy = -gxy + 2.f * gxy * uu[1];
+            const float gy = -V.a[3] + 2.f * V.a[3] * uu[1];
             const float gamma = -kPi + 2.f * kPi * uu[2];
             float s, c;
             sincosf(gamma, &s, &c);

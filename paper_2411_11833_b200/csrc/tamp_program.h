@@ -40,10 +40,11 @@ struct KInst {
     float pose[4];                    // x y z yaw (constant instances)
 };
 
-// StablePlace + CFreePlace of one Place action.
+// StablePlace + CFreePlace of one Place action, or ValidPress / ValidStickPress (+ CFreePlace of the held
+// stick) of one PressButton / PressButtonStick action: SS always, SC (Place) or PC (press), CP unless -1.
 struct KPlace {
-    int16_t inst;                     // instance of the placed object at its placement variable
-    int16_t term_ss, term_sc, term_cp;
+    int16_t inst;                     // instance of the placed / pressing object at its placement variable
+    int16_t term_ss, term_sc, term_cp, term_pc;
     int16_t surface;
     int16_t part_begin, part_count;
     uint16_t obb_mask;                // OBBs checked (support excluded)

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtamp.so")
 
 # ---- limits / enums (include/tamp.h) ----
-ABI_VERSION = 1
+ABI_VERSION = 2
 NJ = 7
 MAX_ROBOT_SPHERES = 32
 MAX_OBB = 16
@@ -29,8 +29,8 @@ MAX_VARS = 96
 MAX_ACTIONS = 64
 MAX_GOAL = 8
 MAX_TERMS = 256
-N_TERM_KINDS = 8
-TERM_NAMES = ("JL", "CF", "KP", "KR", "SS", "SC", "CP", "SELF")
+N_TERM_KINDS = 9
+TERM_NAMES = ("JL", "CF", "KP", "KR", "SS", "SC", "CP", "SELF", "PC")
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_CUDA", 3: "E_NOMEM", 4: "E_STATE", 5: "E_UNSUPPORTED"}
 
 F = ctypes.c_float
@@ -51,7 +51,7 @@ class ObbDesc(ctypes.Structure):
 
 class ObjectDesc(ctypes.Structure):
     _fields_ = [("n_spheres", I32), ("sphere", F * 4 * MAX_OBJ_SPHERES), ("footprint", F), ("grasp_xy", F),
-                ("grasp_z", F), ("grasp_mode", I32)]
+                ("grasp_z", F), ("grasp_mode", I32), ("grasp_y", F)]
 
 
 class SurfaceDesc(ctypes.Structure):
@@ -188,6 +188,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
         d.object[i].grasp_xy = float(o.grasp_xy)
         d.object[i].grasp_z = float(o.grasp_z)
         d.object[i].grasp_mode = int(getattr(o, "grasp_mode", 0))
+        d.object[i].grasp_y = float(getattr(o, "grasp_y", -1.0))
     d.n_surfaces = len(spec.surfaces)
     for i, s in enumerate(spec.surfaces):
         for k in range(4):

@@ -31,7 +31,7 @@ def _ctx(spec, n, x32, g32, gofs=0, n_global=None, lanes=0):
 
 # ---------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("grasp_mode", [0, 1])
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6])
 def test_sampler_matches_oracle(cfg, grasp_mode):
     """K1 (Philox + samplers) vs the oracle's InitializeParticles; ragged N, nonzero global offset;
     top-down (0) and 6-DOF (1) grasp samplers."""
@@ -52,7 +52,7 @@ def test_sampler_matches_oracle(cfg, grasp_mode):
 
 
 @pytest.mark.parametrize("lanes", [4, 8, 16])
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
 def test_cost_and_gradient_match_oracle(cfg, lanes):
     n = 97 if cfg != 4 else 40
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=10 + cfg)
@@ -72,7 +72,7 @@ def test_cost_and_gradient_match_oracle(cfg, lanes):
 
 
 @pytest.mark.parametrize("lanes", [4, 8, 16])
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6])
 def test_one_adam_step_matches_oracle(cfg, lanes):
     n = 97 if cfg != 4 else 40
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=20 + cfg)
@@ -96,7 +96,7 @@ def test_one_adam_step_matches_oracle(cfg, lanes):
 
 
 @pytest.mark.parametrize("lanes", [4, 8, 16])
-@pytest.mark.parametrize("cfg", [1, 2, 3])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 6])
 def test_check_counts_and_classes_match_oracle(cfg, lanes):
     n = 301
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=30 + cfg)

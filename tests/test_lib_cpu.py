@@ -45,7 +45,7 @@ def _query(lib, desc, n):
     return st, nb.value, lib.tamp_last_error().decode()
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
 def test_compiler_accepts_configs(lib, cfg):
     spec = make_config(cfg, n=16)
     st, nb, msg = _query(lib, T.build_desc(spec), 1000)
@@ -77,6 +77,32 @@ def test_compiler_rejects_bad_descriptors(lib):
     d.robot.n_spheres = 33
     assert _query(lib, d, 10)[0] == 5
     assert _query(lib, T.build_desc(spec), 0)[0] == 1
+
+
+def test_compiler_rejects_bad_press_actions(lib):
+    """PressButton needs an empty hand and the virtual fingertip; PressButtonStick needs the stick held;
+    Pick of a virtual object is rejected (P:1055-1063 preconditions)."""
+    spec = make_config(6, n=4)
+    assert _query(lib, T.build_desc(spec), 10)[0] == 0
+    d = T.build_desc(spec)
+    d.action[1].obj = 0                                 # PressButton with the stick (not virtual)
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "grasp" in msg or "virtual" in msg
+    d = T.build_desc(spec)
+    d.action[5].kind = 4                                # PressButton while holding the stick
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "hand not empty" in msg
+    d = T.build_desc(spec)
+    d.action[4].kind = 0                                # no MoveHold: fine; drop the Pick -> stick not held
+    d.action[3].kind = 0
+    d.action[3].q2 = d.action[3].q1
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "not held" in msg
+    d = T.build_desc(spec)
+    d.action[3].obj = 1                                 # Pick the virtual fingertip
+    d.action[3].grasp = 2
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1
 
 
 def test_product_path_fails_loudly_without_library(tmp_path):

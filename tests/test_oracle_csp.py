@@ -1,5 +1,6 @@
 """Oracle pins: skeleton -> CSP, Eq. 2/3/4, Adam, samplers, best-k (CPU only)."""
 import copy
+import dataclasses
 import math
 
 import numpy as np
@@ -8,7 +9,7 @@ import torch
 
 from oracle import tamp_oracle as O
 from workloads import make_config
-from workloads.scenes import Surface, PLACEMENT, CONF
+from workloads.scenes import Surface, PLACEMENT, CONF, PRESS, PRESS_STICK
 
 DT = torch.float64
 
@@ -41,7 +42,8 @@ def test_running_example_constraint_set():
 
 
 @pytest.mark.parametrize("cfg,D,n_hard,n_grasp", [(1, 18, 11, 1), (2, 54, 33, 3), (3, 72, 44, 4),
-                                                  (4, 360, 138, 6), (5, 72, 44, 4)])
+                                                  (4, 360, 138, 6), (5, 72, 44, 4), (6, 29, 17, 2),
+                                                  (7, 22, 12, 1)])
 def test_config_sizes(cfg, D, n_hard, n_grasp):
     """D, hard terms (config 4: 66 + 72 knot terms), frozen grasps."""
     spec = make_config(cfg, n=4)
@@ -216,7 +218,7 @@ def test_permutation_and_batch_split_invariance():
     np.testing.assert_array_equal(gr2, gr[2:3])
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, "1s"])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6, "1s"])
 def test_gradient_vs_central_fd(cfg):
     """Autograd gradient of Eq. 2 against central finite differences, excluding
     coordinates whose FD is unstable between h and h/10 (kink neighbourhoods, "1e-4-wide").
@@ -312,7 +314,7 @@ def test_invalid_particles_are_sticky_and_not_updated():
 # ---------------------------------------------------------------------------------------------
 # samplers
 # ---------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("cfg", [1, 2, 4])
+@pytest.mark.parametrize("cfg", [1, 2, 4, 6])
 def test_samplers(cfg):
     spec = make_config(cfg, n=512)
     csp = O.build_csp(spec)
@@ -326,6 +328,8 @@ def test_samplers(cfg):
         if v.kind == PLACEMENT and not v.const:
             s = spec.surfaces[v.surface]
             o = spec.objects[v.obj]
+            if any(a.kind in (PRESS, PRESS_STICK) and a.placement == vi for a in spec.actions):
+                o = dataclasses.replace(o, footprint=0.0)          # press poses: whole button face (R8)
             p = x[:, csp.offsets[vi]:csp.offsets[vi] + 4]
             assert np.all(p[:, 2] == s.frame[2])
             c, sn = math.cos(s.frame[3]), math.sin(s.frame[3])
@@ -489,3 +493,103 @@ def test_six_dof_grasp_sampler():
     assert ((h - 400.0) ** 2 / 400.0).sum() < 18.5          # chi^2, 4 dof, p = 0.001
     side = face > 0
     np.testing.assert_allclose(g[side, 0, :2, 3], 0.0, atol=1e-15)
+
+
+# ---------------------------------------------------------------------------------------------
+# Stick Button: PressButton / PressButtonStick (R8)
+# ---------------------------------------------------------------------------------------------
+def test_press_skeleton_terms():
+    """PressButton: Kin + ValidPress, hand empty; PressButtonStick: Kin + ValidStickPress with the stick held
+    (P:1055-1063).  The robot's CF at a press conf ignores the pressed button; the virtual fingertip is never
+    in a scene; the held stick is checked by CP at its press pose, not by CF."""
+    spec = make_config(6, n=2)
+    csp = O.build_csp(spec)
+    kinds = [t.kind for t in csp.terms]
+    assert kinds == ["JL", "CF", "KP", "KR", "SS", "PC",              # PressButton(red)
+                     "JL", "CF", "KP", "KR",                          # Pick(stick)
+                     "JL", "CF", "KP", "KR", "SS", "PC", "CP"]        # PressButtonStick(blue)
+    red, blue = spec.surfaces[0].support_obb, spec.surfaces[1].support_obb
+    assert csp.terms[1].excl_obb == (red,) and csp.terms[11].excl_obb == (blue,)
+    assert csp.terms[7].excl_obb == ()
+    for t in csp.terms:
+        if t.scene is not None:
+            assert 1 not in t.scene                       # fingertip: virtual
+    assert 0 in csp.terms[1].scene                        # stick on the table while pressing red
+    assert 0 not in csp.terms[11].scene and 0 not in csp.terms[16].scene   # stick held
+    assert csp.terms[16].surface == 1 and csp.terms[15].obj == 0
+    kinds7 = [t.kind for t in O.build_csp(make_config(7, n=2)).terms]
+    assert kinds7 == ["JL", "CF", "KP", "KR", "SS", "PC"] * 2
+
+
+def _rect_dist(px, py, lo, hi):
+    """Euclidean distance from a point to an axis-aligned rectangle (projection by clipping)."""
+    cx, cy = np.clip(px, lo[0], hi[0]), np.clip(py, lo[1], hi[1])
+    return math.hypot(px - cx, py - cy)
+
+
+def test_press_contact_closed_form():
+    """PC = min over the pressing object's spheres of the distance from the sphere centre's xy to the button
+    face (projection by clipping), SS = |z_bottom - z_top|; random fingertip and stick press poses."""
+    spec = make_config(6, n=1)
+    csp = O.build_csp(spec)
+    rng = np.random.default_rng(3)
+    x0, g = O.initialize_particles(spec, csp, 1, np.arange(1))
+    off_r = csp.offsets[[i for i, v in enumerate(spec.variables) if v.name == "press_red"][0]]
+    off_b = csp.offsets[[i for i, v in enumerate(spec.variables) if v.name == "press_blue_stick"][0]]
+    sr, sb = spec.surfaces[0], spec.surfaces[1]
+    for _ in range(20):
+        x = x0.copy()
+        pr = np.array([sr.frame[0] + rng.uniform(-0.06, 0.06), sr.frame[1] + rng.uniform(-0.06, 0.06),
+                       sr.frame[2] + rng.uniform(-0.01, 0.01), rng.uniform(-4, 4)])
+        pb = np.array([sb.frame[0] + rng.uniform(-0.3, 0.3), sb.frame[1] + rng.uniform(-0.3, 0.3),
+                       sb.frame[2] + rng.uniform(-0.01, 0.01), rng.uniform(-4, 4)])
+        x[0, off_r:off_r + 4] = pr
+        x[0, off_b:off_b + 4] = pb
+        _, Jc, _ = _eval(spec, csp, x, g)
+        # fingertip: one sphere on the frame's z axis
+        assert Jc[0, 4] == pytest.approx(abs(pr[2] - sr.frame[2]), abs=1e-15)
+        assert Jc[0, 5] == pytest.approx(_rect_dist(pr[0] - sr.frame[0], pr[1] - sr.frame[1], sr.lo, sr.hi),
+                                         rel=1e-12, abs=1e-15)
+        st = spec.objects[0]
+        c, sn = math.cos(pb[3]), math.sin(pb[3])
+        d = min(_rect_dist(pb[0] + c * sp[0] - sn * sp[1] - sb.frame[0], pb[1] + sn * sp[0] + c * sp[1] - sb.frame[1],
+                           sb.lo, sb.hi) for sp in st.spheres)
+        assert Jc[0, 14] == pytest.approx(abs(pb[2] - sb.frame[2]), abs=1e-15)
+        assert Jc[0, 15] == pytest.approx(d, rel=1e-12, abs=1e-15)
+
+
+def test_constructed_press_particle_satisfies_press_terms():
+    """Fingertip press pose inside the red face at its height; conf by IK onto T(p) T(g): SS, PC
+    exactly 0 and the Kin residuals at IK precision, so ValidPress and Kin hold (Eq. 3)."""
+    spec = make_config(6, n=4)
+    csp = O.build_csp(spec)
+    x, g = O.initialize_particles(spec, csp, 9, np.arange(4))
+    vi = [i for i, v in enumerate(spec.variables) if v.name == "press_red"][0]
+    qi = [i for i, v in enumerate(spec.variables) if v.name == "q_press_red"][0]
+    s = spec.surfaces[0]
+    rng = np.random.default_rng(0)
+    p = np.stack([s.frame[0] + rng.uniform(-0.015, 0.015, 4), s.frame[1] + rng.uniform(-0.015, 0.015, 4),
+                  np.full(4, s.frame[2]), rng.uniform(-3, 3, 4)], 1)
+    x[:, csp.offsets[vi]:csp.offsets[vi] + 4] = p
+    Tg = np.concatenate([g[:, 0], np.tile([[[0, 0, 0, 1.0]]], (4, 1, 1))], 1)
+    Tt = (O.pose_xyzyaw(torch.as_tensor(p)) @ torch.as_tensor(Tg)).numpy()
+    q0 = np.tile(make_config(1).variables[0].value, (4, 1))
+    x[:, csp.offsets[qi]:csp.offsets[qi] + 7] = O.ik_dls(spec.robot, q0, Tt, 200, 0.05)
+    _, Jc, _ = _eval(spec, csp, x, g)
+    assert np.all(Jc[:, 4] == 0.0) and np.all(Jc[:, 5] == 0.0)
+    assert np.all(Jc[:, 2] <= 1e-6) and np.all(Jc[:, 3] <= 1e-6)
+    tol = np.array([spec.eps[k] for k in ("KP", "KR", "SS", "PC")])
+    assert np.all(Jc[:, 2:6] <= tol)
+
+
+def test_stick_grasp_range():
+    """Top-down stick grasps: TCP anywhere along the stick (|gx| <= grasp_xy) and on its axis (|gy| <= grasp_y)."""
+    spec = make_config(6, n=1000)
+    csp = O.build_csp(spec)
+    _, g = O.initialize_particles(spec, csp, 4, np.arange(1000))
+    st = spec.objects[0]
+    k = csp.grasp_vars.index([i for i, v in enumerate(spec.variables) if v.name == "g_stick"][0])
+    assert np.all(np.abs(g[:, k, 0, 3]) <= st.grasp_xy) and np.abs(g[:, k, 0, 3]).max() > 0.9 * st.grasp_xy
+    assert np.all(np.abs(g[:, k, 1, 3]) <= st.grasp_y) and np.abs(g[:, k, 1, 3]).max() > 0.9 * st.grasp_y
+    kf = csp.grasp_vars.index([i for i, v in enumerate(spec.variables) if v.name == "g_fingertip"][0])
+    np.testing.assert_array_equal(g[:, kf, :, 3], 0.0)

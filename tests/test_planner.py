@@ -74,3 +74,26 @@ def test_algorithm1_loop_gpu():
     assert res is not None and res.skeleton == 1 and res.pops == 1
     cls, cost, gidx, x = planner.decode_records(res.records)
     assert cls[0] == 0
+
+
+@pytest.mark.gpu
+def test_stick_button_skeletons_gpu():
+    """Stick Button: pressing the out-of-reach blue button with the fingertip never
+    satisfies its Kin constraint (zero count -> Eq. 5 penalty), the stick skeleton is solved; Algorithm 1
+    therefore refines the stick skeleton first and returns its satisfying particles."""
+    torch.cuda.set_device(0)
+    n = 4096
+    direct, stick = make_config(7, n=n), make_config(6, n=n)
+    for s in (direct, stick):
+        s.ik_iters = 20
+    ctx = planner.TampContext(direct, n)
+    ctx.sample(seed=1)
+    ctx.optimize(300)
+    counts, _ = ctx.check()
+    kp_blue = [i for i, k in enumerate(ctx.term_kinds) if k == "KP"][1]
+    assert int(counts[kp_blue]) == 0 and int(counts[-2]) == 0
+    res = planner.cutamp([direct, stick], n, seed=5, steps_per_pop=300, max_pops=4, k=4)
+    assert res is not None and res.skeleton == 1 and res.pops == 1
+    assert res.heuristics[1] > res.heuristics[0]
+    cls, cost, gidx, x = planner.decode_records(res.records)
+    assert cls[0] == 0

@@ -19,8 +19,8 @@ import numpy as np
 
 # variable kinds (P:1006-1014 types conf/traj/grasp/placement)
 CONF, PLACEMENT, GRASP, TRAJ = 0, 1, 2, 3
-# action kinds (Listing 1)
-MOVE_FREE, PICK, MOVE_HOLD, PLACE = 0, 1, 2, 3
+# action kinds (Listing 1; PressButton / PressButtonStick of the Stick Button domain)
+MOVE_FREE, PICK, MOVE_HOLD, PLACE, PRESS, PRESS_STICK = 0, 1, 2, 3, 4, 5
 
 INF = float("inf")
 
@@ -65,6 +65,7 @@ class Obj:
     grasp_xy: float           # top-down grasp sampler: TCP xy uniform in [-grasp_xy, grasp_xy]^2 (object frame)
     grasp_z: float            # TCP height above the object bottom
     grasp_mode: int = 0       # 0: top-down 4-DOF grasps; 1: 6-DOF grasps (top or one of the four sides)
+    grasp_y: float = -1.0     # top-down grasp TCP y range (< 0: same as grasp_xy); e.g. along a stick
 
 
 @dataclasses.dataclass
@@ -142,8 +143,8 @@ class ProblemSpec:
     ik_damping: float = 0.1
 
 
-DEFAULT_LAM = dict(JL=1.0, CF=1.0, KP=1.0, KR=5.0, SS=2.0, SC=2.0, CP=1.0, SELF=1.0)
-DEFAULT_EPS = dict(JL=0.0, CF=1e-3, KP=5e-3, KR=0.05, SS=1e-2, SC=1e-3, CP=1e-3, SELF=0.0)
+DEFAULT_LAM = dict(JL=1.0, CF=1.0, KP=1.0, KR=5.0, SS=2.0, SC=2.0, CP=1.0, SELF=1.0, PC=1.0)
+DEFAULT_EPS = dict(JL=0.0, CF=1e-3, KP=5e-3, KR=0.05, SS=1e-2, SC=1e-3, CP=1e-3, SELF=0.0, PC=1e-3)
 
 
 def _line_spheres(p0, p1, r, n=4):
@@ -351,8 +352,70 @@ def config_tetris6_knots(n=131072, steps=100):
     return _tetris(6, ["I", "L", "O", "J", "I", "I"], (6, 4), n, steps, False, 3, "tetris6_knots")
 
 
-CONFIG_NAMES = {1: "pickplace", 2: "obstruction", 3: "tetris4_goal", 4: "tetris6_knots", 5: "tetris4"}
-CONFIG_SIZES = {1: 256, 2: 8192, 3: 32768, 4: 131072, 5: 1 << 20}
+def _button(name, x, y):
+    """4x4x2 cm button on the table: an OBB plus its top face as a press surface (support = the button)."""
+    return OBB(np.array([x, y, 0.01]), 0.0, np.array([0.02, 0.02, 0.01]), name)
+
+
+def fingertip():
+    """Virtual object of PressButton: the point of the closed gripper that touches the button.
+    One 5 mm sphere on its frame origin (its bottom, L15); the TCP sits on that point, approach down
+    (top-down grasp with no offset).  It has no constant initial placement, so it is never in the scene."""
+    return Obj(name="fingertip", spheres=np.array([[0.0, 0.0, 0.005, 0.005]]), init_pose=np.zeros(4),
+               footprint=0.005, grasp_xy=0.0, grasp_z=0.0)
+
+
+def stick(name, length, pose):
+    """Stick tool: 8 spheres of 1.5 cm along its x axis; top-down grasps anywhere along it."""
+    r = 0.015
+    xs = np.linspace(-length / 2 + r, length / 2 - r, 8)
+    return Obj(name=name, spheres=np.array([[x, 0.0, r, r] for x in xs]), init_pose=np.array(pose, float),
+               footprint=length / 2, grasp_xy=length / 2 - 0.03, grasp_y=0.003, grasp_z=0.02)
+
+
+def config_stickbutton(n=4096, steps=100, direct_blue=False):
+    """Stick Button (Fig. 12): press the red button directly, then pick the stick and press the
+    blue button with it; the blue button sits beyond the arm's reach at the end of a walled corridor.
+    direct_blue=True gives the infeasible skeleton that presses blue with the fingertip."""
+    red_xy, blue_xy = (0.45, -0.25), (1.02, 0.20)
+    wall_h = 0.08
+    obbs = [TABLE, _button("btn_red", *red_xy), _button("btn_blue", *blue_xy),
+            OBB(np.array([blue_xy[0] - 0.05, blue_xy[1] + 0.06, wall_h / 2]), 0.0, np.array([0.12, 0.01, wall_h / 2]), "wall_n"),
+            OBB(np.array([blue_xy[0] - 0.05, blue_xy[1] - 0.06, wall_h / 2]), 0.0, np.array([0.12, 0.01, wall_h / 2]), "wall_s")]
+    objs = [stick("stick", 0.40, [0.40, 0.15, 0.0, 0.0]), fingertip()]
+    surfs = [Surface("red_top", np.array([red_xy[0], red_xy[1], 0.02, 0.0]), np.array([-0.02, -0.02]),
+                     np.array([0.02, 0.02]), support_obb=1),
+             Surface("blue_top", np.array([blue_xy[0], blue_xy[1], 0.02, 0.0]), np.array([-0.02, -0.02]),
+                     np.array([0.02, 0.02]), support_obb=2)]
+    lo, hi = _table_bounds()
+    b = _Builder()
+    q0 = b.var(Var(CONF, "q0", const=True, value=Q_HOME.copy()))
+    p0 = b.var(Var(PLACEMENT, "p0_stick", const=True, value=objs[0].init_pose.copy(), obj=0))
+    gf = b.var(Var(GRASP, "g_fingertip", obj=1))
+    pr = b.var(Var(PLACEMENT, "press_red", obj=1, surface=0, lo=lo, hi=hi))
+    qr = b.var(Var(CONF, "q_press_red"))
+    b.actions.append(Action(MOVE_FREE, q1=q0, q2=qr))
+    b.actions.append(Action(PRESS, obj=1, grasp=gf, placement=pr, surface=0, q1=qr))
+    if direct_blue:
+        pb = b.var(Var(PLACEMENT, "press_blue", obj=1, surface=1, lo=lo, hi=hi))
+        qb = b.var(Var(CONF, "q_press_blue"))
+        b.actions.append(Action(MOVE_FREE, q1=qr, q2=qb))
+        b.actions.append(Action(PRESS, obj=1, grasp=gf, placement=pb, surface=1, q1=qb))
+    else:
+        g = b.var(Var(GRASP, "g_stick", obj=0))
+        qp = b.var(Var(CONF, "q_pick_stick"))
+        pb = b.var(Var(PLACEMENT, "press_blue_stick", obj=0, surface=1, lo=lo, hi=hi))
+        qb = b.var(Var(CONF, "q_press_blue"))
+        b.actions.append(Action(MOVE_FREE, q1=qr, q2=qp))
+        b.actions.append(Action(PICK, obj=0, grasp=g, placement=p0, q1=qp))
+        b.actions.append(Action(MOVE_HOLD, obj=0, grasp=g, q1=qp, q2=qb))
+        b.actions.append(Action(PRESS_STICK, obj=0, grasp=g, placement=pb, surface=1, q1=qb))
+    return _spec("stickbutton_direct" if direct_blue else "stickbutton", objs, obbs, surfs, b, [], n, steps)
+
+
+CONFIG_NAMES = {1: "pickplace", 2: "obstruction", 3: "tetris4_goal", 4: "tetris6_knots", 5: "tetris4",
+                6: "stickbutton", 7: "stickbutton_direct"}
+CONFIG_SIZES = {1: 256, 2: 8192, 3: 32768, 4: 131072, 5: 1 << 20, 6: 4096, 7: 4096}
 
 
 def _f32(obj):
@@ -377,7 +440,8 @@ def _f32(obj):
 
 
 def make_config(cfg: int, n: Optional[int] = None, steps: int = 100) -> ProblemSpec:
-    """ProblemSpec of BASELINE.json config `cfg` (1-5) with all float constants float32-representable."""
+    """ProblemSpec of BASELINE.json config `cfg` (1-5; 6/7 = Stick Button skeletons) with all float
+    constants float32-representable."""
     n = CONFIG_SIZES[cfg] if n is None else n
     if cfg == 1:
         spec = config_pickplace(n, steps)
@@ -389,6 +453,8 @@ def make_config(cfg: int, n: Optional[int] = None, steps: int = 100) -> ProblemS
         spec = config_tetris6_knots(n, steps)
     elif cfg == 5:
         spec = config_tetris4(n, steps, goal=False)
+    elif cfg in (6, 7):   # Stick Button family (not a BASELINE config: parity / planner only)
+        spec = config_stickbutton(n, steps, direct_blue=cfg == 7)
     else:
         raise ValueError(cfg)
     return _f32(spec)
