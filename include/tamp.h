@@ -138,6 +138,9 @@ typedef struct {
     int32_t kind, is_const, obj, surface, n_knots;
     float value[7];
     float lo[4], hi[4];
+    uint32_t rng_stream;                  /* sampler stream (Philox counter word 2): 0 = the variable's index;
+                                             equal streams + equal sampler inputs give equal samples, which is
+                                             how a planner reuses a shared subgraph's samples */
 } tamp_var_desc;
 
 /* ground action (Listing 1); unused fields = -1.  Pick/Place use q1 as their conf;
@@ -195,6 +198,7 @@ typedef struct {
     int32_t lanes_per_particle;           /* mapping chosen for the particle kernel */
     int32_t block_threads, block_sync;    /* launch configuration chosen for the particle kernel */
     int64_t pairs_self;                   /* robot self-collision sphere pairs per particle-step */
+    int32_t term_action[TAMP_MAX_TERMS];  /* index of the skeleton action that emitted each hard term */
 } tamp_info;
 
 typedef struct tamp_ctx tamp_ctx;
@@ -219,7 +223,7 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
 tamp_status tamp_get_info(const tamp_ctx* ctx, tamp_info* out);
 
 /* InitializeParticles (Alg. 1): Philox4x32-10 counter RNG (key = seed, counter =
-   (global index, variable id, block)); grasps top-down and frozen, placements uniform on the
+   (global index lo, hi, variable stream = rng_stream or the variable index, block)); grasps top-down and frozen, placements uniform on the
    surface region, confs uniform within joint limits, then (ik_iters > 0) the conditional IK sampler
     toward each Pick/Place conf's Kin target, knots linear interpolation.  Resets Adam
    (m = v = 0, t = 0) and the invalid flags. */

@@ -236,6 +236,7 @@ class Term:
     grasp: int = -1
     placement: int = -1
     surface: int = -1
+    action: int = -1                # index of the skeleton action that emitted the term
 
 
 @dataclasses.dataclass
@@ -280,7 +281,8 @@ def build_csp(spec: ProblemSpec) -> CSP:
     held = None
     terms: List[Term] = []
     trajs = []
-    for a in spec.actions:
+    for ai, a in enumerate(spec.actions):
+        n_before = len(terms)
         if a.kind in (MOVE_FREE, MOVE_HOLD):
             if a.traj >= 0 and V[a.traj].n_knots > 0:
                 hv = (a.obj, a.grasp) if a.kind == MOVE_HOLD else None
@@ -342,6 +344,8 @@ def build_csp(spec: ProblemSpec) -> CSP:
             terms.append(Term("PC", obj=a.obj, placement=a.placement, surface=a.surface))
             if a.kind == PRESS_STICK:
                 terms.append(Term("CP", obj=a.obj, placement=a.placement, surface=a.surface, scene=scene))
+        for t in terms[n_before:]:
+            t.action = ai
     goal = {o: pose[o] for o in spec.goal_objs}
     return CSP(terms=terms, traj_costs=trajs, goal=goal, offsets=offsets, D=D, grasp_vars=grasp_vars,
                lo=np.array(lo, float), hi=np.array(hi, float), lr=np.array(lr, float))
@@ -384,6 +388,11 @@ def ik_dls(robot, q, T_target, iters, damping):
     return q
 
 
+def _stream(V, vi):
+    """Philox counter word of variable vi's sampler: its rng_stream if set, else its index."""
+    return int(getattr(V[vi], "rng_stream", 0)) or vi
+
+
 def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarray):
     """Returns x0 [N, D] float64 and grasps [N, G, 3, 4] float64.
 
@@ -400,7 +409,7 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
         o = spec.objects[V[vi].obj]
         o = dataclasses.replace(o, grasp_y=o.grasp_xy if getattr(o, "grasp_y", -1.0) < 0 else o.grasp_y)
         if getattr(o, "grasp_mode", 0) == 1:     # 6-DOF: face, gx, gy, gamma
-            u = uniforms(seed, gidx, vi, 4)
+            u = uniforms(seed, gidx, _stream(V, vi), 4)
             face = np.minimum(np.floor(u[:, 0] * 5), 4).astype(np.int64)
             gx = -o.grasp_xy + 2 * o.grasp_xy * u[:, 1]
             gy = -o.grasp_y + 2 * o.grasp_y * u[:, 2]
@@ -409,7 +418,7 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
                               torch.full((N,), o.grasp_z, dtype=DT), torch.as_tensor(gamma))
             grasps[:, gi] = T[:, :3, :].numpy()
             continue
-        u = uniforms(seed, gidx, vi, 3)
+        u = uniforms(seed, gidx, _stream(V, vi), 3)
         gx = -o.grasp_xy + 2 * o.grasp_xy * u[:, 0]
         gy = -o.grasp_y + 2 * o.grasp_y * u[:, 1]
         gamma = -math.pi + 2 * math.pi * u[:, 2]
@@ -421,14 +430,14 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
             continue
         off = csp.offsets[vi]
         if v.kind == CONF:
-            u = uniforms(seed, gidx, vi, 7)
+            u = uniforms(seed, gidx, _stream(V, vi), 7)
             x[:, off:off + 7] = spec.robot.joint_lo + u * (spec.robot.joint_hi - spec.robot.joint_lo)
         elif v.kind == PLACEMENT:
             s = spec.surfaces[v.surface]
             f = spec.objects[v.obj].footprint
             if any(a.kind in (PRESS, PRESS_STICK) and a.placement == vi for a in spec.actions):
                 f = 0.0     # press pose: uniform on the whole button face (R8)
-            u = uniforms(seed, gidx, vi, 3)
+            u = uniforms(seed, gidx, _stream(V, vi), 3)
             wx = max(s.hi[0] - s.lo[0] - 2 * f, 0.0)
             wy = max(s.hi[1] - s.lo[1] - 2 * f, 0.0)
             lx = (s.lo[0] + s.hi[0]) / 2 - wx / 2 + u[:, 0] * wx

@@ -82,6 +82,7 @@ struct tamp_ctx {
     int32_t t = 0;
     bool ready = false;
     int32_t term_kind[TAMP_MAX_TERMS];
+    int32_t term_action[TAMP_MAX_TERMS];
     std::vector<float> coords;   // lr | lo | hi, uploaded at init
     int64_t pairs_sb = 0, pairs_ss = 0;
     int32_t n_robot_spheres = 0;
@@ -127,6 +128,7 @@ struct Compiled {
     KSampleProgram SP;
     std::vector<float> lr, lo, hi;
     int32_t term_kind[TAMP_MAX_TERMS];
+    int32_t term_action[TAMP_MAX_TERMS];
     int64_t pairs_sb = 0, pairs_ss = 0;
 };
 
@@ -348,11 +350,13 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
     for (int o = 0; o < d.n_objects; ++o) pose[o] = init_inst[o] >= 0 ? init_inst[o] : -2;
     int held = -1;
     int n_terms = 0, n_fk = 0, n_place = 0, n_traj = 0, n_part = 0;
+    int cur_action = -1;
     auto add_term = [&](int kind) -> int16_t {
         if (n_terms >= TAMP_MAX_TERMS) return -1;
         P.term_lam[n_terms] = d.lam[kind];
         P.term_eps[n_terms] = d.eps[kind];
         C.term_kind[n_terms] = kind;
+        C.term_action[n_terms] = cur_action;
         return (int16_t)n_terms++;
     };
     auto add_partners = [&](int skip_a, int skip_b, int16_t& begin, int16_t& count) -> bool {
@@ -369,6 +373,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
     auto conf_ok = [&](int v) { return v >= 0 && v < d.n_vars && d.var[v].kind == TAMP_VAR_CONF; };
     for (int ai = 0; ai < d.n_actions; ++ai) {
         const tamp_action_desc& a = d.action[ai];
+        cur_action = ai;
         if (a.kind == TAMP_MOVE_FREE || a.kind == TAMP_MOVE_HOLD) {
             REQUIRE(conf_ok(a.q1) && conf_ok(a.q2), TAMP_E_INVALID, "motion endpoints must be conf variables");
             if (a.kind == TAMP_MOVE_HOLD) REQUIRE(held == a.obj && a.obj >= 0, TAMP_E_INVALID, "MoveHold: object not held");
@@ -560,6 +565,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         KSVar& S = SP.v[ns];
         std::memset(&S, 0, sizeof(S));
         S.var_id = (int16_t)v;
+        S.stream = V.rng_stream ? V.rng_stream : (uint32_t)v;
         S.xoff = (int16_t)xoff[v];
         S.slot = (int16_t)gslot[v];
         if (V.kind == TAMP_VAR_GRASP) {
@@ -748,6 +754,7 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     c->P = C.P;
     c->SP = C.SP;
     std::memcpy(c->term_kind, C.term_kind, sizeof(c->term_kind));
+    std::memcpy(c->term_action, C.term_action, sizeof(c->term_action));
     c->pairs_sb = C.pairs_sb;
     c->pairs_ss = C.pairs_ss;
     c->n_robot_spheres = desc->robot.n_spheres;
@@ -882,7 +889,10 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     out->n_hard = c->P.n_terms;
     out->n_grasp = c->P.n_grasp;
     out->n_fk = c->P.n_fk;
-    for (int i = 0; i < c->P.n_terms; ++i) out->term_kind[i] = c->term_kind[i];
+    for (int i = 0; i < c->P.n_terms; ++i) {
+        out->term_kind[i] = c->term_kind[i];
+        out->term_action[i] = c->term_action[i];
+    }
     out->n_local = c->n;
     out->global_offset = c->gofs;
     out->n_global = c->nglob;

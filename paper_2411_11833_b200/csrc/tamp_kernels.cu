@@ -38,8 +38,8 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
-__device__ __forceinline__ void uniform4(uint64_t seed, uint64_t gidx, int var, int block, float u[4]) {
-    const uint4 w = philox4x32_10(make_uint4((uint32_t)gidx, (uint32_t)(gidx >> 32), (uint32_t)var, (uint32_t)block),
+__device__ __forceinline__ void uniform4(uint64_t seed, uint64_t gidx, uint32_t var, int block, float u[4]) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)gidx, (uint32_t)(gidx >> 32), var, (uint32_t)block),
                                   make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
     const float s = 1.0f / 16777216.0f;
     u[0] = (float)(w.x >> 8) * s; u[1] = (float)(w.y >> 8) * s;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
         const KSVar& V = SP.v[vi];
         float u[8];
         if (V.kind == KS_GRASP) {       // grasps in the object frame, frozen
-            uniform4(seed, gidx, V.var_id, 0, u);
+            uniform4(seed, gidx, V.stream, 0, u);
             const float gxy = V.a[0];
             float* g = grasp + (i * SP.n_grasp + V.slot) * 12;
             const bool six = V.a[2] > 0.5f;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
                 g[8] = R[6]; g[9] = R[7]; g[10] = R[8]; g[11] = V.a[1];
             }
         } else if (V.kind == KS_PLACEMENT) {   // uniform on the surface region shrunk by the footprint
-            uniform4(seed, gidx, V.var_id, 0, u);
+            uniform4(seed, gidx, V.stream, 0, u);
             // a = [region lo x, lo y, hi x, hi y, footprint, frame x, frame y, frame z_top, frame yaw]
             const float wx = fmaxf(V.a[2] - V.a[0] - 2.f * V.a[4], 0.f);
             const float wy = fmaxf(V.a[3] - V.a[1] - 2.f * V.a[4], 0.f);
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
             xi[V.xoff + 2] = V.a[7];
             xi[V.xoff + 3] = fyaw + lyaw;
         } else if (V.kind == KS_CONF) {        // uniform within joint limits
-            uniform4(seed, gidx, V.var_id, 0, u);
-            uniform4(seed, gidx, V.var_id, 1, u + 4);
+            uniform4(seed, gidx, V.stream, 0, u);
+            uniform4(seed, gidx, V.stream, 1, u + 4);
 #pragma unroll
             for (int j = 0; j < TAMP_NJ; ++j) xi[V.xoff + j] = SP.jlo[j] + u[j] * (SP.jhi[j] - SP.jlo[j]);
         }

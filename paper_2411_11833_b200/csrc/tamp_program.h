@@ -93,6 +93,7 @@ struct KProgram {
 // Particle-initialisation program (K1).
 enum { KS_GRASP = 0, KS_PLACEMENT = 1, KS_CONF = 2, KS_TRAJ = 3 };
 struct KSVar {
+    uint32_t stream;                            // Philox counter word 2 (rng_stream or the variable index)
     int16_t kind, var_id, xoff, slot;          // slot: grasp slot for KS_GRASP
     int16_t q1_xoff, q1_const, q2_xoff, q2_const, n_knots;
     float a[12];                                // sampler parameters (see k_sample)

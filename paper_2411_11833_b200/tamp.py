@@ -60,7 +60,7 @@ class SurfaceDesc(ctypes.Structure):
 
 class VarDesc(ctypes.Structure):
     _fields_ = [("kind", I32), ("is_const", I32), ("obj", I32), ("surface", I32), ("n_knots", I32),
-                ("value", F * 7), ("lo", F * 4), ("hi", F * 4)]
+                ("value", F * 7), ("lo", F * 4), ("hi", F * 4), ("rng_stream", ctypes.c_uint32)]
 
 
 class ActionDesc(ctypes.Structure):
@@ -89,7 +89,8 @@ class Info(ctypes.Structure):
                 ("n_local", I64), ("global_offset", I64), ("n_global", I64), ("t", I32),
                 ("pairs_sphere_obb", I64), ("pairs_sphere_sphere", I64), ("n_kin", I32), ("n_place", I32),
                 ("n_goal_pairs", I32), ("n_traj_seg", I32), ("n_robot_spheres", I32),
-                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32), ("pairs_self", I64)]
+                ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32), ("pairs_self", I64),
+                ("term_action", I32 * MAX_TERMS)]
 
 
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
@@ -205,6 +206,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
         if v.value is not None:
             for k in range(len(v.value)):
                 dv.value[k] = float(v.value[k])
+        dv.rng_stream = int(getattr(v, "rng_stream", 0)) & 0xFFFFFFFF
         for k in range(4):
             dv.lo[k] = float(v.lo[k]) if v.lo is not None else -math.inf
             dv.hi[k] = float(v.hi[k]) if v.hi is not None else math.inf
@@ -267,6 +269,7 @@ class TampContext:
         _check(self.lib.tamp_get_info(self.h, ctypes.byref(info)))
         self.D, self.n_hard, self.n_grasp, self.n_fk = info.D, info.n_hard, info.n_grasp, info.n_fk
         self.term_kinds = [TERM_NAMES[info.term_kind[i]] for i in range(self.n_hard)]
+        self.term_actions = [int(info.term_action[i]) for i in range(self.n_hard)]
         self.work = dict(pairs_sphere_obb=info.pairs_sphere_obb, pairs_sphere_sphere=info.pairs_sphere_sphere,
                          n_kin=info.n_kin, n_place=info.n_place, n_goal_pairs=info.n_goal_pairs,
                          n_traj_seg=info.n_traj_seg, n_robot_spheres=info.n_robot_spheres, n_fk=info.n_fk,

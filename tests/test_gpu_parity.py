@@ -417,3 +417,31 @@ def test_smooth_collision_matches_oracle(cfg, lanes):
     unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
     close = np.abs(x1 - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
     assert np.all(close | unstable | kinks[:, None])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
+def test_compiled_term_structure_matches_oracle(cfg):
+    """The library's skeleton compiler and the oracle's build_csp emit the same hard terms in the same
+    order, each attributed to the same skeleton action (the planner's subgraph signatures rely on it)."""
+    spec = make_config(cfg, n=8)
+    spec.self_collision = cfg in (1, 6)
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, 8)
+    assert ctx.term_kinds == [t.kind for t in csp.terms]
+    assert ctx.term_actions == [t.action for t in csp.terms]
+    assert ctx.D == csp.D
+
+
+def test_sampler_with_subgraph_streams_matches_oracle():
+    """K1 with caller-chosen sampler streams (rng_stream, used for sharing subgraph samples across
+    skeletons) against the oracle with the same streams."""
+    import paper_2411_11833_b200.planner as planner
+    n, gofs = 301, 77
+    spec = planner.with_subgraph_streams(make_config(6, n=n))
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, n, global_offset=gofs, n_global=1000)
+    ctx.sample(seed=5)
+    st = ctx.get_state()
+    x0, g0 = O.initialize_particles(spec, csp, 5, np.arange(gofs, gofs + n))
+    np.testing.assert_allclose(st["x"].cpu().numpy(), x0, rtol=2e-6, atol=2e-6)
+    np.testing.assert_allclose(st["grasp"].cpu().numpy(), g0.reshape(n, -1, 12), rtol=0, atol=2e-6)

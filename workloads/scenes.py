@@ -94,6 +94,7 @@ class Var:
     n_knots: int = 0                      # traj: free knots
     lo: Optional[np.ndarray] = None       # placement clamp bounds (4,) (L11)
     hi: Optional[np.ndarray] = None
+    rng_stream: int = 0                   # sampler stream (Philox counter word); 0 = the variable's index
 
 
 @dataclasses.dataclass
