@@ -226,6 +226,7 @@ __device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, flo
 }
 
 constexpr float kFar = 1e18f;   // position of padded (absent) spheres: never within reach of anything
+constexpr float kBroadMaxRad = 0.5f;   // OBBs with a larger bounding sphere skip the broad phase and pre-test
 
 // NS query spheres per lane (registers) vs the 8 (padded) spheres of one object instance (shared memory,
 // broadcast to the group).  Fast path: branch-free test of all NS x 8 pairs (d^2 - (ra+rb)^2 < 0 ?), no
@@ -292,6 +293,14 @@ __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], cons
 template <bool GRAD, int NS>
 __device__ __forceinline__ float spheres_vs_obb(const float (&w)[NS][3], const float (&rr)[NS], const KObb& B,
                                                 float lam, float (&g)[NS][3], float smooth) {
+    // a box larger than the arm's reach (the table): no broad phase / pre-test, which would rarely reject
+    if (B.rad >= kBroadMaxRad) {
+        float j = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            j += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, g[k][0], g[k][1], g[k][2], smooth);
+        return j;
+    }
     // broad phase: bounding sphere of the box
     float mb = 1.f;
 #pragma unroll

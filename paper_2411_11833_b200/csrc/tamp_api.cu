@@ -14,6 +14,7 @@
 #include <tuple>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +82,7 @@ struct tamp_ctx {
     int stride_bytes = 0;
     int32_t t = 0;
     bool ready = false;
+    bool checked = false;        // cls / cost / counts are those of the current state (no step since)
     int32_t term_kind[TAMP_MAX_TERMS];
     int32_t term_action[TAMP_MAX_TERMS];
     std::vector<float> coords;   // lr | lo | hi, uploaded at init
@@ -936,6 +938,7 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_inv, 0, (size_t)c->n, st), "sample: zero invalid");
     c->t = 0;
     c->ready = true;
+    c->checked = false;
     return TAMP_OK;
 }
 
@@ -958,6 +961,7 @@ tamp_status tamp_optimize_step(tamp_ctx* c, int32_t n_steps, void* stream) {
         CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->bsync, c->threads, c->P, A, c->smem,
                                  static_cast<cudaStream_t>(stream)), "optimize");
         c->t += k;
+        c->checked = false;
         done += k;
     }
     return TAMP_OK;
@@ -970,6 +974,7 @@ static tamp_status run_check(tamp_ctx* c, cudaStream_t st) {
     A.out_counts = c->at<int32_t>(c->o_counts);
     CUDA_TRY(cudaMemsetAsync(A.out_counts, 0, (TAMP_MAX_TERMS + 2) * 4, st), "check: zero counts");
     CUDA_TRY(launch_particle(MODE_CHECK, c->gs, c->bsync, c->threads, c->P, A, c->smem, st), "check");
+    c->checked = true;
     return TAMP_OK;
 }
 
@@ -994,8 +999,10 @@ tamp_status tamp_best_k(tamp_ctx* c, int32_t k, float* records, void* stream) {
     if (!records || k < 1 || k > 1024 || k > c->n) return fail(TAMP_E_INVALID, "need 1 <= k <= min(1024, n_local)");
     DeviceGuard g(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    tamp_status s = run_check(c, st);
-    if (s != TAMP_OK) return s;
+    if (!c->checked) {       // classes and costs of the current state (a check since the last step reuses them)
+        tamp_status s = run_check(c, st);
+        if (s != TAMP_OK) return s;
+    }
     unsigned long long *ka = c->at<unsigned long long>(c->o_ka), *kb = c->at<unsigned long long>(c->o_kb);
     int32_t *pa = c->at<int32_t>(c->o_pa), *pb = c->at<int32_t>(c->o_pb);
     CUDA_TRY(launch_make_keys(c->at<uint8_t>(c->o_cls), c->at<float>(c->o_cost), c->n, c->gofs, ka, pa, st), "best_k: keys");
@@ -1087,6 +1094,7 @@ tamp_status tamp_set_state(tamp_ctx* c, const float* x, const float* m, const fl
         CUDA_TRY(cudaStreamSynchronize(st), "set_state: sync");
     c->t = t;
     c->ready = true;
+    c->checked = false;
     return TAMP_OK;
 }
 
