@@ -36,6 +36,8 @@ CONFIG_DESC = {
     3: "Tetris-4 packing + min-object-distance goal cost",
     4: "Tetris-6 packing with trajectory-knot collision costs",
     5: "Tetris-4 packing skeleton (particle-count sweep)",
+    6: "Stick Button: press red directly, press the out-of-reach blue button with the stick (not a BASELINE config)",
+    7: "Stick Button, infeasible skeleton: press blue with the fingertip (not a BASELINE config)",
 }
 
 

@@ -175,9 +175,13 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
     }
     const float jlo = gl < TAMP_NJ ? P.jlo[gl] : 0.f;
     const float jhi = gl < TAMP_NJ ? P.jhi[gl] : 0.f;
+    // blockIdx.y selects the conf: the Kin-constrained confs are independent given the sampled grasps and
+    // placements, so (particle, conf) pairs run in parallel (more warps to hide the serial solve's latency)
+    int nth = 0;
     for (int f = 0; f < P.n_fk; ++f) {
         const KFk K = P.fk[f];
         if ((K.term_kp < 0 && K.term_kr < 0) || K.ghost) continue;
+        if (nth++ != (int)blockIdx.y) continue;
         // Kin target T* = T(p) T(g)
         const KInst& I = P.inst[K.kin_inst];
         float pp[4];
@@ -244,10 +248,16 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
         if (gl < TAMP_NJ && active) xp[K.xoff + gl] = q;
         __syncwarp();
     }
-    // knots: linear interpolation between the (refined) endpoint confs
+}
+
+// knots: linear interpolation between the (IK-refined) endpoint confs; 8 lanes per particle
+__global__ void __launch_bounds__(128) k_knots(const __grid_constant__ KProgram P, float* __restrict__ x, int64_t n) {
+    const int gl = threadIdx.x & (kGroup - 1);
+    const int64_t p = (int64_t)blockIdx.x * (blockDim.x / kGroup) + threadIdx.x / kGroup;
+    if (p >= n || gl >= TAMP_NJ) return;
+    float* xp = x + p * P.D;
     for (int tr = 0; tr < P.n_traj; ++tr) {
         const KTraj& Tj = P.traj[tr];
-        if (gl >= TAMP_NJ || !active) continue;
         const float qa = Tj.q1_xoff >= 0 ? xp[Tj.q1_xoff + gl] : P.const_conf[Tj.q1_const][gl];
         const float qb = Tj.q2_xoff >= 0 ? xp[Tj.q2_xoff + gl] : P.const_conf[Tj.q2_const][gl];
         for (int j = 0; j < Tj.n_knots; ++j) {
@@ -378,9 +388,19 @@ int particle_kernel_regs(int gs) { return particle_kernel_regs_sm(gs); }
 cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
                       cudaStream_t st) {
     if (n <= 0 || iters <= 0) return cudaSuccess;
+    int n_kin = 0;
+    for (int f = 0; f < P.n_fk; ++f)
+        if ((P.fk[f].term_kp >= 0 || P.fk[f].term_kr >= 0) && !P.fk[f].ghost) ++n_kin;
     const int per_block = 128 / kGroup;
-    k_ik<<<(unsigned)((n + per_block - 1) / per_block), 128, 0, st>>>(P, x, grasp, n, iters, damping * damping);
-    counted();
+    const unsigned bx = (unsigned)((n + per_block - 1) / per_block);
+    if (n_kin > 0) {
+        k_ik<<<dim3(bx, (unsigned)n_kin), 128, 0, st>>>(P, x, grasp, n, iters, damping * damping);
+        counted();
+    }
+    if (P.n_traj > 0) {
+        k_knots<<<bx, 128, 0, st>>>(P, x, n);
+        counted();
+    }
     return cudaGetLastError();
 }
 
