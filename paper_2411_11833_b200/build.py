@@ -6,8 +6,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 # one translation unit per instantiation group so the (slow) k_particle variants compile in parallel
 SRCS = [os.path.join(HERE, "csrc", f) for f in ("tamp_api.cu", "tamp_kernels.cu", "tamp_particle_hinge.cu",
-                                                 "tamp_particle_smooth.cu")]
+                                                 "tamp_particle_smooth.cu", "tamp_particle_serial.cu")]
 HDRS = [os.path.join(HERE, "csrc", "tamp_program.h"), os.path.join(HERE, "csrc", "particle.cuh"),
+        os.path.join(HERE, "csrc", "particle_serial.cuh"),
         os.path.join(ROOT, "include", "tamp.h")]
 LIB = os.path.join(HERE, "libtamp.so")
 OBJ_DIR = os.path.join(HERE, "csrc", "build")

@@ -1,0 +1,536 @@
+// particle_serial.cuh -- the serial mapping of K2 / K3 / eval: one thread per particle.
+//
+// The lane mapping (particle.cuh) spreads a particle over 4-16 lanes, which hides latency when particles
+// are few but repeats the per-particle serial work (FK scan steps, Kin, bookkeeping) on every lane of the
+// group.  When a launch holds many waves of particles of a small skeleton (config 1 at 2^17-2^20
+// particles), one thread per particle does the minimal work: the chain is composed once, no shuffles.
+//
+// Per FK instance, without storing the link frames: forward T_1 .. T_8 (= tool), Kin at T_8, then a
+// backward sweep over the links 8 -> 1 recovering T_{l-1} = T_l Rz(-q_l) F_l^{-1} while it evaluates
+// that link's spheres and accumulates the suffix wrench (F, M) of all links >= l, so that
+// dJ/dq_l = z_l . (M - o_l x F) is available exactly when joint l is reached.
+// Per-thread state (x, gradient, grasps, instance poses and wrenches) lives in shared memory in
+// thread-major columns (value f of thread t at [f * blockDim + t]: conflict-free).
+// Supported: every term except SELF and held objects at knots (tamp_api.cu selects the lane mapping then).
+#pragma once
+#include "particle.cuh"
+
+namespace tamp {
+
+struct SerialLayout {
+    int x, m, v, g, gT, ipose, iwr, n;   // column offsets (floats per thread)
+};
+
+// mv: Adam moments resident in shared memory for the launch (optimisation mode only)
+__host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool mv) {
+    SerialLayout L;
+    int f = 0;
+    L.x = f;     f += P.D;
+    L.m = f;     f += mv ? P.D : 0;
+    L.v = f;     f += mv ? P.D : 0;
+    L.g = f;     f += P.D;
+    L.gT = f;    f += 12 * P.n_grasp;
+    L.ipose = f; f += 8 * P.n_inst;    // cos, sin, px, py, pz, world bounding-sphere centre xyz
+    L.iwr = f;   f += 6 * P.n_inst;    // wrench (F, M about the world origin) on each instance
+    L.n = f;
+    return L;
+}
+
+constexpr int kSerialThreads = 128;
+
+// dynamic shared memory of a serial-mapping block of `threads` particles (column pitch threads + 1: the
+// cooperative row <-> column transposes hit distinct banks)
+__host__ __device__ inline size_t serial_smem_bytes(const KProgram& P, int threads, bool mv) {
+    return (size_t)serial_layout(P, mv).n * (threads + 1) * sizeof(float);
+}
+
+// term bookkeeping: warp-aggregated counts (every thread of the warp calls it for the same term)
+template <int MODE>
+__device__ __forceinline__ void serial_term(const KProgram& P, const KArgs& A, TermSink<MODE>& sink, int term, float val,
+                                            bool active, int64_t p, int* s_counts) {
+    sink.J = fmaf(P.term_lam[term], val, sink.J);
+    if (MODE == MODE_EVAL) {
+        if (active && A.out_Jc) A.out_Jc[p * P.n_terms + term] = val;
+    } else if (MODE == MODE_CHECK) {
+        const bool ok = val <= P.term_eps[term];
+        sink.sat = sink.sat && ok;
+        const unsigned b = __ballot_sync(FULL, active && ok);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_counts[term], __popc(b));
+    }
+}
+
+template <int MODE, bool SMOOTH>
+__global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_constant__ KProgram P, const KArgs A) {
+    constexpr bool GRAD = MODE != MODE_CHECK;
+    const float smooth = SMOOTH ? P.smooth : 0.f;
+    extern __shared__ float4 smem4[];
+    __shared__ float4 s_osph[TAMP_MAX_OBJECTS][TAMP_MAX_OBJ_SPHERES];
+    __shared__ int s_counts[TAMP_MAX_TERMS + 2];
+    float* S = reinterpret_cast<float*>(smem4);
+    const int NT = blockDim.x, tid = threadIdx.x;
+    const int64_t pid = (int64_t)blockIdx.x * NT + tid;
+    const bool active = pid < A.n;
+    const int64_t p = active ? pid : (A.n - 1);
+    const SerialLayout L = serial_layout(P, MODE == MODE_OPT);
+    const int D = P.D;
+    const int PITCH = NT + 1;
+    auto col = [&](int f) -> float& { return S[(size_t)f * PITCH + tid]; };
+    // block-cooperative, coalesced copy between the block's rows of a [n][w] array and columns c0..c0+w
+    const int64_t row0 = (int64_t)blockIdx.x * NT;
+    const int nrows = (int)min((int64_t)NT, A.n - row0);
+    auto load_rows = [&](const float* src, int w, int c0) {
+        const float* base = src + row0 * w;
+        for (int e = tid; e < nrows * w; e += NT) S[(size_t)(c0 + e % w) * PITCH + e / w] = base[e];
+    };
+    auto store_rows = [&](float* dst, int w, int c0) {
+        float* base = dst + row0 * w;
+        for (int e = tid; e < nrows * w; e += NT) base[e] = S[(size_t)(c0 + e % w) * PITCH + e / w];
+    };
+    auto xs = [&](int d) -> float& { return col(L.x + d); };
+    auto gs = [&](int d) -> float& { return col(L.g + d); };
+    auto ip = [&](int i, int k) -> float& { return col(L.ipose + 8 * i + k); };
+    auto iw = [&](int i, int k) -> float& { return col(L.iwr + 6 * i + k); };
+    auto add_iw = [&](int i, const Wrench& w) {
+        iw(i, 0) += w.f[0]; iw(i, 1) += w.f[1]; iw(i, 2) += w.f[2];
+        iw(i, 3) += w.m[0]; iw(i, 4) += w.m[1]; iw(i, 5) += w.m[2];
+    };
+
+    for (int i = tid; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += NT) {
+        const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
+        s_osph[o][k] = make_float4(P.osph[o][k][0], P.osph[o][k][1], P.osph[o][k][2], P.osph[o][k][3]);
+    }
+    if (MODE == MODE_CHECK)
+        for (int i = tid; i < P.n_terms + 2; i += NT) s_counts[i] = 0;
+    load_rows(A.x, D, L.x);
+    if (MODE == MODE_OPT) {
+        load_rows(A.m, D, L.m);
+        load_rows(A.v, D, L.v);
+    }
+    if (P.n_grasp) load_rows(A.grasp, 12 * P.n_grasp, L.gT);
+    bool invalid = A.invalid[p] != 0;
+    __syncthreads();
+
+    // world sphere k of an instance at pose (cos, sin, px, py, pz)
+    struct IPose { float c, s, x, y, z; };
+    auto ipose = [&](int i) -> IPose { return IPose{ip(i, 0), ip(i, 1), ip(i, 2), ip(i, 3), ip(i, 4)}; };
+    auto inst_sphere = [&](const IPose& q, int obj, int k) -> float4 {
+        const float4 c = s_osph[obj][k];
+        return make_float4(fmaf(q.c, c.x, fmaf(-q.s, c.y, q.x)), fmaf(q.s, c.x, fmaf(q.c, c.y, q.y)), q.z + c.z, c.w);
+    };
+    // one query sphere vs one instance: broad phase on the instance's bounding sphere, then its spheres.
+    // Accumulates dJ/dw into g and the partner's reaction into pw (movable partners).
+    auto sphere_vs_inst = [&](float wx, float wy, float wz, float rr, int ii, float lam, float* g, Wrench& pw) -> float {
+        const int obj = P.inst[ii].obj;
+        const float dx = wx - ip(ii, 5), dy = wy - ip(ii, 6), dz = wz - ip(ii, 7);
+        const float R = rr + P.obound[obj][3];
+        if (fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) >= 0.f) return 0.f;
+        float j = 0.f;
+        const int no = P.osph_n[obj];
+        const IPose q = ipose(ii);
+        for (int k = 0; k < no; ++k) {
+            const float4 B = inst_sphere(q, obj, k);
+            float ux, uy, uz;
+            const float pen = sphere_sphere<GRAD>(wx, wy, wz, rr, B, lam, ux, uy, uz, smooth);
+            if (pen != 0.f) {
+                j += pen;
+                if (GRAD) {
+                    g[0] -= ux; g[1] -= uy; g[2] -= uz;
+                    pw.add_point(B.x, B.y, B.z, ux, uy, uz);
+                }
+            }
+        }
+        return j;
+    };
+    auto sphere_vs_obbs = [&](float wx, float wy, float wz, float rr, uint16_t mask, float lam, float* g) -> float {
+        float j = 0.f;
+        for (int b = 0; b < P.n_obb; ++b) {
+            if (!((mask >> b) & 1)) continue;
+            const KObb& B = P.obb[b];
+            if (B.rad < kBroadMaxRad) {
+                const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
+                const float R = rr + B.rad;
+                if (fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) >= 0.f) continue;
+            }
+            j += sphere_obb<GRAD>(wx, wy, wz, rr, B, lam, g[0], g[1], g[2], smooth);
+        }
+        return j;
+    };
+
+    const int n_iter = (MODE == MODE_OPT) ? A.n_steps : 1;
+    for (int it = 0; it < n_iter; ++it) {
+        TermSink<MODE> sink;
+        float soft = 0.f;
+
+        // ---- instances: pose, world bounding-sphere centre; zero accumulators ----
+        for (int i = 0; i < P.n_inst; ++i) {
+            const KInst& I = P.inst[i];
+            if (I.xoff >= 0 || it == 0) {
+                float px, py, pz, yaw;
+                if (I.xoff >= 0) { px = xs(I.xoff); py = xs(I.xoff + 1); pz = xs(I.xoff + 2); yaw = xs(I.xoff + 3); }
+                else { px = I.pose[0]; py = I.pose[1]; pz = I.pose[2]; yaw = I.pose[3]; }
+                float sy, cy;
+                fsincos(yaw, &sy, &cy);
+                const float* ob = P.obound[I.obj];
+                ip(i, 0) = cy; ip(i, 1) = sy; ip(i, 2) = px; ip(i, 3) = py; ip(i, 4) = pz;
+                ip(i, 5) = fmaf(cy, ob[0], fmaf(-sy, ob[1], px));
+                ip(i, 6) = fmaf(sy, ob[0], fmaf(cy, ob[1], py));
+                ip(i, 7) = pz + ob[2];
+            }
+            if (GRAD)
+                for (int k = 0; k < 6; ++k) iw(i, k) = 0.f;
+        }
+        if (GRAD)
+            for (int d = 0; d < D; ++d) gs(d) = 0.f;
+
+        // ---- robot configurations ----
+        for (int f = 0; f < P.n_fk; ++f) {
+            const KFk K = P.fk[f];
+            if (K.ghost) continue;
+            float q[TAMP_NJ], sq[TAMP_NJ], cq[TAMP_NJ];
+#pragma unroll
+            for (int j = 0; j < TAMP_NJ; ++j) {
+                q[j] = xs(K.xoff + j);
+                fsincos(q[j], &sq[j], &cq[j]);
+            }
+            // forward: T_{j+1} = T_j F_{j+1} Rz(q_{j+1}) (base folded into F_1), tool T_8 = T_7 F_ee
+            M34 T;
+#pragma unroll
+            for (int j = 0; j < TAMP_NJ; ++j) {
+                M34 Aj;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const float* Fr = P.F[j] + 4 * i;
+                    Aj.r[3 * i] = fmaf(Fr[0], cq[j], Fr[1] * sq[j]);
+                    Aj.r[3 * i + 1] = fmaf(Fr[1], cq[j], -Fr[0] * sq[j]);
+                    Aj.r[3 * i + 2] = Fr[2];
+                    Aj.t[i] = Fr[3];
+                }
+                T = j == 0 ? Aj : compose(T, Aj);
+            }
+            {
+                M34 Fe;
+                load_m34(Fe, P.F[kGroup - 1]);
+                T = compose(T, Fe);
+            }
+            Wrench sfx;      // suffix wrench of the links >= the current one (about the world origin)
+            sfx.zero();
+            // Kin(q, o, g, p): FK(q) = T(p) T(g) at the tool frame
+            if (K.term_kp >= 0 || K.term_kr >= 0) {
+                const int ki = K.kin_inst;
+                M34 Tp, Tg;
+                Tp.r[0] = ip(ki, 0); Tp.r[1] = -ip(ki, 1); Tp.r[2] = 0.f;
+                Tp.r[3] = ip(ki, 1); Tp.r[4] = ip(ki, 0); Tp.r[5] = 0.f;
+                Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f;
+                Tp.t[0] = ip(ki, 2); Tp.t[1] = ip(ki, 3); Tp.t[2] = ip(ki, 4);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const int b = L.gT + 12 * K.kin_grasp + 4 * i;
+                    Tg.r[3 * i] = col(b); Tg.r[3 * i + 1] = col(b + 1); Tg.r[3 * i + 2] = col(b + 2); Tg.t[i] = col(b + 3);
+                }
+                const M34 Ts = compose(Tp, Tg);
+                const float dx = T.t[0] - Ts.t[0], dy = T.t[1] - Ts.t[1], dz = T.t[2] - Ts.t[2];
+                const float epos = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                float Mm[9];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        Mm[3 * i + j] = fmaf(T.r[i], Ts.r[j], fmaf(T.r[3 + i], Ts.r[3 + j], T.r[6 + i] * Ts.r[6 + j]));
+                const float wx = Mm[7] - Mm[5], wy = Mm[2] - Mm[6], wz = Mm[3] - Mm[1];
+                const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
+                const float erot = fatan2_pos(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
+                if (K.term_kp >= 0) serial_term<MODE>(P, A, sink, K.term_kp, epos, active, p, s_counts);
+                if (K.term_kr >= 0) serial_term<MODE>(P, A, sink, K.term_kr, erot, active, p, s_counts);
+                if (GRAD) {
+                    Wrench tw;
+                    tw.zero();
+                    if (K.term_kp >= 0 && epos > 0.f) {
+                        const float k = P.term_lam[K.term_kp] / epos;
+                        const float fx = dx * k, fy = dy * k, fz = dz * k;
+                        sfx.add_point(T.t[0], T.t[1], T.t[2], fx, fy, fz);
+                        tw.add_point(Ts.t[0], Ts.t[1], Ts.t[2], -fx, -fy, -fz);
+                    }
+                    if (K.term_kr >= 0 && wn > 0.f) {
+                        const float k = P.term_lam[K.term_kr] / wn;
+                        const float ux = k * fmaf(T.r[0], wx, fmaf(T.r[1], wy, T.r[2] * wz));
+                        const float uy = k * fmaf(T.r[3], wx, fmaf(T.r[4], wy, T.r[5] * wz));
+                        const float uz = k * fmaf(T.r[6], wx, fmaf(T.r[7], wy, T.r[8] * wz));
+                        sfx.m[0] -= ux; sfx.m[1] -= uy; sfx.m[2] -= uz;
+                        tw.m[0] += ux; tw.m[1] += uy; tw.m[2] += uz;
+                    }
+                    if (P.inst[ki].xoff >= 0) add_iw(ki, tw);
+                }
+            }
+            // joint limits: dist_from_bounds(q, lo, hi) (Listing 2)
+            float jl = 0.f;
+            if (K.term_jl >= 0) {
+                float e2 = 0.f;
+#pragma unroll
+                for (int j = 0; j < TAMP_NJ; ++j) {
+                    const float e = fmaxf(fmaxf(P.jlo[j] - q[j], q[j] - P.jhi[j]), 0.f);
+                    e2 = fmaf(e, e, e2);
+                }
+                jl = sqrtf(e2);
+                serial_term<MODE>(P, A, sink, K.term_jl, jl, active, p, s_counts);
+            }
+            (void)sq; (void)cq;
+            // backward sweep over the links 8 -> 1: spheres of link l in T_l, suffix wrench, dJ/dq_l
+            const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
+            float jcf = 0.f;
+#pragma unroll 1
+            for (int l = kGroup - 1; l >= 0; --l) {
+                if (K.term_cf >= 0) {
+                    for (int k = 0; k < P.rsph_n[l]; ++k) {
+                        float wx, wy, wz;
+                        xform(T, P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], wx, wy, wz);
+                        const float rr = P.rsph[l][k][3] + P.eta;
+                        float g[3] = {0.f, 0.f, 0.f};
+                        jcf += sphere_vs_obbs(wx, wy, wz, rr, K.obb_mask, lam_cf, g);
+                        for (int pi = 0; pi < K.part_count; ++pi) {
+                            const int ii = P.partners[K.part_begin + pi];
+                            Wrench pw;
+                            pw.zero();
+                            jcf += sphere_vs_inst(wx, wy, wz, rr, ii, lam_cf, g, pw);
+                            if (GRAD && P.inst[ii].xoff >= 0 && pw.nonzero()) add_iw(ii, pw);
+                        }
+                        if (GRAD) sfx.add_point(wx, wy, wz, g[0], g[1], g[2]);
+                    }
+                }
+                if (l < TAMP_NJ) {     // joint l+1 rotates frame l+1 (= T here) about its z axis
+                    if (GRAD) {
+                        const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
+                        const float ox = T.t[0], oy = T.t[1], oz = T.t[2];
+                        const float mx = sfx.m[0] - (oy * sfx.f[2] - oz * sfx.f[1]);
+                        const float my = sfx.m[1] - (oz * sfx.f[0] - ox * sfx.f[2]);
+                        const float mz = sfx.m[2] - (ox * sfx.f[1] - oy * sfx.f[0]);
+                        float dq = fmaf(zx, mx, fmaf(zy, my, zz * mz));
+                        if (K.term_jl >= 0 && jl > 0.f) {
+                            const float ql = xs(K.xoff + l);
+                            const float e = fmaxf(fmaxf(P.jlo[l] - ql, ql - P.jhi[l]), 0.f);
+                            if (e > 0.f) dq += P.term_lam[K.term_jl] * (ql > P.jhi[l] ? e : -e) / jl;
+                        }
+                        gs(K.xoff + l) += dq;
+                    }
+                }
+                if (l > 0) {           // T_{l} -> T_{l-1}: right-multiply by (F_l Rz(q_l))^-1 = Rz(-q_l) F_l^-1
+                    if (l < TAMP_NJ) {
+                        float sl, cl;
+                        fsincos(xs(K.xoff + l), &sl, &cl);
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            const float a = T.r[3 * i], b = T.r[3 * i + 1];
+                            T.r[3 * i] = fmaf(a, cl, -b * sl);
+                            T.r[3 * i + 1] = fmaf(a, sl, b * cl);
+                        }
+                    }
+                    M34 Fi;
+                    load_m34(Fi, P.Finv[l]);
+                    T = compose(T, Fi);
+                }
+            }
+            if (K.term_cf >= 0) serial_term<MODE>(P, A, sink, K.term_cf, jcf, active, p, s_counts);
+        }
+
+        // ---- StablePlace / press contact / CFreePlace per Place or press action ----
+        for (int pl = 0; pl < P.n_place; ++pl) {
+            const KPlace& Q = P.place[pl];
+            const int ii = Q.inst;
+            const KInst& I = P.inst[ii];
+            const KSurface& Sf = P.surf[Q.surface];
+            const int obj = I.obj, no = P.osph_n[obj];
+            const IPose qi = ipose(ii);
+            Wrench own;
+            own.zero();
+            {   // support |z_bottom - z_top|
+                const float pz = ip(ii, 4);
+                const float e = fabsf(pz - Sf.frame[2]);
+                serial_term<MODE>(P, A, sink, Q.term_ss, e, active, p, s_counts);
+                if (GRAD && e > 0.f) own.add_point(ip(ii, 2), ip(ii, 3), pz, 0.f, 0.f, P.term_lam[Q.term_ss] * (pz > Sf.frame[2] ? 1.f : -1.f));
+            }
+            float sy, cy;
+            fsincos(Sf.frame[3], &sy, &cy);
+            if (Q.term_sc >= 0) {   // containment: sum over spheres of dist_from_bounds(xy, lo + r, hi - r)
+                float e = 0.f;
+                for (int k = 0; k < no; ++k) {
+                    const float4 c = inst_sphere(qi, obj, k);
+                    const float rx = c.x - Sf.frame[0], ry = c.y - Sf.frame[1];
+                    const float lx = fmaf(cy, rx, sy * ry), ly = fmaf(-sy, rx, cy * ry);
+                    const float lox = Sf.lo[0] + c.w, hix = Sf.hi[0] - c.w;
+                    const float loy = Sf.lo[1] + c.w, hiy = Sf.hi[1] - c.w;
+                    const float ex = fmaxf(fmaxf(lox - lx, lx - hix), 0.f);
+                    const float ey = fmaxf(fmaxf(loy - ly, ly - hiy), 0.f);
+                    const float eu = sqrtf(fmaf(ex, ex, ey * ey));
+                    e += eu;
+                    if (GRAD && eu > 0.f) {
+                        const float kk = P.term_lam[Q.term_sc] / eu;
+                        const float glx = (lx > hix ? ex : (lx < lox ? -ex : 0.f)) * kk;
+                        const float gly = (ly > hiy ? ey : (ly < loy ? -ey : 0.f)) * kk;
+                        own.add_point(c.x, c.y, c.z, fmaf(cy, glx, -sy * gly), fmaf(sy, glx, cy * gly), 0.f);
+                    }
+                }
+                serial_term<MODE>(P, A, sink, Q.term_sc, e, active, p, s_counts);
+            }
+            if (Q.term_pc >= 0) {   // press contact: min over spheres of dist_from_bounds(xy, lo, hi)
+                float emin = kFar, gx = 0.f, gy = 0.f, cx = 0.f, cyy = 0.f, cz = 0.f;
+                for (int k = 0; k < no; ++k) {
+                    const float4 c = inst_sphere(qi, obj, k);
+                    const float rx = c.x - Sf.frame[0], ry = c.y - Sf.frame[1];
+                    const float lx = fmaf(cy, rx, sy * ry), ly = fmaf(-sy, rx, cy * ry);
+                    const float ex = fmaxf(fmaxf(Sf.lo[0] - lx, lx - Sf.hi[0]), 0.f);
+                    const float ey = fmaxf(fmaxf(Sf.lo[1] - ly, ly - Sf.hi[1]), 0.f);
+                    const float eu = sqrtf(fmaf(ex, ex, ey * ey));
+                    if (eu < emin) {
+                        emin = eu;
+                        gx = eu > 0.f ? (lx > Sf.hi[0] ? ex : (lx < Sf.lo[0] ? -ex : 0.f)) / eu : 0.f;
+                        gy = eu > 0.f ? (ly > Sf.hi[1] ? ey : (ly < Sf.lo[1] ? -ey : 0.f)) / eu : 0.f;
+                        cx = c.x; cyy = c.y; cz = c.z;
+                    }
+                }
+                serial_term<MODE>(P, A, sink, Q.term_pc, emin, active, p, s_counts);
+                if (GRAD && emin > 0.f) {
+                    const float lam = P.term_lam[Q.term_pc];
+                    own.add_point(cx, cyy, cz, lam * fmaf(cy, gx, -sy * gy), lam * fmaf(sy, gx, cy * gy), 0.f);
+                }
+            }
+            if (Q.term_cp >= 0) {   // CFreePlace: the object's spheres vs OBBs (support excluded) and other objects
+                const float lam_cp = P.term_lam[Q.term_cp];
+                float jcp = 0.f;
+                for (int k = 0; k < no; ++k) {
+                    const float4 c = inst_sphere(qi, obj, k);
+                    const float rr = c.w + P.eta;
+                    float g[3] = {0.f, 0.f, 0.f};
+                    jcp += sphere_vs_obbs(c.x, c.y, c.z, rr, Q.obb_mask, lam_cp, g);
+                    for (int pi = 0; pi < Q.part_count; ++pi) {
+                        const int jj = P.partners[Q.part_begin + pi];
+                        Wrench pw;
+                        pw.zero();
+                        jcp += sphere_vs_inst(c.x, c.y, c.z, rr, jj, lam_cp, g, pw);
+                        if (GRAD && P.inst[jj].xoff >= 0 && pw.nonzero()) add_iw(jj, pw);
+                    }
+                    if (GRAD) own.add_point(c.x, c.y, c.z, g[0], g[1], g[2]);
+                }
+                serial_term<MODE>(P, A, sink, Q.term_cp, jcp, active, p, s_counts);
+            }
+            if (GRAD) add_iw(ii, own);
+        }
+
+        // ---- soft costs (Eq. 2 second sum) ----
+        if (P.n_goal > 1) {   // MinimizeObjDist (Listing 2 obj_dist)
+            for (int a = 0; a < P.n_goal; ++a)
+                for (int b = a + 1; b < P.n_goal; ++b) {
+                    const int ia = P.goal_inst[a], ib = P.goal_inst[b];
+                    const float ax = ip(ia, 2), ay = ip(ia, 3), az = ip(ia, 4);
+                    const float bx = ip(ib, 2), by = ip(ib, 3), bz = ip(ib, 4);
+                    const float dx = ax - bx, dy = ay - by, dz = az - bz;
+                    const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+                    soft = fmaf(P.lam_goal, d, soft);
+                    if (GRAD && d > 0.f) {
+                        const float k = P.lam_goal / d;
+                        Wrench w;
+                        if (P.inst[ia].xoff >= 0) { w.zero(); w.add_point(ax, ay, az, dx * k, dy * k, dz * k); add_iw(ia, w); }
+                        if (P.inst[ib].xoff >= 0) { w.zero(); w.add_point(bx, by, bz, -dx * k, -dy * k, -dz * k); add_iw(ib, w); }
+                    }
+                }
+        }
+        for (int tr = 0; tr < P.n_traj; ++tr) {   // TrajLength(tau) = sum_j ||k_{j+1} - k_j||
+            const KTraj& Tj = P.traj[tr];
+            const int nseg = Tj.n_knots + 1;
+            auto xoff_of = [&](int j) -> int {
+                if (j == 0) return Tj.q1_xoff;
+                if (j == nseg) return Tj.q2_xoff;
+                return Tj.knot_xoff + 7 * (j - 1);
+            };
+            auto val = [&](int j, int jt) -> float {
+                const int o = xoff_of(j);
+                if (o >= 0) return xs(o + jt);
+                return P.const_conf[j == 0 ? Tj.q1_const : Tj.q2_const][jt];
+            };
+            for (int j = 0; j < nseg; ++j) {
+                float dl[TAMP_NJ], s2 = 0.f;
+#pragma unroll
+                for (int jt = 0; jt < TAMP_NJ; ++jt) {
+                    dl[jt] = val(j + 1, jt) - val(j, jt);
+                    s2 = fmaf(dl[jt], dl[jt], s2);
+                }
+                const float len = sqrtf(s2);
+                soft = fmaf(P.lam_traj, len, soft);
+                if (GRAD && len > 0.f) {
+                    const int o1 = xoff_of(j + 1), o0 = xoff_of(j);
+#pragma unroll
+                    for (int jt = 0; jt < TAMP_NJ; ++jt) {
+                        const float g = P.lam_traj * dl[jt] / len;
+                        if (o1 >= 0) gs(o1 + jt) += g;
+                        if (o0 >= 0) gs(o0 + jt) -= g;
+                    }
+                }
+            }
+        }
+        const float Jtot = sink.J + soft;
+
+        // ---- instance wrenches -> placement gradients: dJ/dt = F, dJ/dyaw = z . (M - t x F) ----
+        if (GRAD)
+            for (int i = 0; i < P.n_inst; ++i) {
+                const KInst& I = P.inst[i];
+                if (I.xoff < 0) continue;
+                gs(I.xoff) += iw(i, 0);
+                gs(I.xoff + 1) += iw(i, 1);
+                gs(I.xoff + 2) += iw(i, 2);
+                gs(I.xoff + 3) += iw(i, 5) - (xs(I.xoff) * iw(i, 1) - xs(I.xoff + 1) * iw(i, 0));
+            }
+
+        if (MODE == MODE_EVAL) {
+            if (active) {
+                if (A.out_J) A.out_J[p] = Jtot;
+                if (A.out_soft) A.out_soft[p] = soft;
+                if (A.out_grad) for (int d = 0; d < D; ++d) A.out_grad[p * D + d] = gs(d);
+            }
+        } else if (MODE == MODE_CHECK) {
+            const bool inv = invalid || !isfinite(Jtot);
+            const int cls = inv ? 2 : (sink.sat ? 0 : 1);
+            if (active) {
+                A.out_cls[p] = (uint8_t)cls;
+                A.out_cost[p] = cls == 0 ? soft : (cls == 1 ? Jtot : 0.f);
+            }
+            const unsigned b0 = __ballot_sync(FULL, active && cls == 0), b2 = __ballot_sync(FULL, active && cls == 2);
+            if ((tid & 31) == 0) {
+                if (b0) atomicAdd(&s_counts[P.n_terms], __popc(b0));
+                if (b2) atomicAdd(&s_counts[P.n_terms + 1], __popc(b2));
+            }
+        } else {
+            // ---- Adam (Kingma & Ba) with grad scale 1/N (Eq. 4) + projection (L11) ----
+            bool bad = !isfinite(Jtot);
+            for (int d = 0; d < D; ++d) bad |= !isfinite(gs(d));
+            invalid = invalid || bad;
+            const float bc1 = A.bc1[it];
+            const float bc2 = A.bc2[it];
+            if (!invalid) {
+                for (int d = 0; d < D; ++d) {
+                    const float g = gs(d) * P.grad_scale;
+                    const float mm = fmaf(P.beta1, col(L.m + d), (1.f - P.beta1) * g);
+                    const float vv = fmaf(P.beta2, col(L.v + d), (1.f - P.beta2) * g * g);
+                    col(L.m + d) = mm;
+                    col(L.v + d) = vv;
+                    const float mh = mm / bc1;
+                    const float vh = vv / bc2;
+                    const float xn = xs(d) - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
+                    xs(d) = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
+                }
+            }
+        }
+    }
+
+    if (MODE == MODE_OPT) {
+        if (active) A.invalid[p] = invalid ? 1 : 0;
+        __syncthreads();
+        store_rows(A.x, D, L.x);
+        store_rows(A.m, D, L.m);
+        store_rows(A.v, D, L.v);
+    }
+    if (MODE == MODE_CHECK) {
+        __syncthreads();
+        for (int i = tid; i < P.n_terms + 2; i += NT)
+            if (s_counts[i]) atomicAdd(&A.out_counts[i], s_counts[i]);
+    }
+}
+
+}  // namespace tamp

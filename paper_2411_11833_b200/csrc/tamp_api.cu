@@ -21,6 +21,7 @@
 
 #include "../../include/tamp.h"
 #include "tamp_program.h"
+#include "particle_serial.cuh"
 
 namespace tamp {
 cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
@@ -30,6 +31,7 @@ cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int6
 cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
                       cudaStream_t st);
 int particle_kernel_regs(int gs);
+int serial_kernel_regs();
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
                         cudaStream_t st, unsigned long long** kres, int32_t** pres);
 cudaError_t launch_make_keys(const uint8_t* cls, const float* cost, int64_t n, int64_t gofs, unsigned long long* keys,
@@ -113,6 +115,13 @@ static H34 h_mul(const H34& a, const H34& b) {
 static H34 h_rx(double a) { H34 m = h_ident(); m.r[4] = cos(a); m.r[5] = -sin(a); m.r[7] = sin(a); m.r[8] = cos(a); return m; }
 static H34 h_rz(double a) { H34 m = h_ident(); m.r[0] = cos(a); m.r[1] = -sin(a); m.r[3] = sin(a); m.r[4] = cos(a); return m; }
 static H34 h_tr(double x, double y, double z) { H34 m = h_ident(); m.t[0] = x; m.t[1] = y; m.t[2] = z; return m; }
+static H34 h_inv(const H34& a) {
+    H34 o{};
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) o.r[3 * i + j] = a.r[3 * j + i];
+    for (int i = 0; i < 3; ++i) o.t[i] = -(o.r[3 * i] * a.t[0] + o.r[3 * i + 1] * a.t[1] + o.r[3 * i + 2] * a.t[2]);
+    return o;
+}
 static void h_store(const H34& a, float* o) {
     for (int i = 0; i < 3; ++i) {
         o[4 * i] = (float)a.r[3 * i]; o[4 * i + 1] = (float)a.r[3 * i + 1];
@@ -201,6 +210,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             H34 F = h_mul(h_rx(al), h_tr(a, 0.0, dd));
             if (j == 0) F = h_mul(T, F);
             h_store(F, P.F[j]);
+            h_store(h_inv(F), P.Finv[j]);
             P.jlo[j] = R.joint_lo[j];
             P.jhi[j] = R.joint_hi[j];
             SP.jlo[j] = R.joint_lo[j];
@@ -208,6 +218,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         }
         H34 tool = h_mul(h_mul(h_tr(0, 0, R.flange_d), h_rz(R.tcp_yaw)), h_tr(0, 0, R.tcp_d));
         h_store(tool, P.F[kGroup - 1]);
+        h_store(h_inv(tool), P.Finv[kGroup - 1]);
         int packed[TAMP_MAX_ROBOT_SPHERES];
         for (int s = 0; s < R.n_spheres; ++s) {
             const int l = R.sphere_link[s];
@@ -766,10 +777,10 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     }
     c->ik_iters = desc->ik_iters;
     c->ik_damping = desc->ik_damping;
-    if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 4 && desc->lanes_per_particle != 8 &&
-        desc->lanes_per_particle != 16) {
+    if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 1 && desc->lanes_per_particle != 4 &&
+        desc->lanes_per_particle != 8 && desc->lanes_per_particle != 16) {
         delete c;
-        return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 4, 8 or 16");
+        return fail(TAMP_E_INVALID, "lanes_per_particle must be 0, 1, 4, 8 or 16");
     }
     // auto: 8 lanes (one per link frame) -- measured faster than 16 on every config, even at 8K particles
     // (profiles/r1: the 16-lane mapping doubles the FK/kin instruction count for little latency gain)
@@ -781,6 +792,14 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         // waves when a 512-thread block (128 particles) fits shared memory (config 1 at 1M: +10 %);
         // 8 lanes elsewhere (sweeps 9, 13)
         c->gs = desc->lanes_per_particle ? desc->lanes_per_particle : (n_fk_real >= 24 ? 16 : 8);
+        // serial mapping (one thread per particle) for many particles of a small skeleton: no redundant
+        // per-particle work; config 1 at 64K-1M particles +27-34 % over the lane mappings (profiles/README.md),
+        // but 4x slower on the collision-heavy Tetris skeletons (D = 72), so only for small D
+        if (!desc->lanes_per_particle && n_local >= 65536 && c->P.D <= 32 && !c->P.has_self) {
+            bool held = false;
+            for (int f = 0; f < c->P.n_fk; ++f) held |= c->P.fk[f].held_grasp >= 0;
+            if (!held) c->gs = 1;
+        }
     }
     ws_layout(c);
     smem_layout(c);
@@ -792,7 +811,42 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         const bool many_waves = n_local > (int64_t)n_sm * 4 * (768 / 8);
         if (many_waves && 128 * c->stride_bytes + 4096 <= smem_optin) c->gs = 4;
     }
-    {
+    if (c->gs == 1) {
+        // serial mapping (particle_serial.cuh): one thread per particle, per-thread state in shared memory
+        bool held = false;
+        for (int f = 0; f < c->P.n_fk; ++f) held |= c->P.fk[f].held_grasp >= 0;
+        int smem_optin = 227 * 1024;
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        cudaGetLastError();
+        c->threads = desc->block_threads ? desc->block_threads : kSerialThreads;
+        if (c->threads % 32 || c->threads < 32 || c->threads > kSerialThreads) {
+            delete c;
+            return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 128] for 1 lane per particle");
+        }
+        // auto: the block size with the most resident warps per SM (shared memory holds the per-particle state)
+        if (!desc->block_threads) {
+            int smem_sm = 228 * 1024;
+            cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+            cudaGetLastError();
+            const int regs = std::max(32, serial_kernel_regs());
+            int best_w = -1;
+            for (int t = 32; t <= kSerialThreads; t += 32) {
+                const size_t sb = serial_smem_bytes(c->P, t, true) + 3 * 1024;   // + static smem, reserved
+                if (sb > (size_t)smem_optin + 3 * 1024) continue;
+                const int by_smem = (int)((size_t)smem_sm / sb);
+                const int by_regs = 65536 / (((regs + 7) & ~7) * t);
+                const int w = std::min(std::min(by_smem, by_regs), 32) * (t / 32);
+                if (w > best_w || (w == best_w && t > c->threads)) { best_w = w; c->threads = t; }
+            }
+        }
+        c->smem = serial_smem_bytes(c->P, c->threads, true);
+        if (c->P.has_self || held || c->smem + 4096 > (size_t)smem_optin) {
+            delete c;
+            return fail(TAMP_E_UNSUPPORTED, "1 lane per particle: no SELF term, no held objects at knots, and the "
+                                            "per-particle state must fit shared memory");
+        }
+        c->bsync = 0;
+    } else {
         // launch configuration of the particle kernel.  Auto: block-synchronous phases with one large block
         // per SM holding that SM's share of the particles (all warps of an SM walk the same code region ->
         // shared instruction cache), bounded by 768 threads and by shared memory.

@@ -373,12 +373,16 @@ cudaError_t launch_particle_sm(bool smooth, int mode, int gs, int bsync, int thr
                                size_t smem, cudaStream_t st);
 int particle_kernel_regs_sm(int gs);
 
-// gs = lanes per particle: 4 (two link frames per lane), 8 (one), 16 (two FK instances at a time);
+// gs = lanes per particle: 1 (serial mapping), 4 (two link frames per lane), 8 (one), 16 (two FK instances);
 // threads = block size (multiple of 32, <= 768); smem sized for threads / gs particles;
 // bsync = block-synchronisation level (see k_particle).
+cudaError_t launch_particle_serial(bool smooth, int mode, int threads, const KProgram& P, const KArgs& A,
+                                   cudaStream_t st);
+
 cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
                             cudaStream_t st) {
     if (A.n <= 0) return cudaSuccess;
+    if (gs == 1) return launch_particle_serial(P.smooth > 0.f, mode, threads, P, A, st);
     return launch_particle_sm(P.smooth > 0.f, mode, gs, bsync, threads, P, A, smem, st);
 }
 

@@ -77,6 +77,7 @@ struct KProgram {
     // robot: per lane l of a particle group, the fixed transform F_{l+1} (3x4 row-major; base folded
     // into F_1) or, for lane 7, the tool transform F_ee; and the spheres attached to that frame.
     float F[kGroup][12];
+    float Finv[kGroup][12];              // F^-1 of each (serial mapping: backward sweep over the links)
     float rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK][4];
     int32_t rsph_n[kGroup];
     float jlo[TAMP_NJ], jhi[TAMP_NJ];

@@ -51,9 +51,11 @@ def test_sampler_matches_oracle(cfg, grasp_mode):
     assert float(st["m"].abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("lanes", [4, 8, 16])
+@pytest.mark.parametrize("lanes", [1, 4, 8, 16])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
 def test_cost_and_gradient_match_oracle(cfg, lanes):
+    if lanes == 1 and cfg == 4:
+        pytest.skip("serial mapping: no held objects at knots (the library refuses it, test_serial_mapping_limits)")
     n = 97 if cfg != 4 else 40
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=10 + cfg)
     ctx = _ctx(spec, n, x32, g32, lanes=lanes)
@@ -71,9 +73,11 @@ def test_cost_and_gradient_match_oracle(cfg, lanes):
     assert ok.mean() > 0.85
 
 
-@pytest.mark.parametrize("lanes", [4, 8, 16])
+@pytest.mark.parametrize("lanes", [1, 4, 8, 16])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 6])
 def test_one_adam_step_matches_oracle(cfg, lanes):
+    if lanes == 1 and cfg == 4:
+        pytest.skip("serial mapping: no held objects at knots")
     n = 97 if cfg != 4 else 40
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=20 + cfg)
     ctx = _ctx(spec, n, x32, g32, n_global=1000, lanes=lanes)
@@ -95,7 +99,7 @@ def test_one_adam_step_matches_oracle(cfg, lanes):
     assert np.array_equal(st["grasp"].cpu().numpy(), g32.reshape(n, -1, 12))
 
 
-@pytest.mark.parametrize("lanes", [4, 8, 16])
+@pytest.mark.parametrize("lanes", [1, 4, 8, 16])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 6])
 def test_check_counts_and_classes_match_oracle(cfg, lanes):
     n = 301
@@ -445,3 +449,40 @@ def test_sampler_with_subgraph_streams_matches_oracle():
     x0, g0 = O.initialize_particles(spec, csp, 5, np.arange(gofs, gofs + n))
     np.testing.assert_allclose(st["x"].cpu().numpy(), x0, rtol=2e-6, atol=2e-6)
     np.testing.assert_allclose(st["grasp"].cpu().numpy(), g0.reshape(n, -1, 12), rtol=0, atol=2e-6)
+
+
+def test_serial_mapping_limits():
+    """The serial mapping (1 lane per particle) refuses what it does not implement -- the SELF term and held
+    objects at trajectory knots -- instead of computing something else."""
+    from paper_2411_11833_b200.tamp import TampError
+    spec = make_config(1, n=8)
+    spec.self_collision = True
+    with pytest.raises(TampError):
+        TampContext(spec, 8, lanes_per_particle=1)
+    with pytest.raises(TampError):
+        TampContext(make_config(4, n=8), 8, lanes_per_particle=1)
+    assert TampContext(make_config(1, n=8), 8, lanes_per_particle=1).lanes_per_particle == 1
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_serial_mapping_long_run_matches_lane_mapping(cfg):
+    """100 fused Adam steps with the serial and the 8-lane mapping from the same start: the same optimisation.
+    Per-particle trajectories separate where fp32 summation order tips a hinge / kink decision (the one-step
+    parity tests pin each step against the oracle), so this compares the populations: most particles agree
+    closely, the cost distribution and the satisfied counts match."""
+    n = 512
+    spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=60 + cfg)
+    outs = []
+    for lanes in (1, 8):
+        ctx = _ctx(spec, n, x32, g32, lanes=lanes)
+        ctx.optimize(100)
+        J, _, _, _ = ctx.eval()
+        counts, _ = ctx.check()
+        outs.append((J.cpu().numpy(), counts.cpu().numpy()))
+    (J1, c1), (J8, c8) = outs
+    close = np.abs(J1 - J8) <= 1e-3 * np.abs(J8) + 1e-4
+    assert close.mean() > (0.9 if cfg == 1 else 0.5)
+    for q in (0.25, 0.5, 0.75):
+        a, b = np.quantile(J1, q), np.quantile(J8, q)
+        assert abs(a - b) <= 0.05 * abs(b) + 1e-3
+    assert np.abs(c1.astype(np.int64) - c8).max() <= max(5, n // 20)
