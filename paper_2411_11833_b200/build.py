@@ -12,6 +12,10 @@ HDRS = [os.path.join(HERE, "csrc", "tamp_program.h"), os.path.join(HERE, "csrc",
         os.path.join(ROOT, "include", "tamp.h")]
 LIB = os.path.join(HERE, "libtamp.so")
 OBJ_DIR = os.path.join(HERE, "csrc", "build")
+# the particle kernels use the approximate (MUFU-based, ~1-2 ulp) fp32 division and square root: no slow-path
+# branches in the step loop; the parity tolerances (1e-4 relative cost) are orders of magnitude wider
+FAST_DIV_SQRT = ["-prec-div=false", "-prec-sqrt=false"]
+FAST_UNITS = ("tamp_particle_hinge.cu", "tamp_particle_smooth.cu", "tamp_particle_serial.cu")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
@@ -36,7 +40,8 @@ def build(force=False, verbose=False):
         return LIB
     os.makedirs(OBJ_DIR, exist_ok=True)
     objs = [os.path.join(OBJ_DIR, os.path.basename(s)[:-3] + ".o") for s in SRCS]
-    procs = [subprocess.Popen([nvcc()] + NVCC_FLAGS + ["-c", "-o", o, s], stdout=subprocess.PIPE,
+    procs = [subprocess.Popen([nvcc()] + NVCC_FLAGS + (FAST_DIV_SQRT if os.path.basename(s) in FAST_UNITS else [])
+                              + ["-c", "-o", o, s], stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True) for s, o in zip(SRCS, objs)]
     logs, failed = [], []
     for s, p in zip(SRCS, procs):
