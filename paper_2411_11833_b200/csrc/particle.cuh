@@ -391,8 +391,9 @@ __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, T
 // instances a particle group processes concurrently: 1, or 2 (two LPF-lane halves run the two FK instances
 // of a pair of identical structure).  GS = LPF * HP lanes per particle.
 // BSYNC: block-synchronous phases so that all warps of a block execute the same code region at a time and
-// share the instruction cache.  0 = off (warp-level only), 1 = at phase boundaries, 2 = also after every
-// FK instance.
+// share the instruction cache.  0 = off (warp-level only), 1 = one block barrier per step, after the FK loop
+// (every other phase boundary only needs its particle group, i.e. __syncwarp; measured best: barriers at
+// every phase boundary cost 3 %), 2 = also after every FK instance.
 // SMOOTH: CHOMP-smooth collision cost (compile-time so that the hinge kernels carry no extra state)
 template <int MODE, int LPF, int HP, int BSYNC, bool SMOOTH>
 __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                 for (int c = gl; c < 6; c += GS) iwr[8 * i + c] = 0.f;
         }
         if (GRAD) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
-        phase_sync();
+        __syncwarp();
 
         // ---- phase B: robot configurations (Pick/Place confs, knots) ----
         // HP = 2: the two halves process the two FK instances of a pair of identical structure concurrently
@@ -1011,7 +1012,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
 
         // ---- phase E: instance wrenches -> placement gradients ----
         if (GRAD) {
-            phase_sync();
+            __syncwarp();
             for (int i = 0; i < P.n_inst; ++i) {
                 const KInst& I = P.inst[i];
                 if (I.xoff < 0) continue;
@@ -1023,7 +1024,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                     gs[I.xoff + 3] += wr[5] - (tx * wr[1] - ty * wr[0]);
                 }
             }
-            phase_sync();
+            __syncwarp();
         }
 
         if (MODE == MODE_EVAL) {
@@ -1061,7 +1062,7 @@ __global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __gr
                     xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
                 }
             }
-            phase_sync();
+            __syncwarp();
         }
     }
 
