@@ -15,7 +15,7 @@ OBJ_DIR = os.path.join(HERE, "csrc", "build")
 # the particle kernels use the approximate (MUFU-based, ~1-2 ulp) fp32 division and square root: no slow-path
 # branches in the step loop; the parity tolerances (1e-4 relative cost) are orders of magnitude wider
 FAST_DIV_SQRT = ["-prec-div=false", "-prec-sqrt=false"]
-FAST_UNITS = ("tamp_particle_hinge.cu", "tamp_particle_smooth.cu", "tamp_particle_serial.cu")
+FAST_UNITS = ("tamp_particle_hinge.cu", "tamp_particle_smooth.cu", "tamp_particle_serial.cu", "tamp_kernels.cu")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
                     E[3 * i + j] = fmaf(Ts.r[3 * i], Tee.r[3 * j], fmaf(Ts.r[3 * i + 1], Tee.r[3 * j + 1], Ts.r[3 * i + 2] * Tee.r[3 * j + 2]));
             const float wx = E[7] - E[5], wy = E[2] - E[6], wz = E[3] - E[1];
             const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
-            const float th = atan2f(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
+            const float th = fatan2_pos(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
             const float k = wn > 0.f ? th / wn : 0.f;
             e[3] = wx * k; e[4] = wy * k; e[5] = wz * k;
             // Jacobian column of my joint
