@@ -395,8 +395,11 @@ __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, T
 // (every other phase boundary only needs its particle group, i.e. __syncwarp; measured best: barriers at
 // every phase boundary cost 3 %), 2 = also after every FK instance.
 // SMOOTH: CHOMP-smooth collision cost (compile-time so that the hinge kernels carry no extra state)
-template <int MODE, int LPF, int HP, int BSYNC, bool SMOOTH>
-__global__ void __launch_bounds__(LPF == 4 ? 512 : 768, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
+// MAXT: launch bound -- 768 (<= 80 registers: many resident warps for multi-wave launches) or 512 (<= 128
+// registers, no spills: single-wave launches of <= 512-thread blocks and the 16-lane mapping; +7 % on config 2,
+// +24 % on config 4)
+template <int MODE, int LPF, int HP, int BSYNC, bool SMOOTH, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     const float smooth = SMOOTH ? P.smooth : 0.f;
     constexpr int GS = LPF * HP;                                   // lanes per particle

@@ -30,7 +30,7 @@ cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int6
                           cudaStream_t st);
 cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
                       cudaStream_t st);
-int particle_kernel_regs(int gs);
+int particle_kernel_regs(int gs, int threads);
 int serial_kernel_regs();
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
                         cudaStream_t st, unsigned long long** kres, int32_t** pres);
@@ -856,13 +856,13 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         cudaGetLastError();
         const int ppw = 32 / c->gs;                                     // particles per warp
         const int static_smem = 4096;
-        const int max_threads = c->gs == 4 ? 512 : 768;                // __launch_bounds__ of the variant
+        const int max_threads = c->gs == 8 ? 768 : 512;                // __launch_bounds__ of the variants
         int max_pp = std::min(max_threads / c->gs, (smem_optin - static_smem) / c->stride_bytes);
         max_pp = (max_pp / ppw) * ppw;
         if (desc->block_threads) {
             if (desc->block_threads % 32 || desc->block_threads < 32 || desc->block_threads > max_threads) {
                 delete c;
-                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 768] (512 for 4 lanes)");
+                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 768] (512 for 4 / 16 lanes)");
             }
             c->threads = desc->block_threads;
         } else {
@@ -878,8 +878,8 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             if (pp <= max_pp) {
                 c->threads = (int)std::min<int64_t>(std::max<int64_t>(pp, 4 * ppw), std::max(max_pp, ppw)) * c->gs;
             } else {
-                const int regs = std::max(32, particle_kernel_regs(c->gs));
                 auto blocks_per_sm = [&](int t) {
+                    const int regs = std::max(32, particle_kernel_regs(c->gs, t));   // variant run by t threads
                     const int ppb = t / c->gs;
                     const int by_regs = 65536 / (((regs + 7) & ~7) * t);
                     const int by_smem = (smem_optin + 1024) / (ppb * c->stride_bytes + static_smem + 1024);

@@ -371,7 +371,7 @@ static inline void counted() { note_launch(); }
 
 cudaError_t launch_particle_sm(bool smooth, int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A,
                                size_t smem, cudaStream_t st);
-int particle_kernel_regs_sm(int gs);
+int particle_kernel_regs_sm(int gs, int threads);
 
 // gs = lanes per particle: 1 (serial mapping), 4 (two link frames per lane), 8 (one), 16 (two FK instances);
 // threads = block size (multiple of 32, <= 768); smem sized for threads / gs particles;
@@ -387,7 +387,7 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
 }
 
 // registers per thread of the hot kernel (for the launch-configuration policy)
-int particle_kernel_regs(int gs) { return particle_kernel_regs_sm(gs); }
+int particle_kernel_regs(int gs, int threads) { return particle_kernel_regs_sm(gs, threads); }
 
 cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
                       cudaStream_t st) {

@@ -1,54 +1,26 @@
-// tamp_particle_hinge.cu -- instantiations of k_particle with the hinge collision cost
-// (split from tamp_kernels.cu so the instantiations compile in parallel).
-#include "particle.cuh"
+// tamp_particle_hinge.cu -- k_particle with the hinge collision cost: 8 lanes, 768-thread bound (multi-wave
+// launches) and 4 lanes (split from tamp_kernels.cu so the instantiations compile in parallel).
+#include "particle_launch.cuh"
 
 namespace tamp {
-void note_launch();
-static inline void counted() { note_launch(); }
 
-template <int MODE, int LPF, int HP, int BSYNC, bool SM>
-static cudaError_t launch_particle_t(const KProgram& P, const KArgs& A, int threads, size_t smem, cudaStream_t st) {
-    auto fn = k_particle<MODE, LPF, HP, BSYNC, SM>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int per_block = threads / (LPF * HP);
-    const int64_t blocks = (A.n + per_block - 1) / per_block;
-    fn<<<(unsigned)blocks, threads, smem, st>>>(P, A);
-    counted();
-    return cudaGetLastError();
-}
+cudaError_t launch_particle_hinge_rich(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A,
+                                       size_t smem, cudaStream_t st);
+int particle_regs_hinge_rich(int gs);
 
-template <int LPF, int HP, bool SM>
-static cudaError_t launch_particle_map(int mode, int bsync, const KProgram& P, const KArgs& A, int threads, size_t smem,
-                                       cudaStream_t st) {
-    if (mode == MODE_EVAL) return launch_particle_t<MODE_EVAL, LPF, HP, 2, SM>(P, A, threads, smem, st);
-    if (mode == MODE_CHECK) {
-        if (bsync == 0) return launch_particle_t<MODE_CHECK, LPF, HP, 0, SM>(P, A, threads, smem, st);
-        if (bsync == 1) return launch_particle_t<MODE_CHECK, LPF, HP, 1, SM>(P, A, threads, smem, st);
-        return launch_particle_t<MODE_CHECK, LPF, HP, 2, SM>(P, A, threads, smem, st);
-    }
-    switch (bsync) {
-        case 0: return launch_particle_t<MODE_OPT, LPF, HP, 0, SM>(P, A, threads, smem, st);
-        case 1: return launch_particle_t<MODE_OPT, LPF, HP, 1, SM>(P, A, threads, smem, st);
-        default: return launch_particle_t<MODE_OPT, LPF, HP, 2, SM>(P, A, threads, smem, st);
-    }
-}
-
-
+// 16 lanes, and 8 lanes in blocks of <= 512 threads: the 512-thread-bound (register-rich) instantiations
 cudaError_t launch_particle_hinge(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A,
-                                 size_t smem, cudaStream_t st) {
-    if (gs == 16) return launch_particle_map<8, 2, false>(mode, bsync, P, A, threads, smem, st);
-    if (gs == 4) return launch_particle_map<4, 1, false>(mode, bsync, P, A, threads, smem, st);
-    return launch_particle_map<8, 1, false>(mode, bsync, P, A, threads, smem, st);
+                                  size_t smem, cudaStream_t st) {
+    if (gs == 16 || (gs == 8 && threads <= 512)) return launch_particle_hinge_rich(mode, gs, bsync, threads, P, A, smem, st);
+    if (gs == 4) return launch_particle_map<4, 1, false, 512>(mode, bsync, P, A, threads, smem, st);
+    return launch_particle_map<8, 1, false, 768>(mode, bsync, P, A, threads, smem, st);
 }
 
-int particle_kernel_regs_sm(int gs) {
-    cudaFuncAttributes a;
-    cudaError_t e = gs == 16 ? cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 8, 2, 1, false>)
-                  : gs == 4  ? cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 4, 1, 1, false>)
-                             : cudaFuncGetAttributes(&a, k_particle<MODE_OPT, 8, 1, 1, false>);
-    if (e != cudaSuccess) { cudaGetLastError(); return 80; }
-    return a.numRegs;
+// registers per thread of the variant a block of `threads` threads would run (launch-configuration policy)
+int particle_kernel_regs_sm(int gs, int threads) {
+    if (gs == 16 || (gs == 8 && threads <= 512)) return particle_regs_hinge_rich(gs);
+    if (gs == 4) return particle_regs_t<4, 1, false, 512>();
+    return particle_regs_t<8, 1, false, 768>();
 }
 
 cudaError_t launch_particle_smooth(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A,
