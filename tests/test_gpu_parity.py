@@ -309,6 +309,26 @@ def test_launch_configuration_invariance_bit_exact(lanes):
             assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1])
 
 
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_register_budget_variants_bit_exact(cfg):
+    """8 lanes: blocks of <= 512 threads run the 512-bound (register-rich) instantiation, larger blocks the
+    768-bound one -- same arithmetic, bit-identical results."""
+    spec = make_config(cfg, n=600)
+    ref = None
+    for threads in (256, 640):
+        c = TampContext(spec, 600, lanes_per_particle=8, block_threads=threads, block_sync=1)
+        c.sample(seed=9)
+        c.optimize(5)
+        counts, _ = c.check()
+        J, _, _, g = c.eval()
+        out = [c.get_state()["x"].cpu().numpy(), counts.cpu().numpy(), J.cpu().numpy(), g.cpu().numpy()]
+        if ref is None:
+            ref = out
+        else:
+            for a, b in zip(out, ref):
+                assert np.array_equal(a, b)
+
+
 def test_long_launch_is_split_and_matches_short_launches():
     """n_steps > 64 per call is split into launches of <= 64 fused steps with identical results."""
     spec = make_config(1, n=64)
