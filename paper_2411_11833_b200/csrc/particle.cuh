@@ -162,10 +162,11 @@ __device__ __forceinline__ float smooth_cost(float p, float s, float& gsc) {
 template <bool GRAD>
 __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float rr, const KObb& B, float lam,
                                             float& gx, float& gy, float& gz, float smooth = 0.f) {
+    // boxes are yawed about the world z axis (tamp_obb_desc): R = Rz(yaw), p = R^T (w - c)
     const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
-    const float px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
-    const float py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
-    const float pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
+    const float px = fmaf(B.R[0], dx, B.R[3] * dy);
+    const float py = fmaf(B.R[1], dx, B.R[4] * dy);
+    const float pz = dz;
     const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(pz) - B.h[2];
     const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
     const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
@@ -194,9 +195,9 @@ __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float 
     pen = smooth_cost(pen, smooth, gsc);
     lam *= gsc;
     if (GRAD) {   // dJ/dw = -R grad_p
-        gx = fmaf(-lam, fmaf(B.R[0], gpx, fmaf(B.R[1], gpy, B.R[2] * gpz)), gx);
-        gy = fmaf(-lam, fmaf(B.R[3], gpx, fmaf(B.R[4], gpy, B.R[5] * gpz)), gy);
-        gz = fmaf(-lam, fmaf(B.R[6], gpx, fmaf(B.R[7], gpy, B.R[8] * gpz)), gz);
+        gx = fmaf(-lam, fmaf(B.R[0], gpx, B.R[1] * gpy), gx);
+        gy = fmaf(-lam, fmaf(B.R[3], gpx, B.R[4] * gpy), gy);
+        gz = fmaf(-lam, gpz, gz);
     }
     return pen;
 }
@@ -314,10 +315,9 @@ __device__ __forceinline__ float spheres_vs_obb(const float (&w)[NS][3], const f
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
-        const float px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
-        const float py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
-        const float pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
-        const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(pz) - B.h[2];
+        const float px = fmaf(B.R[0], dx, B.R[3] * dy);
+        const float py = fmaf(B.R[1], dx, B.R[4] * dy);
+        const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(dz) - B.h[2];
         const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
         const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
         const float mx = fmaxf(ax, fmaxf(ay, az));

@@ -57,7 +57,7 @@ struct KTraj {
 };
 
 struct KSurface { float frame[4]; float lo[2], hi[2]; };
-struct KObb { float R[9]; float c[3]; float h[3]; float rad; };   // rad = |h| (bounding sphere)
+struct KObb { float R[9]; float c[3]; float h[3]; float rad; };   // R = Rz(yaw) (the kernels rely on it); rad = |h|
 
 struct KProgram {
     int32_t D, n_terms, n_fk, n_inst, n_place, n_traj, n_goal, n_grasp, n_obb;
