@@ -74,17 +74,30 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
     const SerialLayout L = serial_layout(P, MODE == MODE_OPT);
     const int D = P.D;
     const int PITCH = NT + 1;
-    auto col = [&](int f) -> float& { return S[(size_t)f * PITCH + tid]; };
+    auto col = [&](int f) -> float& { return S[f * PITCH + tid]; };
     // block-cooperative, coalesced copy between the block's rows of a [n][w] array and columns c0..c0+w
     const int64_t row0 = (int64_t)blockIdx.x * NT;
     const int nrows = (int)min((int64_t)NT, A.n - row0);
+    // element e = row * w + c of the block's rows; (row, c) advanced incrementally (no division per element)
     auto load_rows = [&](const float* src, int w, int c0) {
         const float* base = src + row0 * w;
-        for (int e = tid; e < nrows * w; e += NT) S[(size_t)(c0 + e % w) * PITCH + e / w] = base[e];
+        const int dq = NT / w, dr = NT % w;
+        int q = tid / w, r = tid % w;
+        for (int e = tid; e < nrows * w; e += NT) {
+            S[(c0 + r) * PITCH + q] = base[e];
+            q += dq; r += dr;
+            if (r >= w) { r -= w; ++q; }
+        }
     };
     auto store_rows = [&](float* dst, int w, int c0) {
         float* base = dst + row0 * w;
-        for (int e = tid; e < nrows * w; e += NT) base[e] = S[(size_t)(c0 + e % w) * PITCH + e / w];
+        const int dq = NT / w, dr = NT % w;
+        int q = tid / w, r = tid % w;
+        for (int e = tid; e < nrows * w; e += NT) {
+            base[e] = S[(c0 + r) * PITCH + q];
+            q += dq; r += dr;
+            if (r >= w) { r -= w; ++q; }
+        }
     };
     auto xs = [&](int d) -> float& { return col(L.x + d); };
     auto gs = [&](int d) -> float& { return col(L.g + d); };
@@ -95,9 +108,14 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
         iw(i, 3) += w.m[0]; iw(i, 4) += w.m[1]; iw(i, 5) += w.m[2];
     };
 
+    __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];
     for (int i = tid; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += NT) {
         const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
         s_osph[o][k] = make_float4(P.osph[o][k][0], P.osph[o][k][1], P.osph[o][k][2], P.osph[o][k][3]);
+    }
+    for (int i = tid; i < kGroup * TAMP_MAX_SPHERES_PER_LINK; i += NT) {
+        const int l = i / TAMP_MAX_SPHERES_PER_LINK, k = i % TAMP_MAX_SPHERES_PER_LINK;
+        s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3] + P.eta);
     }
     if (MODE == MODE_CHECK)
         for (int i = tid; i < P.n_terms + 2; i += NT) s_counts[i] = 0;
@@ -277,15 +295,30 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
             // backward sweep over the links 8 -> 1: spheres of link l in T_l, suffix wrench, dJ/dq_l
             const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
             float jcf = 0.f;
+            // one box to test (the table): its data in registers for the whole configuration
+            const bool one_obb = K.obb_mask != 0 && (K.obb_mask & (K.obb_mask - 1)) == 0;
+            KObb B0;
+            if (one_obb) B0 = P.obb[__ffs(K.obb_mask) - 1];
 #pragma unroll 1
             for (int l = kGroup - 1; l >= 0; --l) {
                 if (K.term_cf >= 0) {
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
+                        const float4 c4 = s_rsph[l][k];
                         float wx, wy, wz;
-                        xform(T, P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], wx, wy, wz);
-                        const float rr = P.rsph[l][k][3] + P.eta;
+                        xform(T, c4.x, c4.y, c4.z, wx, wy, wz);
+                        const float rr = c4.w;
                         float g[3] = {0.f, 0.f, 0.f};
-                        jcf += sphere_vs_obbs(wx, wy, wz, rr, K.obb_mask, lam_cf, g);
+                        if (one_obb) {
+                            bool near = true;
+                            if (B0.rad < kBroadMaxRad) {
+                                const float dx = wx - B0.c[0], dy = wy - B0.c[1], dz = wz - B0.c[2];
+                                const float R = rr + B0.rad;
+                                near = fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f;
+                            }
+                            if (near) jcf += sphere_obb<GRAD>(wx, wy, wz, rr, B0, lam_cf, g[0], g[1], g[2], smooth);
+                        } else {
+                            jcf += sphere_vs_obbs(wx, wy, wz, rr, K.obb_mask, lam_cf, g);
+                        }
                         for (int pi = 0; pi < K.part_count; ++pi) {
                             const int ii = P.partners[K.part_begin + pi];
                             Wrench pw;
