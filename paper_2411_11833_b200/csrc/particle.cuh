@@ -33,6 +33,23 @@ __device__ __forceinline__ M34 compose(const M34& a, const M34& b) {
     return c;
 }
 
+// T(p) T(g) for a placement T(p) = (Rz(yaw), t) stored as the 3x4 rows of ipose (cos at [0], sin at [4]):
+// rows 0 / 1 of the rotation mix, row 2 is T(g)'s
+__device__ __forceinline__ M34 compose_rz(const float* ip, const M34& b) {
+    const float c = ip[0], s = ip[4];
+    M34 o;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        o.r[j] = fmaf(c, b.r[j], -s * b.r[3 + j]);
+        o.r[3 + j] = fmaf(s, b.r[j], c * b.r[3 + j]);
+        o.r[6 + j] = b.r[6 + j];
+    }
+    o.t[0] = fmaf(c, b.t[0], fmaf(-s, b.t[1], ip[3]));
+    o.t[1] = fmaf(s, b.t[0], fmaf(c, b.t[1], ip[7]));
+    o.t[2] = b.t[2] + ip[11];
+    return o;
+}
+
 __device__ __forceinline__ M34 shfl_m34(const M34& a, int src, int width = kGroup) {
     M34 o;
 #pragma unroll
@@ -693,10 +710,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
 
             // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the segment
             if (K.term_kp >= 0 || K.term_kr >= 0) {
-                M34 Tp, Tg;
-                load_m34(Tp, ipose + 16 * K.kin_inst);
+                M34 Tg;
                 load_m34(Tg, gT + 16 * K.kin_grasp);
-                const M34 Ts = compose(Tp, Tg);
+                const M34 Ts = compose_rz(ipose + 16 * K.kin_inst, Tg);
                 // position error e = ||t_ee - t*||  (L5)
                 const float dx = Tee.t[0] - Ts.t[0], dy = Tee.t[1] - Ts.t[1], dz = Tee.t[2] - Ts.t[2];
                 const float e2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));

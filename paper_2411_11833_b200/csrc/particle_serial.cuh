@@ -235,17 +235,14 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
             // Kin(q, o, g, p): FK(q) = T(p) T(g) at the tool frame
             if (K.term_kp >= 0 || K.term_kr >= 0) {
                 const int ki = K.kin_inst;
-                M34 Tp, Tg;
-                Tp.r[0] = ip(ki, 0); Tp.r[1] = -ip(ki, 1); Tp.r[2] = 0.f;
-                Tp.r[3] = ip(ki, 1); Tp.r[4] = ip(ki, 0); Tp.r[5] = 0.f;
-                Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f;
-                Tp.t[0] = ip(ki, 2); Tp.t[1] = ip(ki, 3); Tp.t[2] = ip(ki, 4);
+                M34 Tg;
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
                     const int b = L.gT + 12 * K.kin_grasp + 4 * i;
                     Tg.r[3 * i] = col(b); Tg.r[3 * i + 1] = col(b + 1); Tg.r[3 * i + 2] = col(b + 2); Tg.t[i] = col(b + 3);
                 }
-                const M34 Ts = compose(Tp, Tg);
+                const float ipk[12] = {ip(ki, 0), 0.f, 0.f, ip(ki, 2), ip(ki, 1), 0.f, 0.f, ip(ki, 3), 0.f, 0.f, 0.f, ip(ki, 4)};
+                const M34 Ts = compose_rz(ipk, Tg);   // T(p) T(g), T(p) = (Rz(yaw), t)
                 const float dx = T.t[0] - Ts.t[0], dy = T.t[1] - Ts.t[1], dz = T.t[2] - Ts.t[2];
                 const float epos = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                 float Mm[9];
