@@ -870,8 +870,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             }
             // containment: sum over spheres of dist_from_bounds(xy in surface frame, lo + r, hi - r)
             if (Q.term_sc >= 0) {
-                float sy, cy;
-                fsincos(Sf.frame[3], &sy, &cy);
+                const float sy = Sf.sy, cy = Sf.cy;
                 float e = 0.f;
 #pragma unroll
                 for (int u = 0; u < NSO; ++u) {
@@ -898,8 +897,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             // dist_from_bounds(xy in the face frame, lo, hi); the subgradient goes to the arg-min sphere
             // (lowest index on ties)
             if (Q.term_pc >= 0) {
-                float sy, cy;
-                fsincos(Sf.frame[3], &sy, &cy);
+                const float sy = Sf.sy, cy = Sf.cy;
                 float emin = kFar, glx_min = 0.f, gly_min = 0.f;
                 int kmin = TAMP_MAX_OBJ_SPHERES;
 #pragma unroll

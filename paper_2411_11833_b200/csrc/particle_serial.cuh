@@ -377,8 +377,7 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
                 serial_term<MODE>(P, A, sink, Q.term_ss, e, active, p, s_counts);
                 if (GRAD && e > 0.f) own.add_point(ip(ii, 2), ip(ii, 3), pz, 0.f, 0.f, P.term_lam[Q.term_ss] * (pz > Sf.frame[2] ? 1.f : -1.f));
             }
-            float sy, cy;
-            fsincos(Sf.frame[3], &sy, &cy);
+            const float sy = Sf.sy, cy = Sf.cy;
             if (Q.term_sc >= 0) {   // containment: sum over spheres of dist_from_bounds(xy, lo + r, hi - r)
                 float e = 0.f;
                 for (int k = 0; k < no; ++k) {

@@ -293,6 +293,8 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         REQUIRE(S.lo[0] <= S.hi[0] && S.lo[1] <= S.hi[1], TAMP_E_INVALID, "surface lo must be <= hi");
         REQUIRE(S.support_obb < d.n_obb && S.support_obj < d.n_objects, TAMP_E_INVALID, "surface support out of range");
         for (int k = 0; k < 4; ++k) P.surf[s].frame[k] = S.frame[k];
+        P.surf[s].cy = (float)cos((double)S.frame[3]);
+        P.surf[s].sy = (float)sin((double)S.frame[3]);
         for (int k = 0; k < 2; ++k) { P.surf[s].lo[k] = S.lo[k]; P.surf[s].hi[k] = S.hi[k]; }
     }
 

@@ -56,7 +56,7 @@ struct KTraj {
     int16_t knot_xoff, n_knots;
 };
 
-struct KSurface { float frame[4]; float lo[2], hi[2]; };
+struct KSurface { float frame[4]; float lo[2], hi[2]; float cy, sy; };   // cy, sy: cos / sin of the frame yaw
 struct KObb { float R[9]; float c[3]; float h[3]; float rad; };   // R = Rz(yaw) (the kernels rely on it); rad = |h|
 
 struct KProgram {
