@@ -405,7 +405,7 @@ def main():
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinstr/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_unit": "bytes per launch (ncu, profiles/ncu_traffic.json)",
             "algorithmic_bytes_per_launch": n * (2 * 3 * ctx.D * 4 + 48 * ctx.n_grasp),
-            "kernel": "k_particle<MODE_OPT>",
+            "kernel": "k_serial<MODE_OPT>" if ctx.lanes_per_particle == 1 else "k_particle<MODE_OPT>",
             "note": f"FP32-pipe instructions (FFMA=1) of the minimal per-unit evaluation, {instr} per particle-step; "
                     f"peak = {nsm} SM x 128 lanes x {sm_max:.0f} MHz ({src} sm_max_mhz)"}
     if clocks:
