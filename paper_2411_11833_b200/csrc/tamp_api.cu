@@ -176,6 +176,63 @@ static void count_pairs(const tamp_problem_desc& d, Compiled& C) {
         if (!(cond)) return fail(st, msg);        \
     } while (0)
 
+// Every index the kernels dereference, checked against its array once per compile (defence in depth: the
+// kernels do no bounds checks in the step loop, and compute-sanitizer is not available on the GPU pool).
+static tamp_status check_program(const KProgram& P, const KSampleProgram& SP) {
+    auto term_ok = [&](int t) { return t == -1 || (t >= 0 && t < P.n_terms); };
+    auto conf_ok = [&](int xoff) { return xoff >= 0 && xoff + TAMP_NJ <= P.D; };
+    auto inst_ok = [&](int i) { return i >= 0 && i < P.n_inst; };
+    auto grasp_ok = [&](int g) { return g >= 0 && g < P.n_grasp; };
+    auto partners_ok = [&](int b, int n) {
+        if (b < 0 || n < 0 || b + n > kMaxPartners) return false;
+        for (int k = 0; k < n; ++k) if (!inst_ok(P.partners[b + k])) return false;
+        return true;
+    };
+    const uint32_t obb_all = (1u << P.n_obb) - 1u;
+    REQUIRE(P.n_terms >= 0 && P.n_terms <= TAMP_MAX_TERMS && P.n_fk <= TAMP_MAX_FK && P.n_inst <= kMaxInst &&
+            P.n_place <= kMaxPlace && P.n_traj <= kMaxTraj && P.D <= TAMP_MAX_D && P.n_grasp <= TAMP_MAX_GRASPS,
+            TAMP_E_UNSUPPORTED, "internal: program sizes out of range");
+    for (int f = 0; f < P.n_fk; ++f) {
+        const KFk& K = P.fk[f];
+        REQUIRE(conf_ok(K.xoff) && term_ok(K.term_jl) && term_ok(K.term_cf) && term_ok(K.term_kp) &&
+                term_ok(K.term_kr) && term_ok(K.term_self) && (K.obb_mask & ~obb_all) == 0 &&
+                partners_ok(K.part_begin, K.part_count), TAMP_E_INVALID, "internal: configuration entry out of range");
+        if (K.term_kp >= 0 || K.term_kr >= 0)
+            REQUIRE(inst_ok(K.kin_inst) && grasp_ok(K.kin_grasp), TAMP_E_INVALID, "internal: Kin target out of range");
+        if (K.held_grasp >= 0)
+            REQUIRE(grasp_ok(K.held_grasp) && K.held_obj >= 0 && K.held_obj < TAMP_MAX_OBJECTS, TAMP_E_INVALID,
+                    "internal: held object out of range");
+    }
+    for (int i = 0; i < P.n_inst; ++i) {
+        const KInst& I = P.inst[i];
+        REQUIRE(I.obj >= 0 && I.obj < TAMP_MAX_OBJECTS && (I.xoff < 0 || I.xoff + 4 <= P.D), TAMP_E_INVALID,
+                "internal: object instance out of range");
+    }
+    for (int q = 0; q < P.n_place; ++q) {
+        const KPlace& Q = P.place[q];
+        REQUIRE(inst_ok(Q.inst) && P.inst[Q.inst].xoff >= 0 && term_ok(Q.term_ss) && Q.term_ss >= 0 &&
+                term_ok(Q.term_sc) && term_ok(Q.term_cp) && term_ok(Q.term_pc) && Q.surface >= 0 &&
+                Q.surface < TAMP_MAX_SURFACES && (Q.obb_mask & ~obb_all) == 0 && partners_ok(Q.part_begin, Q.part_count),
+                TAMP_E_INVALID, "internal: place / press entry out of range");
+    }
+    for (int t = 0; t < P.n_traj; ++t) {
+        const KTraj& Tj = P.traj[t];
+        REQUIRE((Tj.q1_xoff >= 0 ? conf_ok(Tj.q1_xoff) : (Tj.q1_const >= 0 && Tj.q1_const < kMaxConstConf)) &&
+                (Tj.q2_xoff >= 0 ? conf_ok(Tj.q2_xoff) : (Tj.q2_const >= 0 && Tj.q2_const < kMaxConstConf)) &&
+                Tj.n_knots >= 1 && Tj.knot_xoff >= 0 && Tj.knot_xoff + TAMP_NJ * Tj.n_knots <= P.D,
+                TAMP_E_INVALID, "internal: trajectory entry out of range");
+    }
+    for (int k = 0; k < P.n_goal; ++k) REQUIRE(inst_ok(P.goal_inst[k]), TAMP_E_INVALID, "internal: goal out of range");
+    for (int v = 0; v < SP.n_vars; ++v) {
+        const KSVar& V = SP.v[v];
+        if (V.kind == KS_GRASP) REQUIRE(grasp_ok(V.slot), TAMP_E_INVALID, "internal: sampler grasp slot out of range");
+        else if (V.kind == KS_PLACEMENT) REQUIRE(V.xoff >= 0 && V.xoff + 4 <= P.D, TAMP_E_INVALID, "internal: sampler placement");
+        else if (V.kind == KS_CONF) REQUIRE(conf_ok(V.xoff), TAMP_E_INVALID, "internal: sampler conf out of range");
+        else REQUIRE(V.xoff >= 0 && V.xoff + TAMP_NJ * V.n_knots <= P.D, TAMP_E_INVALID, "internal: sampler knots");
+    }
+    return TAMP_OK;
+}
+
 static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compiled& C) {
     std::memset(&C.P, 0, sizeof(C.P));
     std::memset(&C.SP, 0, sizeof(C.SP));
@@ -620,7 +677,7 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
     }
     SP.n_vars = ns;
     count_pairs(d, C);
-    return TAMP_OK;
+    return check_program(C.P, C.SP);
 }
 
 // shared-memory layout of the particle kernel

@@ -6,7 +6,7 @@ from workloads import make_config
 from paper_2411_11833_b200 import TampContext
 
 torch.cuda.set_device(0)
-for cfg, lanes, selfc in [(1, 8, False), (2, 16, True), (4, 4, False), (3, 8, False)]:
+for cfg, lanes, selfc in [(1, 8, False), (2, 16, True), (4, 4, False), (3, 8, False), (1, 1, False), (6, 8, False)]:
     spec = make_config(cfg, n=40)
     spec.ik_iters = 3
     spec.self_collision = selfc
