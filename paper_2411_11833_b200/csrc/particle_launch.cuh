@@ -35,12 +35,15 @@ static cudaError_t launch_particle_map(int mode, int bsync, const KProgram& P, c
 
 template <int LPF, int HP, bool SM, int MAXT>
 static int particle_regs_t() {
+    static int cached = 0;   // a property of the loaded module: queried once per process
+    if (cached) return cached;
     cudaFuncAttributes a;
     if (cudaFuncGetAttributes(&a, k_particle<MODE_OPT, LPF, HP, 1, SM, MAXT>) != cudaSuccess) {
         cudaGetLastError();
         return MAXT == 512 ? 128 : 80;
     }
-    return a.numRegs;
+    cached = a.numRegs;
+    return cached;
 }
 
 }  // namespace tamp

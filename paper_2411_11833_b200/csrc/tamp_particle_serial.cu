@@ -30,9 +30,12 @@ cudaError_t launch_particle_serial(bool smooth, int mode, int threads, const KPr
 }
 
 int serial_kernel_regs() {
+    static int cached = 0;
+    if (cached) return cached;
     cudaFuncAttributes a;
     if (cudaFuncGetAttributes(&a, k_serial<MODE_OPT, false>) != cudaSuccess) { cudaGetLastError(); return 128; }
-    return a.numRegs;
+    cached = a.numRegs;
+    return cached;
 }
 
 }  // namespace tamp

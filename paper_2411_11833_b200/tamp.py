@@ -152,6 +152,14 @@ def _check(status: int):
 # ---------------------------------------------------------------------------------------------
 # ProblemSpec (workloads/) -> tamp_problem_desc marshalling
 # ---------------------------------------------------------------------------------------------
+def _copy_floats(dst, values: np.ndarray):
+    """Copy a contiguous float32 vector into the leading elements of a (nested) ctypes float array."""
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    if v.nbytes > ctypes.sizeof(dst):
+        raise ValueError("descriptor array too small")
+    ctypes.memmove(ctypes.addressof(dst), v.ctypes.data, v.nbytes)
+
+
 def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block_threads: int = 0,
                block_sync: int = -1) -> ProblemDesc:
     d = ProblemDesc()
@@ -166,13 +174,15 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
     for k in range(4):
         d.robot.base[k] = float(r.base[k])
     d.robot.n_spheres = len(r.spheres)
+    _copy_floats(d.robot.sphere, np.asarray(r.spheres, dtype=np.float32).reshape(-1))
     for s in range(len(r.spheres)):
-        for k in range(4):
-            d.robot.sphere[s][k] = float(r.spheres[s][k])
         d.robot.sphere_link[s] = int(r.sphere_link[s])
+    masks = [0] * len(r.spheres)
     for i, j in getattr(r, "self_pairs", []):
-        d.robot.self_mask[i] |= 1 << j
-        d.robot.self_mask[j] |= 1 << i
+        masks[i] |= 1 << j
+        masks[j] |= 1 << i
+    for i, m in enumerate(masks):
+        d.robot.self_mask[i] = m
     d.n_obb = len(spec.obbs)
     for b, o in enumerate(spec.obbs):
         for k in range(3):
@@ -182,9 +192,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
     d.n_objects = len(spec.objects)
     for i, o in enumerate(spec.objects):
         d.object[i].n_spheres = len(o.spheres)
-        for s in range(len(o.spheres)):
-            for k in range(4):
-                d.object[i].sphere[s][k] = float(o.spheres[s][k])
+        _copy_floats(d.object[i].sphere, np.asarray(o.spheres, dtype=np.float32).reshape(-1))
         d.object[i].footprint = float(o.footprint)
         d.object[i].grasp_xy = float(o.grasp_xy)
         d.object[i].grasp_z = float(o.grasp_z)
