@@ -531,3 +531,34 @@ def test_ten_adam_steps_match_oracle(cfg, lanes):
     _, counts_o, *_ = O.check(spec, csp, so)
     diff = np.abs(counts.cpu().numpy().astype(np.int64) - counts_o)
     assert diff.max() <= (~follow).sum() + 1
+
+
+def test_abi_error_behaviour():
+    """Call order and argument errors return a status with a message, never abort; the
+    context stays usable afterwards."""
+    from paper_2411_11833_b200.tamp import TampError
+    spec = make_config(1, n=16)
+    ctx = TampContext(spec, 16)
+    for call in (lambda: ctx.optimize(1), lambda: ctx.check(), lambda: ctx.best_k(2), lambda: ctx.eval()):
+        with pytest.raises(TampError, match="E_STATE"):
+            call()
+    ctx.sample(seed=1)
+    with pytest.raises(TampError, match="E_INVALID"):
+        ctx.optimize(-1)
+    ctx.optimize(0)                                         # no-op
+    assert ctx.t == 0
+    for k in (0, 17, 2000):
+        with pytest.raises(TampError, match="E_INVALID"):
+            ctx.best_k(k)
+    rec = ctx.best_k(4)
+    with pytest.raises(TampError, match="E_INVALID"):
+        ctx.merge_best_k(rec, 5)                            # k > records
+    ctx.optimize(3)
+    counts, _ = ctx.check()
+    assert ctx.t == 3 and int(counts[:-2].min()) >= 0
+    with pytest.raises(TampError):
+        TampContext(spec, 0)                                # no particles
+    with pytest.raises(TampError, match="E_INVALID"):
+        TampContext(spec, 16, lanes_per_particle=3)
+    with pytest.raises(TampError, match="E_INVALID"):
+        TampContext(spec, 16, lanes_per_particle=8, block_threads=100)
