@@ -169,10 +169,14 @@ typedef struct {
     float beta1, beta2, adam_eps;         /* Adam (L9) */
     float lr_conf, lr_pos, lr_yaw, lr_knot;
     float grad_scale;                     /* <= 0: use 1 / n_global (Eq. 4) */
-    int32_t lanes_per_particle;           /* kernel mapping: 8 or 16 lanes per particle; 0 = auto */
-    int32_t block_threads;                /* particle-kernel block size (multiple of 32, <= 768); 0 = auto */
-    int32_t block_sync;                   /* block-synchronous phases: 0 off, 1 phase boundaries, 2 + every
-                                             FK instance, 3 + inside the FK body; -1 auto (2) */
+    int32_t lanes_per_particle;           /* kernel mapping (schedule only; results agree to fp32 rounding):
+                                             1 = one thread per particle (serial mapping, no SELF / held objects),
+                                             4 / 8 = lanes per configuration's link frames, 16 = two
+                                             configurations at a time; 0 = auto */
+    int32_t block_threads;                /* particle-kernel block size (multiple of 32, <= 768; <= 512 for 4 / 16
+                                             lanes, <= 128 for 1); 0 = auto */
+    int32_t block_sync;                   /* block barriers of the link mappings: 0 none, 1 one per step after
+                                             the configuration loop, 2 + after every configuration; -1 auto (1) */
     int32_t self_collision;               /* 1: add a SELF term after every CF term */
     int32_t collision_smooth;             /* 1: CHOMP-smooth collision cost instead of the hinge:
                                              p - eta/2 (p > eta), p^2/(2 eta) (0 < p <= eta), p = r + eta - sd;

@@ -826,9 +826,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             }
             // keep the block's warps in step through the (large) FK loop body (profiles/README.md):
             // every FK instance (2) or every other one (3)
-            if (BSYNC == 2 || (BSYNC == 3 && ((f0 / HP) & 1))) __syncthreads();
+            if (BSYNC == 2) __syncthreads();
         }
-        if (BSYNC == 1 || BSYNC == 3) phase_sync();   // all warps leave the FK loop before phase C
+        if (BSYNC == 1) phase_sync();   // all warps leave the FK loop before phase C
         // combine the halves' phase-B terms
         if (HP > 1) {
             sinkB.J += __shfl_xor_sync(FULL, sinkB.J, LPF);

@@ -80,7 +80,7 @@ struct tamp_ctx {
     int ik_iters = 0;            // conditional IK sampler iterations
     float ik_damping = 0.1f;
     int threads = 128;           // particle-kernel block size
-    int bsync = 2;               // block-synchronisation level of the particle kernel (0..3)
+    int bsync = 2;               // block-synchronisation level of the particle kernel (0..2)
     int stride_bytes = 0;
     int32_t t = 0;
     bool ready = false;
