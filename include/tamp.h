@@ -143,7 +143,7 @@ typedef struct {
                                              how a planner reuses a shared subgraph's samples */
 } tamp_var_desc;
 
-/* ground action (Listing 1); unused fields = -1.  Pick/Place use q1 as their conf;
+/* ground action (Listing 1); unused fields = -1.  Pick/Place/Press use q1 as their conf;
    MoveFree/MoveHold go q1 -> q2 through traj (-1 = deferred motion). */
 typedef struct { int32_t kind, obj, grasp, placement, surface, q1, q2, traj; } tamp_action_desc;
 
@@ -182,7 +182,7 @@ typedef struct {
                                              p - eta/2 (p > eta), p^2/(2 eta) (0 < p <= eta), p = r + eta - sd;
                                              needs eta > 0 */
     int32_t ik_iters;                     /* conditional IK sampler: damped-least-squares iterations
-                                             per Pick/Place conf inside tamp_sample_particles; 0 = uniform confs */
+                                             per Pick/Place/Press conf inside tamp_sample_particles; 0 = uniform confs */
     float ik_damping;                     /* DLS damping mu (dq = J^T (J J^T + mu^2 I)^-1 e) */
 } tamp_problem_desc;
 
@@ -229,7 +229,7 @@ tamp_status tamp_get_info(const tamp_ctx* ctx, tamp_info* out);
 /* InitializeParticles (Alg. 1): Philox4x32-10 counter RNG (key = seed, counter =
    (global index lo, hi, variable stream = rng_stream or the variable index, block)); grasps top-down and frozen, placements uniform on the
    surface region, confs uniform within joint limits, then (ik_iters > 0) the conditional IK sampler
-    toward each Pick/Place conf's Kin target, knots linear interpolation.  Resets Adam
+    toward each Pick/Place/Press conf's Kin target, knots linear interpolation.  Resets Adam
    (m = v = 0, t = 0) and the invalid flags. */
 tamp_status tamp_sample_particles(tamp_ctx* ctx, uint64_t seed, void* stream);
 
