@@ -219,6 +219,22 @@ __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float 
     return pen;
 }
 
+// Can a sphere (centre w, radius r) reach the OBB?  false only if it is outside the box and its centre is at
+// least r from it -- the exact test sphere_obb rejects on, so a bounding sphere that fails it bounds only
+// spheres whose hinges are all zero.
+__device__ __forceinline__ bool obb_within(float wx, float wy, float wz, float r, const KObb& B) {
+    const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
+    const float px = fmaf(B.R[0], dx, B.R[3] * dy);
+    const float py = fmaf(B.R[1], dx, B.R[4] * dy);
+    const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(dz) - B.h[2];
+    const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
+    const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+    return !(fmaxf(ax, fmaxf(ay, az)) > 0.f && s >= r * r);
+}
+// slack added to a link's bounding radius in the link-level broad phase: covers the fp32 difference between
+// transforming the link's bounding centre and its sphere centres (~1e-7 m at arm scale)
+constexpr float kLinkMargin = 1e-5f;
+
 // Sphere vs sphere.  Returns the hinge; if GRAD: (ux, uy, uz) = lam * (w_a - w_b)/||.|| (0 if inactive).
 template <bool GRAD>
 __device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, float rr, float4 b,

@@ -298,7 +298,30 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
             if (one_obb) B0 = P.obb[__ffs(K.obb_mask) - 1];
 #pragma unroll 1
             for (int l = kGroup - 1; l >= 0; --l) {
-                if (K.term_cf >= 0) {
+                // link broad phase (conservative, results unchanged): the link's bounding sphere against the
+                // boxes and the partner instances' bounding spheres; a link that reaches none of them has only
+                // zero hinges and zero gradients, so its spheres are skipped
+                bool near = K.term_cf >= 0 && P.rsph_n[l] > 0;
+                if (near) {
+                    const float* lb = P.lbound[l];
+                    float bx, by, bz;
+                    xform(T, lb[0], lb[1], lb[2], bx, by, bz);
+                    const float br = lb[3] + P.eta + kLinkMargin;
+                    near = false;
+                    if (one_obb) {
+                        near = obb_within(bx, by, bz, br, B0);
+                    } else {
+                        for (int b = 0; b < P.n_obb; ++b)
+                            if ((K.obb_mask >> b) & 1) near = near || obb_within(bx, by, bz, br, P.obb[b]);
+                    }
+                    for (int pi = 0; pi < K.part_count && !near; ++pi) {
+                        const int ii = P.partners[K.part_begin + pi];
+                        const float dx = bx - ip(ii, 5), dy = by - ip(ii, 6), dz = bz - ip(ii, 7);
+                        const float R = br + P.obound[P.inst[ii].obj][3];
+                        near = fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f;
+                    }
+                }
+                if (near) {
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
                         const float4 c4 = s_rsph[l][k];
                         float wx, wy, wz;

@@ -101,11 +101,13 @@ EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_size
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libtamp.so (raises if absent: the product path has no fallback)."""
+def load(path: str = None):
+    """Load libtamp.so (raises if absent: the product path has no fallback).  TAMP_LIB selects another build
+    of the same library (A/B kernel experiments)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("TAMP_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libtamp.so not built ({path}); run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
