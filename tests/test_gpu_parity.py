@@ -279,6 +279,43 @@ def test_full_size_sampled_against_oracle(cfg, n):
     assert np.all(close | unstable | kinks[:, None])
 
 
+@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (1, 1 << 20)])
+def test_full_size_mid_optimisation_against_oracle(cfg, n):
+    """The bench's own state: IK-initialised particles (ik_iters = 20, as bench.py) after 3 launches of 10 fused
+    steps (contact-rich: the IK puts grippers at their targets), in the auto launch configuration.  On 24
+    sampled particles the oracle recomputes cost, per-term costs and gradient at that state, and one more
+    Adam step from the GPU's own moments (m, v, t): the state the bench's timed launches work on."""
+    spec = make_config(cfg, n=n)
+    spec.ik_iters = 20
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, n)
+    ctx.sample(seed=3000 + cfg)
+    for _ in range(3):
+        ctx.optimize(10)
+    st = ctx.get_state()
+    idx = np.sort(np.random.default_rng(6).choice(n, 24, replace=False))
+    x32 = st["x"].cpu().numpy()[idx].astype(np.float64)
+    g32 = st["grasp"].cpu().numpy()[idx].reshape(len(idx), -1, 3, 4).astype(np.float64)
+    m32, v32 = st["m"].cpu().numpy()[idx].astype(np.float64), st["v"].cpu().numpy()[idx].astype(np.float64)
+    J, soft, Jc, grad = (t.cpu().numpy()[idx] for t in ctx.eval())
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32, g32)
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(soft, softo, rtol=COST_RTOL, atol=COST_ATOL)
+    ok = grad_ok(grad, grado)
+    kinks = kink_mask(spec, csp, x32, g32, grado, np.random.default_rng(3)) if not ok.all() else ~ok
+    assert np.all(ok | kinks)
+    assert ctx.t == 30
+    ctx.optimize(1)
+    x1 = ctx.get_state()["x"].cpu().numpy()[idx]
+    so = O.new_state(x32, g32)
+    so.m, so.v, so.t = m32, v32, 30
+    O.optimize(spec, csp, so, 1, 1.0 / n)
+    unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
+    close = np.abs(x1 - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
+    assert np.all(close | unstable | kinks[:, None])
+
+
 def test_edge_sizes():
     """N = 1 (a lone particle in a 16-particle block) and k = N."""
     spec, csp, x32, g32 = oracle_inputs(1, 1, seed=80)
