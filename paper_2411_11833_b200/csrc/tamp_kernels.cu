@@ -120,8 +120,8 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
 
 // ------------------------------------------------------------------------------------------------
 // K1b: conditional IK sampler -- damped least squares toward each Pick/Place conf's Kin target
-// T(p) T(g), one particle per 8-lane group (lane j = joint j+1, the same FK product scan as K2), then the
-// knots are re-interpolated from the refined endpoint confs.
+// T(p) T(g), one thread per (particle, conf) pair, then the knots are re-interpolated from the refined endpoint
+// confs.
 //   e = [t* - t_ee ; rotvec(R* R_ee^T)],  J = [z_j x (t_ee - o_j) ; z_j],  dq = J^T (J J^T + mu^2 I)^-1 e
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float y[6]) {
@@ -159,95 +159,107 @@ __device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float
     }
 }
 
+// One thread per (particle, conf) pair: the Kin-constrained confs are independent given the sampled grasps and
+// placements (grid.y = conf).  The chain is composed once per iteration; the joint axes z_j and origins o_j of
+// the forward pass stay in registers for J J^T = sum_j c_j c_j^T, c_j = [z_j x (t_ee - o_j) ; z_j], and for
+// dq_j = c_j . y.  (An earlier 8-lanes-per-pair mapping with the FK product scan repeated the 6x6 solve on every
+// lane of the group: 4.4x slower at config 2, profiles/README.md.)
 __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, float* __restrict__ x,
-                                            const float* __restrict__ grasp, int64_t n, int iters, float damp2) {
-    const int gl = threadIdx.x & (kGroup - 1);
-    const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / kGroup) + threadIdx.x / kGroup;
-    const bool active = pid < n;
-    const int64_t p = active ? pid : (n - 1);
-    const int D = P.D;
-    float* xp = x + p * D;
-    M34 F;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        F.r[3 * i] = P.F[gl][4 * i]; F.r[3 * i + 1] = P.F[gl][4 * i + 1];
-        F.r[3 * i + 2] = P.F[gl][4 * i + 2]; F.t[i] = P.F[gl][4 * i + 3];
+                                                   const float* __restrict__ grasp, int64_t n, int iters, float damp2) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int fsel = -1, nth = 0;
+    for (int f = 0; f < P.n_fk && fsel < 0; ++f) {
+        if ((P.fk[f].term_kp < 0 && P.fk[f].term_kr < 0) || P.fk[f].ghost) continue;
+        if (nth++ == (int)blockIdx.y) fsel = f;
     }
-    const float jlo = gl < TAMP_NJ ? P.jlo[gl] : 0.f;
-    const float jhi = gl < TAMP_NJ ? P.jhi[gl] : 0.f;
-    // blockIdx.y selects the conf: the Kin-constrained confs are independent given the sampled grasps and
-    // placements, so (particle, conf) pairs run in parallel (more warps to hide the serial solve's latency)
-    int nth = 0;
-    for (int f = 0; f < P.n_fk; ++f) {
-        const KFk K = P.fk[f];
-        if ((K.term_kp < 0 && K.term_kr < 0) || K.ghost) continue;
-        if (nth++ != (int)blockIdx.y) continue;
-        // Kin target T* = T(p) T(g)
-        const KInst& I = P.inst[K.kin_inst];
-        float pp[4];
+    if (fsel < 0) return;
+    const KFk K = P.fk[fsel];
+    float* xp = x + p * P.D;
+    // Kin target T* = T(p) T(g)
+    const KInst& I = P.inst[K.kin_inst];
+    float pp[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pp[k] = I.xoff >= 0 ? xp[I.xoff + k] : I.pose[k];
-        float sy, cy;
-        fsincos(pp[3], &sy, &cy);
-        M34 Tp, Tg;
-        Tp.r[0] = cy; Tp.r[1] = -sy; Tp.r[2] = 0.f; Tp.r[3] = sy; Tp.r[4] = cy; Tp.r[5] = 0.f;
-        Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f; Tp.t[0] = pp[0]; Tp.t[1] = pp[1]; Tp.t[2] = pp[2];
-        load_m34(Tg, grasp + (p * P.n_grasp + K.kin_grasp) * 12);
-        const M34 Ts = compose(Tp, Tg);
-        float q = gl < TAMP_NJ ? xp[K.xoff + gl] : 0.f;
-        for (int it = 0; it < iters; ++it) {
-            M34 T;
-            {
-                float s, c;
-                fsincos(q, &s, &c);
+    for (int k = 0; k < 4; ++k) pp[k] = I.xoff >= 0 ? xp[I.xoff + k] : I.pose[k];
+    float sy, cy;
+    fsincos(pp[3], &sy, &cy);
+    M34 Tp, Tg;
+    Tp.r[0] = cy; Tp.r[1] = -sy; Tp.r[2] = 0.f; Tp.r[3] = sy; Tp.r[4] = cy; Tp.r[5] = 0.f;
+    Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f; Tp.t[0] = pp[0]; Tp.t[1] = pp[1]; Tp.t[2] = pp[2];
+    load_m34(Tg, grasp + (p * P.n_grasp + K.kin_grasp) * 12);
+    const M34 Ts = compose(Tp, Tg);
+    float q[TAMP_NJ];
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    T.r[3 * i] = fmaf(F.r[3 * i], c, F.r[3 * i + 1] * s);
-                    T.r[3 * i + 1] = fmaf(F.r[3 * i + 1], c, -F.r[3 * i] * s);
-                    T.r[3 * i + 2] = F.r[3 * i + 2];
-                    T.t[i] = F.t[i];
-                }
+    for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];
+    for (int it = 0; it < iters; ++it) {
+        float z[TAMP_NJ][3], o[TAMP_NJ][3];
+        M34 T;
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) {
+            float s, c;
+            fsincos(q[j], &s, &c);
+            M34 Aj;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const float* Fr = P.F[j] + 4 * i;
+                Aj.r[3 * i] = fmaf(Fr[0], c, Fr[1] * s);
+                Aj.r[3 * i + 1] = fmaf(Fr[1], c, -Fr[0] * s);
+                Aj.r[3 * i + 2] = Fr[2];
+                Aj.t[i] = Fr[3];
             }
+            T = j == 0 ? Aj : compose(T, Aj);
 #pragma unroll
-            for (int d = 1; d < kGroup; d <<= 1) {
-                const M34 U = shfl_up_m34(T, d);
-                if (gl >= d) T = compose(U, T);
-            }
-            const M34 Tee = shfl_m34(T, kGroup - 1);
-            float e[6];
-            e[0] = Ts.t[0] - Tee.t[0]; e[1] = Ts.t[1] - Tee.t[1]; e[2] = Ts.t[2] - Tee.t[2];
-            float E[9];   // R* R_ee^T
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j)
-                    E[3 * i + j] = fmaf(Ts.r[3 * i], Tee.r[3 * j], fmaf(Ts.r[3 * i + 1], Tee.r[3 * j + 1], Ts.r[3 * i + 2] * Tee.r[3 * j + 2]));
-            const float wx = E[7] - E[5], wy = E[2] - E[6], wz = E[3] - E[1];
-            const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
-            const float th = fatan2_pos(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
-            const float k = wn > 0.f ? th / wn : 0.f;
-            e[3] = wx * k; e[4] = wy * k; e[5] = wz * k;
-            // Jacobian column of my joint
-            float c[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (gl < TAMP_NJ) {
-                const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
-                const float rx = Tee.t[0] - T.t[0], ry = Tee.t[1] - T.t[1], rz = Tee.t[2] - T.t[2];
-                c[0] = zy * rz - zz * ry; c[1] = zz * rx - zx * rz; c[2] = zx * ry - zy * rx;
-                c[3] = zx; c[4] = zy; c[5] = zz;
-            }
-            float A[21];
-#pragma unroll
-            for (int i = 0; i < 6; ++i)
-#pragma unroll
-                for (int j = 0; j <= i; ++j) A[i * (i + 1) / 2 + j] = gsum<kGroup>(c[i] * c[j]) + (i == j ? damp2 : 0.f);
-            float y[6];
-            chol6_solve(A, e, y);
-            const float dq = fmaf(c[0], y[0], fmaf(c[1], y[1], fmaf(c[2], y[2], fmaf(c[3], y[3], fmaf(c[4], y[4], c[5] * y[5])))));
-            if (gl < TAMP_NJ) q = fminf(fmaxf(q + dq, jlo), jhi);
+            for (int i = 0; i < 3; ++i) { z[j][i] = T.r[3 * i + 2]; o[j][i] = T.t[i]; }
         }
-        if (gl < TAMP_NJ && active) xp[K.xoff + gl] = q;
-        __syncwarp();
+        {
+            M34 Fe;
+            load_m34(Fe, P.F[kGroup - 1]);
+            T = compose(T, Fe);
+        }
+        float e[6];
+        e[0] = Ts.t[0] - T.t[0]; e[1] = Ts.t[1] - T.t[1]; e[2] = Ts.t[2] - T.t[2];
+        float E[9];   // R* R_ee^T
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                E[3 * i + j] = fmaf(Ts.r[3 * i], T.r[3 * j], fmaf(Ts.r[3 * i + 1], T.r[3 * j + 1], Ts.r[3 * i + 2] * T.r[3 * j + 2]));
+        const float wx = E[7] - E[5], wy = E[2] - E[6], wz = E[3] - E[1];
+        const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
+        const float th = fatan2_pos(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
+        const float kk = wn > 0.f ? th / wn : 0.f;
+        e[3] = wx * kk; e[4] = wy * kk; e[5] = wz * kk;
+        auto column = [&](int j, float (&c)[6]) {
+            const float rx = T.t[0] - o[j][0], ry = T.t[1] - o[j][1], rz = T.t[2] - o[j][2];
+            c[0] = z[j][1] * rz - z[j][2] * ry; c[1] = z[j][2] * rx - z[j][0] * rz; c[2] = z[j][0] * ry - z[j][1] * rx;
+            c[3] = z[j][0]; c[4] = z[j][1]; c[5] = z[j][2];
+        };
+        float A[21];
+#pragma unroll
+        for (int i = 0; i < 21; ++i) A[i] = 0.f;
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) {
+            float c[6];
+            column(j, c);
+#pragma unroll
+            for (int a = 0; a < 6; ++a)
+#pragma unroll
+                for (int b = 0; b <= a; ++b) A[a * (a + 1) / 2 + b] = fmaf(c[a], c[b], A[a * (a + 1) / 2 + b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 6; ++a) A[a * (a + 1) / 2 + a] += damp2;
+        float y[6];
+        chol6_solve(A, e, y);
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) {
+            float c[6];
+            column(j, c);
+            const float dq = fmaf(c[0], y[0], fmaf(c[1], y[1], fmaf(c[2], y[2], fmaf(c[3], y[3], fmaf(c[4], y[4], c[5] * y[5])))));
+            q[j] = fminf(fmaxf(q[j] + dq, P.jlo[j]), P.jhi[j]);
+        }
     }
+#pragma unroll
+    for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
 }
 
 // knots: linear interpolation between the (IK-refined) endpoint confs; 8 lanes per particle
@@ -398,7 +410,8 @@ cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n
     const int per_block = 128 / kGroup;
     const unsigned bx = (unsigned)((n + per_block - 1) / per_block);
     if (n_kin > 0) {
-        k_ik<<<dim3(bx, (unsigned)n_kin), 128, 0, st>>>(P, x, grasp, n, iters, damping * damping);
+        k_ik<<<dim3((unsigned)((n + 127) / 128), (unsigned)n_kin), 128, 0, st>>>(P, x, grasp, n, iters,
+                                                                                 damping * damping);
         counted();
     }
     if (P.n_traj > 0) {
