@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--self-collision", action="store_true", help="add the SELF term (SURVEY §8(f) f2)")
     p.add_argument("--ik-iters", type=int, default=20,
                    help="conditional IK sampler iterations in InitializeParticles (P:521); 0 = uniform confs")
+    p.add_argument("--ik-seeds", type=int, default=8, help="IK restarts per conf (1, 2, 4, 8; DESIGN.md R6)")
     return p.parse_args()
 
 
@@ -349,6 +350,7 @@ def main():
         n = 131072 // 8                              # config 4: 128K particles over 8 GPUs (per-rank share)
     spec = make_config(cfg, n=n)
     spec.ik_iters = args.ik_iters
+    spec.ik_seeds = args.ik_seeds
     spec.self_collision = args.self_collision
     n_global = n * world
     ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes,
@@ -453,7 +455,7 @@ def main():
                            "particles_per_gpu": n, "particles_global": n_global, "D": ctx.D,
                            "hard_terms": ctx.n_hard, "adam_steps_per_step": args.adam_steps,
                            "check_every": args.check_every, "best_k": args.k, "l2": "flushed between steps",
-                           "ik_iters": args.ik_iters, "self_collision": args.self_collision,
+                           "ik_iters": args.ik_iters, "ik_seeds": args.ik_seeds, "self_collision": args.self_collision,
                            "lanes_per_particle": ctx.lanes_per_particle, "block_threads": ctx.block_threads,
                            "block_sync": ctx.block_sync,
                            "parallelism": f"dp{world}"},

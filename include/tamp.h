@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TAMP_ABI_VERSION 2
+#define TAMP_ABI_VERSION 3
 
 /* compiled limits of the sm_100a kernels (exceeding one returns TAMP_E_UNSUPPORTED) */
 #define TAMP_NJ 7                     /* 7-DOF arm */
@@ -184,6 +184,12 @@ typedef struct {
     int32_t ik_iters;                     /* conditional IK sampler: damped-least-squares iterations
                                              per Pick/Place/Press conf inside tamp_sample_particles; 0 = uniform confs */
     float ik_damping;                     /* DLS damping mu (dq = J^T (J J^T + mu^2 I)^-1 e) */
+    int32_t ik_seeds;                     /* IK restarts per conf, 1, 2, 4 or 8 (0 = 1), solved in parallel (cuRobo's
+                                             solver is multi-seed): seed 0 starts from the uniform conf sample,
+                                             seed s >= 1 from a fresh uniform conf (Philox blocks 2s, 2s+1 of the conf's
+                                             stream); kept: the first seed whose final position / rotation error is
+                                             <= 1e-3 m / 1e-3 rad, else the one with the smallest sum of the two
+                                             (lowest seed on ties) -- DESIGN.md R6 */
 } tamp_problem_desc;
 
 /* what the compiled CSP looks like (term order = DESIGN.md "canonical term order") */

@@ -388,6 +388,42 @@ def ik_dls(robot, q, T_target, iters, damping):
     return q
 
 
+IK_TOL_POS, IK_TOL_ROT = 1e-3, 1e-3
+
+
+def ik_errors(robot, q, T_target):
+    """Kin errors of the tool frame at q against T_target: (||t* - t_ee||, geodesic angle of R* R_ee^T)."""
+    Tee = forward_kinematics(robot, torch.as_tensor(q, dtype=DT))[:, 8]
+    Tt = torch.as_tensor(T_target, dtype=DT)
+    ep = torch.linalg.vector_norm(Tt[:, :3, 3] - Tee[:, :3, 3], dim=-1)
+    th = rotation_angle(Tt[:, :3, :3], Tee[:, :3, :3])
+    return ep.numpy(), th.numpy()
+
+
+def ik_restarts(spec, q0, T_target, seed, gidx, stream):
+    """The conditional IK sampler with spec.ik_seeds restarts (R6; cuRobo's solver is multi-seed,
+    P:521).  Restart 0 starts from q0 (the uniform conf sample), restart s >= 1 from a fresh uniform conf drawn
+    from Philox blocks 2s, 2s+1 of the conf's stream; each runs ik_dls.  Kept per particle: the first restart
+    whose final errors are <= (1e-3 m, 1e-3 rad), else the one with the smallest e_pos + theta (lowest index
+    on ties)."""
+    S = int(getattr(spec, "ik_seeds", 1) or 1)
+    lo, hi = spec.robot.joint_lo, spec.robot.joint_hi
+    if S == 1:
+        return ik_dls(spec.robot, q0, T_target, spec.ik_iters, spec.ik_damping)
+    u = uniforms(seed, gidx, stream, 8 * S)
+    qs, conv, score = [], [], []
+    for s in range(S):
+        start = q0 if s == 0 else lo + u[:, 8 * s:8 * s + 7] * (hi - lo)
+        q = ik_dls(spec.robot, start, T_target, spec.ik_iters, spec.ik_damping)
+        ep, th = ik_errors(spec.robot, q, T_target)
+        qs.append(q)
+        conv.append((ep <= IK_TOL_POS) & (th <= IK_TOL_ROT))
+        score.append(ep + th)
+    conv, score = np.stack(conv, 1), np.stack(score, 1)
+    keep = np.where(conv.any(axis=1), np.argmax(conv, axis=1), np.argmin(score, axis=1))
+    return np.stack(qs, 1)[np.arange(len(q0)), keep]
+
+
 def _stream(V, vi):
     """Philox counter word of variable vi's sampler: its rng_stream if set, else its index."""
     return int(getattr(V[vi], "rng_stream", 0)) or vi
@@ -461,7 +497,7 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
             Tg = np.concatenate([grasps[:, gslot[a.grasp]], bottom], 1)
             Tt = (pose_xyzyaw(torch.as_tensor(pval)) @ torch.as_tensor(Tg)).numpy()
             off = csp.offsets[a.q1]
-            x[:, off:off + 7] = ik_dls(spec.robot, x[:, off:off + 7], Tt, spec.ik_iters, spec.ik_damping)
+            x[:, off:off + 7] = ik_restarts(spec, x[:, off:off + 7], Tt, seed, gidx, _stream(V, a.q1))
     for a in spec.actions:
         if a.kind in (MOVE_FREE, MOVE_HOLD) and a.traj >= 0 and V[a.traj].n_knots > 0:
             K = V[a.traj].n_knots

@@ -28,7 +28,8 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
                             cudaStream_t st);
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
                           cudaStream_t st);
-cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
+cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, const float* grasp, int64_t n, int64_t gofs,
+                      uint64_t seed, int iters, float damping, int n_seeds,
                       cudaStream_t st);
 int particle_kernel_regs(int gs, int threads);
 int serial_kernel_regs();
@@ -79,6 +80,7 @@ struct tamp_ctx {
     int gs = 8;                  // lanes per particle in the particle kernel
     int ik_iters = 0;            // conditional IK sampler iterations
     float ik_damping = 0.1f;
+    int ik_seeds = 1;            // IK restarts per conf (1, 2, 4, 8)
     int threads = 128;           // particle-kernel block size
     int bsync = 2;               // block-synchronisation level of the particle kernel (0..2)
     int stride_bytes = 0;
@@ -836,6 +838,11 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
     }
     c->ik_iters = desc->ik_iters;
     c->ik_damping = desc->ik_damping;
+    c->ik_seeds = desc->ik_seeds ? desc->ik_seeds : 1;
+    if (c->ik_seeds != 1 && c->ik_seeds != 2 && c->ik_seeds != 4 && c->ik_seeds != 8) {
+        delete c;
+        return fail(TAMP_E_INVALID, "ik_seeds must be 0, 1, 2, 4 or 8");
+    }
     if (desc->lanes_per_particle != 0 && desc->lanes_per_particle != 1 && desc->lanes_per_particle != 4 &&
         desc->lanes_per_particle != 8 && desc->lanes_per_particle != 16) {
         delete c;
@@ -1044,7 +1051,8 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     DeviceGuard g(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(launch_sample(c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, st), "sample");
-    CUDA_TRY(launch_ik(c->P, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->ik_iters, c->ik_damping, st),
+    CUDA_TRY(launch_ik(c->P, c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, c->ik_iters,
+                       c->ik_damping, c->ik_seeds, st),
              "sample: IK");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero m");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero v");

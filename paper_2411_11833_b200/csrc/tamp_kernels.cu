@@ -159,21 +159,70 @@ __device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float
     }
 }
 
-// One thread per (particle, conf) pair: the Kin-constrained confs are independent given the sampled grasps and
-// placements (grid.y = conf).  The chain is composed once per iteration; the joint axes z_j and origins o_j of
-// the forward pass stay in registers for J J^T = sum_j c_j c_j^T, c_j = [z_j x (t_ee - o_j) ; z_j], and for
-// dq_j = c_j . y.  (An earlier 8-lanes-per-pair mapping with the FK product scan repeated the 6x6 solve on every
-// lane of the group: 4.4x slower at config 2, profiles/README.md.)
-__global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, float* __restrict__ x,
-                                                   const float* __restrict__ grasp, int64_t n, int iters, float damp2) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
+// One thread per (particle, conf, seed): the Kin-constrained confs are independent given the sampled grasps and
+// placements (grid.y = conf), and the S restarts of a conf (R6) run on S adjacent lanes.  The chain is
+// composed once per iteration; the joint axes z_j and origins o_j of the forward pass stay in registers for
+// J J^T = sum_j c_j c_j^T, c_j = [z_j x (t_ee - o_j) ; z_j], and for dq_j = c_j . y.  (An earlier 8-lanes-per-pair
+// mapping with the FK product scan repeated the 6x6 solve on every lane of the group: 4.4x slower at config 2,
+// profiles/README.md.)
+struct KIkStreams { uint32_t stream[TAMP_MAX_FK]; };   // Philox stream of each Kin conf's sampler
+constexpr float kIkTolPos = 1e-3f, kIkTolRot = 1e-3f;  // a restart counts as converged below both
+
+// tool pose of the chain at q, and the Kin errors to T*: e_pos = ||t* - t_ee||, theta = angle(R* R_ee^T)
+__device__ __forceinline__ void ik_fk(const KProgram& P, const float (&q)[TAMP_NJ], M34& T, float (&z)[TAMP_NJ][3],
+                                      float (&o)[TAMP_NJ][3]) {
+#pragma unroll
+    for (int j = 0; j < TAMP_NJ; ++j) {
+        float s, c;
+        fsincos(q[j], &s, &c);
+        M34 Aj;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const float* Fr = P.F[j] + 4 * i;
+            Aj.r[3 * i] = fmaf(Fr[0], c, Fr[1] * s);
+            Aj.r[3 * i + 1] = fmaf(Fr[1], c, -Fr[0] * s);
+            Aj.r[3 * i + 2] = Fr[2];
+            Aj.t[i] = Fr[3];
+        }
+        T = j == 0 ? Aj : compose(T, Aj);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) { z[j][i] = T.r[3 * i + 2]; o[j][i] = T.t[i]; }
+    }
+    M34 Fe;
+    load_m34(Fe, P.F[kGroup - 1]);
+    T = compose(T, Fe);
+}
+
+__device__ __forceinline__ void ik_error(const M34& Ts, const M34& T, float (&e)[6], float& epos, float& th) {
+    e[0] = Ts.t[0] - T.t[0]; e[1] = Ts.t[1] - T.t[1]; e[2] = Ts.t[2] - T.t[2];
+    float E[9];   // R* R_ee^T
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            E[3 * i + j] = fmaf(Ts.r[3 * i], T.r[3 * j], fmaf(Ts.r[3 * i + 1], T.r[3 * j + 1], Ts.r[3 * i + 2] * T.r[3 * j + 2]));
+    const float wx = E[7] - E[5], wy = E[2] - E[6], wz = E[3] - E[1];
+    const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
+    th = fatan2_pos(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
+    const float kk = wn > 0.f ? th / wn : 0.f;
+    e[3] = wx * kk; e[4] = wy * kk; e[5] = wz * kk;
+    epos = sqrtf(fmaf(e[0], e[0], fmaf(e[1], e[1], e[2] * e[2])));
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, const KIkStreams Z, float* __restrict__ x,
+                                            const float* __restrict__ grasp, int64_t n, int64_t gofs, uint64_t seed,
+                                            int iters, float damp2) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int sd = (int)(threadIdx.x & (S - 1));          // restart index
+    const bool active = t / S < n;
+    const int64_t p = active ? t / S : n - 1;              // idle lanes mirror the last pair (shuffles below)
     int fsel = -1, nth = 0;
     for (int f = 0; f < P.n_fk && fsel < 0; ++f) {
         if ((P.fk[f].term_kp < 0 && P.fk[f].term_kr < 0) || P.fk[f].ghost) continue;
         if (nth++ == (int)blockIdx.y) fsel = f;
     }
-    if (fsel < 0) return;
+    if (fsel < 0) return;                                   // block-uniform
     const KFk K = P.fk[fsel];
     float* xp = x + p * P.D;
     // Kin target T* = T(p) T(g)
@@ -189,46 +238,21 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
     load_m34(Tg, grasp + (p * P.n_grasp + K.kin_grasp) * 12);
     const M34 Ts = compose(Tp, Tg);
     float q[TAMP_NJ];
+    if (sd == 0) {
 #pragma unroll
-    for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];
+        for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];
+    } else {                                                // restart: a fresh uniform conf
+        float u[8];
+        uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd, u);
+        uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd + 1, u + 4);
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) q[j] = P.jlo[j] + u[j] * (P.jhi[j] - P.jlo[j]);
+    }
+    float z[TAMP_NJ][3], o[TAMP_NJ][3], e[6], epos, th;
+    M34 T;
     for (int it = 0; it < iters; ++it) {
-        float z[TAMP_NJ][3], o[TAMP_NJ][3];
-        M34 T;
-#pragma unroll
-        for (int j = 0; j < TAMP_NJ; ++j) {
-            float s, c;
-            fsincos(q[j], &s, &c);
-            M34 Aj;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const float* Fr = P.F[j] + 4 * i;
-                Aj.r[3 * i] = fmaf(Fr[0], c, Fr[1] * s);
-                Aj.r[3 * i + 1] = fmaf(Fr[1], c, -Fr[0] * s);
-                Aj.r[3 * i + 2] = Fr[2];
-                Aj.t[i] = Fr[3];
-            }
-            T = j == 0 ? Aj : compose(T, Aj);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) { z[j][i] = T.r[3 * i + 2]; o[j][i] = T.t[i]; }
-        }
-        {
-            M34 Fe;
-            load_m34(Fe, P.F[kGroup - 1]);
-            T = compose(T, Fe);
-        }
-        float e[6];
-        e[0] = Ts.t[0] - T.t[0]; e[1] = Ts.t[1] - T.t[1]; e[2] = Ts.t[2] - T.t[2];
-        float E[9];   // R* R_ee^T
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-                E[3 * i + j] = fmaf(Ts.r[3 * i], T.r[3 * j], fmaf(Ts.r[3 * i + 1], T.r[3 * j + 1], Ts.r[3 * i + 2] * T.r[3 * j + 2]));
-        const float wx = E[7] - E[5], wy = E[2] - E[6], wz = E[3] - E[1];
-        const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
-        const float th = fatan2_pos(0.5f * wn, 0.5f * (E[0] + E[4] + E[8] - 1.f));
-        const float kk = wn > 0.f ? th / wn : 0.f;
-        e[3] = wx * kk; e[4] = wy * kk; e[5] = wz * kk;
+        ik_fk(P, q, T, z, o);
+        ik_error(Ts, T, e, epos, th);
         auto column = [&](int j, float (&c)[6]) {
             const float rx = T.t[0] - o[j][0], ry = T.t[1] - o[j][1], rz = T.t[2] - o[j][2];
             c[0] = z[j][1] * rz - z[j][2] * ry; c[1] = z[j][2] * rx - z[j][0] * rz; c[2] = z[j][0] * ry - z[j][1] * rx;
@@ -258,8 +282,30 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
             q[j] = fminf(fmaxf(q[j] + dq, P.jlo[j]), P.jhi[j]);
         }
     }
+    int keep = 0;
+    if (S > 1) {   // choose among the restarts: first converged, else the smallest epos + theta (lowest seed on ties)
+        ik_fk(P, q, T, z, o);
+        ik_error(Ts, T, e, epos, th);
+        const unsigned lane0 = threadIdx.x & 31 & ~(unsigned)(S - 1);
+        const unsigned conv = (__ballot_sync(FULL, epos <= kIkTolPos && th <= kIkTolRot) >> lane0) & ((1u << S) - 1u);
+        if (conv) {
+            keep = __ffs(conv) - 1;
+        } else {
+            float best = epos + th;
+            int bi = sd;
 #pragma unroll
-    for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
+            for (int m = 1; m < S; m <<= 1) {
+                const float ob = __shfl_xor_sync(FULL, best, m, S);
+                const int oi = __shfl_xor_sync(FULL, bi, m, S);
+                if (ob < best || (ob == best && oi < bi) || (best != best && ob == ob)) { best = ob; bi = oi; }
+            }
+            keep = bi;
+        }
+    }
+    if (active && sd == keep) {
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
+    }
 }
 
 // knots: linear interpolation between the (IK-refined) endpoint confs; 8 lanes per particle
@@ -401,17 +447,29 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
 // registers per thread of the hot kernel (for the launch-configuration policy)
 int particle_kernel_regs(int gs, int threads) { return particle_kernel_regs_sm(gs, threads); }
 
-cudaError_t launch_ik(const KProgram& P, float* x, const float* grasp, int64_t n, int iters, float damping,
-                      cudaStream_t st) {
+cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, const float* grasp, int64_t n, int64_t gofs,
+                      uint64_t seed, int iters, float damping, int n_seeds, cudaStream_t st) {
     if (n <= 0 || iters <= 0) return cudaSuccess;
+    KIkStreams Z;
     int n_kin = 0;
-    for (int f = 0; f < P.n_fk; ++f)
-        if ((P.fk[f].term_kp >= 0 || P.fk[f].term_kr >= 0) && !P.fk[f].ghost) ++n_kin;
+    for (int f = 0; f < P.n_fk; ++f) {
+        if ((P.fk[f].term_kp < 0 && P.fk[f].term_kr < 0) || P.fk[f].ghost) continue;
+        Z.stream[n_kin] = 0u;
+        for (int v = 0; v < SP.n_vars; ++v)      // the conf sampler that drew this conf (seed 0's start)
+            if (SP.v[v].kind == KS_CONF && SP.v[v].xoff == P.fk[f].xoff) Z.stream[n_kin] = SP.v[v].stream;
+        ++n_kin;
+    }
     const int per_block = 128 / kGroup;
     const unsigned bx = (unsigned)((n + per_block - 1) / per_block);
     if (n_kin > 0) {
-        k_ik<<<dim3((unsigned)((n + 127) / 128), (unsigned)n_kin), 128, 0, st>>>(P, x, grasp, n, iters,
-                                                                                 damping * damping);
+        const dim3 grid((unsigned)((n * n_seeds + 127) / 128), (unsigned)n_kin);
+        const float d2 = damping * damping;
+        switch (n_seeds) {
+            case 8: k_ik<8><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
+            case 4: k_ik<4><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
+            case 2: k_ik<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
+            default: k_ik<1><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
+        }
         counted();
     }
     if (P.n_traj > 0) {

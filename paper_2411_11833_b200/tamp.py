@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtamp.so")
 
 # ---- limits / enums (include/tamp.h) ----
-ABI_VERSION = 2
+ABI_VERSION = 3
 NJ = 7
 MAX_ROBOT_SPHERES = 32
 MAX_OBB = 16
@@ -81,7 +81,7 @@ class ProblemDesc(ctypes.Structure):
                 ("beta1", F), ("beta2", F), ("adam_eps", F),
                 ("lr_conf", F), ("lr_pos", F), ("lr_yaw", F), ("lr_knot", F), ("grad_scale", F),
                 ("lanes_per_particle", I32), ("block_threads", I32), ("block_sync", I32),
-                ("self_collision", I32), ("collision_smooth", I32), ("ik_iters", I32), ("ik_damping", F)]
+                ("self_collision", I32), ("collision_smooth", I32), ("ik_iters", I32), ("ik_damping", F), ("ik_seeds", I32)]
 
 
 class Info(ctypes.Structure):
@@ -242,6 +242,7 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
     d.collision_smooth = int(bool(getattr(spec, "collision_smooth", False)))
     d.ik_iters = int(getattr(spec, "ik_iters", 0))
     d.ik_damping = float(getattr(spec, "ik_damping", 0.1))
+    d.ik_seeds = int(getattr(spec, "ik_seeds", 1))
     return d
 
 

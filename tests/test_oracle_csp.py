@@ -412,6 +412,48 @@ def test_ik_initialisation_improves_kin_residuals():
     assert ((Jc1[:, 2] <= 5e-3) & (Jc1[:, 3] <= 0.05)).mean() > 0.25
 
 
+def test_ik_restarts_keep_first_converged_restart():
+    """IK restarts (R6): restart 0 is the single-seed sampler exactly; with 8 restarts the kept conf is the first
+    restart that reaches the FK target (checked against FK, pinned above) and far more Kin terms start satisfied;
+    restart s draws Philox blocks 2s, 2s+1 of the conf's stream (the same draw the conf sampler makes for s = 0)."""
+    from oracle.philox import uniforms
+    spec = make_config(3, n=96)
+    spec.ik_iters = 20
+    csp = O.build_csp(spec)
+    gidx = np.arange(96)
+    x1, g = O.initialize_particles(spec, csp, 4, gidx)
+    spec.ik_seeds = 8
+    x8, g8 = O.initialize_particles(spec, csp, 4, gidx)
+    assert np.array_equal(g, g8)
+    _, Jc1, _ = _eval(spec, csp, x1, g)
+    _, Jc8, _ = _eval(spec, csp, x8, g)
+    kin = [i for i, t in enumerate(csp.terms) if t.kind in ("KP", "KR")]
+    ok1 = np.all(Jc1[:, kin] <= np.array([spec.eps[csp.terms[i].kind] for i in kin]), axis=1)
+    ok8 = np.all(Jc8[:, kin] <= np.array([spec.eps[csp.terms[i].kind] for i in kin]), axis=1)
+    assert ok8.mean() > 0.5 and ok8.mean() > 5 * max(ok1.mean(), 0.01)
+    # first conf of the skeleton: recompute the restarts by hand and check the kept one
+    a = [a for a in spec.actions if a.kind == 1][0]           # the first Pick
+    off, vi = csp.offsets[a.q1], a.q1
+    q0 = spec.robot.joint_lo + uniforms(4, gidx, vi, 7) * (spec.robot.joint_hi - spec.robot.joint_lo)
+    pv = spec.variables[a.placement]
+    bottom = np.zeros((96, 1, 4))
+    bottom[..., 3] = 1.0
+    Tt = (O.pose_xyzyaw(torch.as_tensor(np.broadcast_to(pv.value, (96, 4)).copy())) @
+          torch.as_tensor(np.concatenate([g[:, 0], bottom], 1))).numpy()
+    u = uniforms(4, gidx, vi, 64)
+    assert np.array_equal(u[:, :7], uniforms(4, gidx, vi, 7))
+    qs = [O.ik_dls(spec.robot, q0 if s == 0 else spec.robot.joint_lo + u[:, 8 * s:8 * s + 7] *
+                   (spec.robot.joint_hi - spec.robot.joint_lo), Tt, 20, spec.ik_damping) for s in range(8)]
+    errs = [O.ik_errors(spec.robot, q, Tt) for q in qs]
+    for i in range(96):
+        conv = [s for s in range(8) if errs[s][0][i] <= 1e-3 and errs[s][1][i] <= 1e-3]
+        keep = conv[0] if conv else int(np.argmin([errs[s][0][i] + errs[s][1][i] for s in range(8)]))
+        assert np.array_equal(x8[i, off:off + 7], qs[keep][i])
+    F = O.forward_kinematics(spec.robot, torch.as_tensor(x8[:, off:off + 7]))[:, 8].numpy()
+    reached = np.linalg.norm(F[:, :3, 3] - Tt[:, :3, 3], axis=1) <= 1e-3
+    assert reached.mean() > 0.8
+
+
 def test_plan_heuristic_eq5():
     """counts [10, 5] -> H = 7.5; a zero count takes the penalty."""
     assert O.plan_heuristic([10, 5], -100.0) == 7.5

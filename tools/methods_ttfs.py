@@ -22,6 +22,7 @@ for cfg in cfgs:
         for trial in range(trials):
             spec = make_config(cfg, n=n)
             spec.ik_iters = 20
+            spec.ik_seeds = 8
             torch.cuda.synchronize()
             t = time.perf_counter()
             res = planner.cutamp([spec], n, seed=1000 * cfg + trial, steps_per_pop=1000, max_pops=1, method=method)

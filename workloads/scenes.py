@@ -142,6 +142,7 @@ class ProblemSpec:
     # confs only, the paper's `Optimization` baseline init)
     ik_iters: int = 0
     ik_damping: float = 0.1
+    ik_seeds: int = 1           # IK restarts per conf (R6): 1, 2, 4 or 8
 
 
 DEFAULT_LAM = dict(JL=1.0, CF=1.0, KP=1.0, KR=5.0, SS=2.0, SC=2.0, CP=1.0, SELF=1.0, PC=1.0)
