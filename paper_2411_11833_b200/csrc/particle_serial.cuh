@@ -36,7 +36,7 @@ __host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool mv
     return L;
 }
 
-constexpr int kSerialThreads = 128;
+constexpr int kSerialThreads = 512;   // launch bound (blocks of <= 512 threads, <= 128 registers)
 
 // dynamic shared memory of a serial-mapping block of `threads` particles (column pitch threads + 1: the
 // cooperative row <-> column transposes hit distinct banks)
@@ -60,7 +60,7 @@ __device__ __forceinline__ void serial_term(const KProgram& P, const KArgs& A, T
 }
 
 template <int MODE, bool SMOOTH>
-__global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_constant__ KProgram P, const KArgs A) {
+__global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     const float smooth = SMOOTH ? P.smooth : 0.f;
     extern __shared__ float4 smem4[];
@@ -382,6 +382,9 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
                 }
             }
             if (K.term_cf >= 0) serial_term<MODE>(P, A, sink, K.term_cf, jcf, active, p, s_counts);
+            // block-synchronous configurations: every warp of the block executes the same (large) code region at
+            // a time and the instruction cache is shared (the kernel body is ~100 KB of SASS)
+            if (A.bsync) __syncthreads();
         }
 
         // ---- StablePlace / press contact / CFreePlace per Place or press action ----
@@ -464,6 +467,7 @@ __global__ void __launch_bounds__(kSerialThreads, 4) k_serial(const __grid_const
                 serial_term<MODE>(P, A, sink, Q.term_cp, jcp, active, p, s_counts);
             }
             if (GRAD) add_iw(ii, own);
+            if (A.bsync) __syncthreads();
         }
 
         // ---- soft costs (Eq. 2 second sum) ----

@@ -776,6 +776,7 @@ static KArgs base_args(tamp_ctx* c) {
     A.off_gT = c->off_gT;
     A.off_gTi = c->off_gTi;
     A.off_rsw = c->off_rsw;
+    A.bsync = c->gs == 1 ? c->bsync : 0;
     return A;
 }
 
@@ -884,24 +885,30 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         int smem_optin = 227 * 1024;
         cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         cudaGetLastError();
-        c->threads = desc->block_threads ? desc->block_threads : kSerialThreads;
+        c->threads = desc->block_threads ? desc->block_threads : 128;
         if (c->threads % 32 || c->threads < 32 || c->threads > kSerialThreads) {
             delete c;
-            return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 128] for 1 lane per particle");
+            return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 512] for 1 lane per particle");
         }
-        // auto: the block size with the most resident warps per SM (shared memory holds the per-particle state)
+        // block-synchronous configurations (default): one large block per SM whose warps walk the ~100 KB kernel
+        // body together and share the instruction cache (`no_instruction` was the top stall with independent
+        // small blocks: 1.6 cycles per issued instruction, profiles/README.md)
+        c->bsync = desc->block_sync >= 0 ? (desc->block_sync ? 1 : 0) : 1;
+        // auto: with barriers, the largest block that fits one per SM (shared memory holds the per-particle
+        // state, columns of pitch threads + 1); without, the block size with the most resident warps per SM
         if (!desc->block_threads) {
             int smem_sm = 228 * 1024;
             cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
             cudaGetLastError();
             const int regs = std::max(32, serial_kernel_regs());
             int best_w = -1;
-            for (int t = 32; t <= kSerialThreads; t += 32) {
-                const size_t sb = serial_smem_bytes(c->P, t, true) + 3 * 1024;   // + static smem, reserved
-                if (sb > (size_t)smem_optin + 3 * 1024) continue;
+            for (int t = 32; t <= (c->bsync ? kSerialThreads : 128); t += 32) {
+                const size_t sb = serial_smem_bytes(c->P, t, true) + 4096;   // + static smem, reserved
+                if (sb > (size_t)smem_optin) continue;
                 const int by_smem = (int)((size_t)smem_sm / sb);
                 const int by_regs = 65536 / (((regs + 7) & ~7) * t);
-                const int w = std::min(std::min(by_smem, by_regs), 32) * (t / 32);
+                const int blocks = c->bsync ? std::min(std::min(by_smem, by_regs), 1) : std::min(std::min(by_smem, by_regs), 32);
+                const int w = blocks * (t / 32);
                 if (w > best_w || (w == best_w && t > c->threads)) { best_w = w; c->threads = t; }
             }
         }
@@ -911,7 +918,6 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             return fail(TAMP_E_UNSUPPORTED, "1 lane per particle: no SELF term, no held objects at knots, and the "
                                             "per-particle state must fit shared memory");
         }
-        c->bsync = 0;
     } else {
         // launch configuration of the particle kernel.  Auto: block-synchronous phases with one large block
         // per SM holding that SM's share of the particles (all warps of an SM walk the same code region ->
