@@ -29,7 +29,7 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
                           cudaStream_t st);
 cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, const float* grasp, int64_t n, int64_t gofs,
-                      uint64_t seed, int iters, float damping, int n_seeds,
+                      uint64_t seed, int iters, float damping, int n_seeds, int32_t* list, int32_t* list_n,
                       cudaStream_t st);
 int particle_kernel_regs(int gs, int threads);
 int serial_kernel_regs();
@@ -72,7 +72,7 @@ struct tamp_ctx {
     char* base = nullptr;
     size_t ws_bytes = 0;
     // workspace offsets
-    size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, total;
+    size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, o_iklist, o_ikn, total;
     int64_t n_keys = 0;
     // shared-memory layout of the particle kernel (floats per particle)
     int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi, off_rsw;
@@ -728,6 +728,12 @@ static void ws_layout(tamp_ctx* c) {
     c->o_coords = take((size_t)3 * (D > 0 ? D : 1) * 4);
     c->o_counts = take((size_t)(TAMP_MAX_TERMS + 2) * 4);
     c->o_stage = take((size_t)1024 * (D + 4) * 4);
+    // IK restarts: per Kin conf, the list of particles whose first IK run did not converge (+ its length)
+    int n_kin = 0;
+    for (int f = 0; f < c->P.n_fk; ++f)
+        if ((c->P.fk[f].term_kp >= 0 || c->P.fk[f].term_kr >= 0) && !c->P.fk[f].ghost) ++n_kin;
+    c->o_iklist = take((size_t)n_kin * n * 4);
+    c->o_ikn = take((size_t)(n_kin > 0 ? n_kin : 1) * 4);
     c->total = o;
 }
 
@@ -1058,7 +1064,7 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(launch_sample(c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, st), "sample");
     CUDA_TRY(launch_ik(c->P, c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, c->ik_iters,
-                       c->ik_damping, c->ik_seeds, st),
+                       c->ik_damping, c->ik_seeds, c->at<int32_t>(c->o_iklist), c->at<int32_t>(c->o_ikn), st),
              "sample: IK");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero m");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero v");

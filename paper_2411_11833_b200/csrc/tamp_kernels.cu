@@ -209,45 +209,8 @@ __device__ __forceinline__ void ik_error(const M34& Ts, const M34& T, float (&e)
     epos = sqrtf(fmaf(e[0], e[0], fmaf(e[1], e[1], e[2] * e[2])));
 }
 
-template <int S>
-__global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, const KIkStreams Z, float* __restrict__ x,
-                                            const float* __restrict__ grasp, int64_t n, int64_t gofs, uint64_t seed,
-                                            int iters, float damp2) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int sd = (int)(threadIdx.x & (S - 1));          // restart index
-    const bool active = t / S < n;
-    const int64_t p = active ? t / S : n - 1;              // idle lanes mirror the last pair (shuffles below)
-    int fsel = -1, nth = 0;
-    for (int f = 0; f < P.n_fk && fsel < 0; ++f) {
-        if ((P.fk[f].term_kp < 0 && P.fk[f].term_kr < 0) || P.fk[f].ghost) continue;
-        if (nth++ == (int)blockIdx.y) fsel = f;
-    }
-    if (fsel < 0) return;                                   // block-uniform
-    const KFk K = P.fk[fsel];
-    float* xp = x + p * P.D;
-    // Kin target T* = T(p) T(g)
-    const KInst& I = P.inst[K.kin_inst];
-    float pp[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) pp[k] = I.xoff >= 0 ? xp[I.xoff + k] : I.pose[k];
-    float sy, cy;
-    fsincos(pp[3], &sy, &cy);
-    M34 Tp, Tg;
-    Tp.r[0] = cy; Tp.r[1] = -sy; Tp.r[2] = 0.f; Tp.r[3] = sy; Tp.r[4] = cy; Tp.r[5] = 0.f;
-    Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f; Tp.t[0] = pp[0]; Tp.t[1] = pp[1]; Tp.t[2] = pp[2];
-    load_m34(Tg, grasp + (p * P.n_grasp + K.kin_grasp) * 12);
-    const M34 Ts = compose(Tp, Tg);
-    float q[TAMP_NJ];
-    if (sd == 0) {
-#pragma unroll
-        for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];
-    } else {                                                // restart: a fresh uniform conf
-        float u[8];
-        uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd, u);
-        uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd + 1, u + 4);
-#pragma unroll
-        for (int j = 0; j < TAMP_NJ; ++j) q[j] = P.jlo[j] + u[j] * (P.jhi[j] - P.jlo[j]);
-    }
+// DLS iterations from q (in place)
+__device__ __forceinline__ void ik_iterate(const KProgram& P, const M34& Ts, float (&q)[TAMP_NJ], int iters, float damp2) {
     float z[TAMP_NJ][3], o[TAMP_NJ][3], e[6], epos, th;
     M34 T;
     for (int it = 0; it < iters; ++it) {
@@ -282,27 +245,123 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
             q[j] = fminf(fmaxf(q[j] + dq, P.jlo[j]), P.jhi[j]);
         }
     }
-    int keep = 0;
-    if (S > 1) {   // choose among the restarts: first converged, else the smallest epos + theta (lowest seed on ties)
-        ik_fk(P, q, T, z, o);
-        ik_error(Ts, T, e, epos, th);
-        const unsigned lane0 = threadIdx.x & 31 & ~(unsigned)(S - 1);
-        const unsigned conv = (__ballot_sync(FULL, epos <= kIkTolPos && th <= kIkTolRot) >> lane0) & ((1u << S) - 1u);
-        if (conv) {
-            keep = __ffs(conv) - 1;
-        } else {
-            float best = epos + th;
-            int bi = sd;
+}
+
+// final errors of q: converged (<= kIkTolPos, kIkTolRot) and the restart score e_pos + theta
+__device__ __forceinline__ bool ik_final(const KProgram& P, const M34& Ts, const float (&q)[TAMP_NJ], float& score) {
+    float z[TAMP_NJ][3], o[TAMP_NJ][3], e[6], epos, th;
+    M34 T;
+    ik_fk(P, q, T, z, o);
+    ik_error(Ts, T, e, epos, th);
+    score = epos + th;
+    return epos <= kIkTolPos && th <= kIkTolRot;
+}
+
+// the Kin conf of grid row blockIdx.y: its KFk and the target T* = T(p) T(g) of particle p
+__device__ __forceinline__ bool ik_target(const KProgram& P, const float* xp, const float* grasp, int64_t p, KFk& K, M34& Ts) {
+    int fsel = -1, nth = 0;
+    for (int f = 0; f < P.n_fk && fsel < 0; ++f) {
+        if ((P.fk[f].term_kp < 0 && P.fk[f].term_kr < 0) || P.fk[f].ghost) continue;
+        if (nth++ == (int)blockIdx.y) fsel = f;
+    }
+    if (fsel < 0) return false;
+    K = P.fk[fsel];
+    const KInst& I = P.inst[K.kin_inst];
+    float pp[4];
 #pragma unroll
-            for (int m = 1; m < S; m <<= 1) {
-                const float ob = __shfl_xor_sync(FULL, best, m, S);
-                const int oi = __shfl_xor_sync(FULL, bi, m, S);
-                if (ob < best || (ob == best && oi < bi) || (best != best && ob == ob)) { best = ob; bi = oi; }
-            }
-            keep = bi;
+    for (int k = 0; k < 4; ++k) pp[k] = I.xoff >= 0 ? xp[I.xoff + k] : I.pose[k];
+    float sy, cy;
+    fsincos(pp[3], &sy, &cy);
+    M34 Tp, Tg;
+    Tp.r[0] = cy; Tp.r[1] = -sy; Tp.r[2] = 0.f; Tp.r[3] = sy; Tp.r[4] = cy; Tp.r[5] = 0.f;
+    Tp.r[6] = 0.f; Tp.r[7] = 0.f; Tp.r[8] = 1.f; Tp.t[0] = pp[0]; Tp.t[1] = pp[1]; Tp.t[2] = pp[2];
+    load_m34(Tg, grasp + (p * P.n_grasp + K.kin_grasp) * 12);
+    Ts = compose(Tp, Tg);
+    return true;
+}
+
+// Stage A: restart 0 of every (particle, conf) pair from its uniform sample.  With restarts (list != nullptr),
+// pairs that did not converge are appended to the conf's list (warp-aggregated atomics; the order of a list
+// does not affect any result).
+__global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, float* __restrict__ x,
+                                            const float* __restrict__ grasp, int64_t n, int iters, float damp2,
+                                            int32_t* __restrict__ list, int32_t* __restrict__ list_n) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    float* xp = x + p * P.D;
+    KFk K;
+    M34 Ts;
+    if (!ik_target(P, xp, grasp, p, K, Ts)) return;
+    float q[TAMP_NJ];
+#pragma unroll
+    for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];
+    ik_iterate(P, Ts, q, iters, damp2);
+#pragma unroll
+    for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
+    if (list) {
+        float score;
+        const bool fail = !ik_final(P, Ts, q, score);
+        const unsigned m = __ballot_sync(__activemask(), fail);
+        if (fail) {
+            const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&list_n[blockIdx.y], __popc(m));
+            base = __shfl_sync(m, base, leader);
+            list[(int64_t)blockIdx.y * n + base + __popc(m & ((1u << lane) - 1u))] = (int32_t)p;
         }
     }
-    if (active && sd == keep) {
+}
+
+// Stage B: restarts 1 .. S-1 of the pairs restart 0 left unconverged, on S adjacent lanes (lane 0 re-scores the
+// restart-0 conf).  Kept: the first converged restart, else the smallest e_pos + theta (lowest index on ties);
+// the result equals running all S restarts of every pair and selecting the same way.
+template <int S>
+__global__ void __launch_bounds__(128) k_ik_restarts(const __grid_constant__ KProgram P, const KIkStreams Z,
+                                                     float* __restrict__ x, const float* __restrict__ grasp, int64_t n,
+                                                     int64_t gofs, uint64_t seed, int iters, float damp2,
+                                                     const int32_t* __restrict__ list, const int32_t* __restrict__ list_n) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int sd = (int)(threadIdx.x & (S - 1));
+    const int64_t cnt = list_n[blockIdx.y];
+    if ((int64_t)blockIdx.x * blockDim.x / S >= cnt) return;       // block-uniform: past the list
+    const bool active = t / S < cnt;
+    const int64_t e = active ? t / S : cnt - 1;                    // idle lanes mirror the last entry (shuffles)
+    const int64_t p = list[(int64_t)blockIdx.y * n + e];
+    float* xp = x + p * P.D;
+    KFk K;
+    M34 Ts;
+    if (!ik_target(P, xp, grasp, p, K, Ts)) return;
+    float q[TAMP_NJ];
+    if (sd == 0) {
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];   // restart 0's result (stage A)
+    } else {                                                         // restart: a fresh uniform conf
+        float u[8];
+        uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd, u);
+        uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd + 1, u + 4);
+#pragma unroll
+        for (int j = 0; j < TAMP_NJ; ++j) q[j] = P.jlo[j] + u[j] * (P.jhi[j] - P.jlo[j]);
+        ik_iterate(P, Ts, q, iters, damp2);
+    }
+    float score;
+    const bool conv = ik_final(P, Ts, q, score);
+    const unsigned lane0 = threadIdx.x & 31 & ~(unsigned)(S - 1);
+    const unsigned cm = (__ballot_sync(FULL, conv) >> lane0) & ((1u << S) - 1u);
+    int keep;
+    if (cm) {
+        keep = __ffs(cm) - 1;
+    } else {
+        float best = score;
+        int bi = sd;
+#pragma unroll
+        for (int m = 1; m < S; m <<= 1) {
+            const float ob = __shfl_xor_sync(FULL, best, m, S);
+            const int oi = __shfl_xor_sync(FULL, bi, m, S);
+            if (ob < best || (ob == best && oi < bi) || (best != best && ob == ob)) { best = ob; bi = oi; }
+        }
+        keep = bi;
+    }
+    if (active && sd == keep && keep != 0) {
 #pragma unroll
         for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
     }
@@ -448,29 +507,40 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
 int particle_kernel_regs(int gs, int threads) { return particle_kernel_regs_sm(gs, threads); }
 
 cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, const float* grasp, int64_t n, int64_t gofs,
-                      uint64_t seed, int iters, float damping, int n_seeds, cudaStream_t st) {
+                      uint64_t seed, int iters, float damping, int n_seeds, int32_t* list, int32_t* list_n,
+                      cudaStream_t st) {
     if (n <= 0 || iters <= 0) return cudaSuccess;
     KIkStreams Z;
     int n_kin = 0;
     for (int f = 0; f < P.n_fk; ++f) {
         if ((P.fk[f].term_kp < 0 && P.fk[f].term_kr < 0) || P.fk[f].ghost) continue;
         Z.stream[n_kin] = 0u;
-        for (int v = 0; v < SP.n_vars; ++v)      // the conf sampler that drew this conf (seed 0's start)
+        for (int v = 0; v < SP.n_vars; ++v)      // the conf sampler that drew this conf (restart 0's start)
             if (SP.v[v].kind == KS_CONF && SP.v[v].xoff == P.fk[f].xoff) Z.stream[n_kin] = SP.v[v].stream;
         ++n_kin;
     }
     const int per_block = 128 / kGroup;
     const unsigned bx = (unsigned)((n + per_block - 1) / per_block);
     if (n_kin > 0) {
-        const dim3 grid((unsigned)((n * n_seeds + 127) / 128), (unsigned)n_kin);
         const float d2 = damping * damping;
-        switch (n_seeds) {
-            case 8: k_ik<8><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
-            case 4: k_ik<4><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
-            case 2: k_ik<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
-            default: k_ik<1><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2); break;
+        const bool restarts = n_seeds > 1;
+        if (restarts) {
+            const cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int32_t) * n_kin, st);
+            if (e != cudaSuccess) return e;
         }
+        k_ik<<<dim3((unsigned)((n + 127) / 128), (unsigned)n_kin), 128, 0, st>>>(P, x, grasp, n, iters, d2,
+                                                                                restarts ? list : nullptr, list_n);
         counted();
+        if (restarts) {
+            // grid sized for the worst case (every pair unconverged); blocks past the list exit at once
+            const dim3 grid((unsigned)((n * n_seeds + 127) / 128), (unsigned)n_kin);
+            switch (n_seeds) {
+                case 8: k_ik_restarts<8><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, list, list_n); break;
+                case 4: k_ik_restarts<4><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, list, list_n); break;
+                default: k_ik_restarts<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, list, list_n); break;
+            }
+            counted();
+        }
     }
     if (P.n_traj > 0) {
         k_knots<<<bx, 128, 0, st>>>(P, x, n);
