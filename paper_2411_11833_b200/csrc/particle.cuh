@@ -403,6 +403,15 @@ struct TermSink {
     bool sat = true;
 };
 
+// Value of a term that is a sum of per-lane parts (collision hinges, containment): reduced over the group for
+// the check / eval, whose per-term values and J must be exact.  The optimisation step needs J only for its
+// finiteness test (the gradient is assembled separately), and the group ballot of that test sees a non-finite
+// part on any lane, so it keeps the parts lane-local and skips the shuffle chain.
+template <int MODE, int W>
+__device__ __forceinline__ float term_sum(float v) {
+    return MODE == MODE_OPT ? v : gsum<W>(v);
+}
+
 template <int MODE>
 __device__ __forceinline__ void finish_term(const KProgram& P, const KArgs& A, TermSink<MODE>& sink, int term,
                                             float val, int gl, bool active, int64_t p, int* s_counts,
@@ -668,7 +677,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                         }
                     }
                 }
-                finish_term<MODE>(P, A, sinkB, K.term_self, gsum<LPF>(js), ll, active, p, s_counts, real);
+                finish_term<MODE>(P, A, sinkB, K.term_self, term_sum<MODE, LPF>(js), ll, active, p, s_counts, real);
                 __syncwarp();
             }
             Wrench Wl[LPL];                   // wrench (about the world origin) on each of my links
@@ -722,7 +731,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
             }
             if (K.term_cf >= 0)
-                finish_term<MODE>(P, A, sinkB, K.term_cf, gsum<LPF>(jcf), ll, active, p, s_counts, real);
+                finish_term<MODE>(P, A, sinkB, K.term_cf, term_sum<MODE, LPF>(jcf), ll, active, p, s_counts, real);
 
             // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the segment
             if (K.term_kp >= 0 || K.term_kr >= 0) {
@@ -907,7 +916,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                         gq[u][1] += fmaf(sy, glx, cy * gly);
                     }
                 }
-                finish_term<MODE>(P, A, sink, Q.term_sc, gsum<GS>(e), gl, active, p, s_counts);
+                finish_term<MODE>(P, A, sink, Q.term_sc, term_sum<MODE, GS>(e), gl, active, p, s_counts);
             }
             // press contact (ValidPress / ValidStickPress, R8): min over the object's spheres of
             // dist_from_bounds(xy in the face frame, lo, hi); the subgradient goes to the arg-min sphere
@@ -963,7 +972,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                         [&](Wrench& pw) { flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl); },
                         smooth);
                 }
-                finish_term<MODE>(P, A, sink, Q.term_cp, gsum<GS>(jcp), gl, active, p, s_counts);
+                finish_term<MODE>(P, A, sink, Q.term_cp, term_sum<MODE, GS>(jcp), gl, active, p, s_counts);
             }
             if (GRAD) {
 #pragma unroll
