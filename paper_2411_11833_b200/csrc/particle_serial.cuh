@@ -321,7 +321,28 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         near = fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f;
                     }
                 }
-                if (near) {
+                if (near && one_obb && K.part_count == 0) {
+                    // one box, no partner instances (pick-place): the exact reject test of all of the link's
+                    // spheres first (straight-line code, independent chains), hinges and gradients only for those
+                    // that reach the box -- the others add exact zeros, so the result is unchanged
+                    const int ns = P.rsph_n[l];
+                    float wq[TAMP_MAX_SPHERES_PER_LINK][3], rq[TAMP_MAX_SPHERES_PER_LINK];
+                    bool hit[TAMP_MAX_SPHERES_PER_LINK];
+#pragma unroll
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                        const float4 c4 = s_rsph[l][k];
+                        xform(T, c4.x, c4.y, c4.z, wq[k][0], wq[k][1], wq[k][2]);
+                        rq[k] = c4.w;
+                        hit[k] = k < ns && obb_within(wq[k][0], wq[k][1], wq[k][2], rq[k], B0);
+                    }
+#pragma unroll
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                        if (!hit[k]) continue;
+                        float g[3] = {0.f, 0.f, 0.f};
+                        jcf += sphere_obb<GRAD>(wq[k][0], wq[k][1], wq[k][2], rq[k], B0, lam_cf, g[0], g[1], g[2], smooth);
+                        if (GRAD) sfx.add_point(wq[k][0], wq[k][1], wq[k][2], g[0], g[1], g[2]);
+                    }
+                } else if (near) {
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
                         const float4 c4 = s_rsph[l][k];
                         float wx, wy, wz;
