@@ -322,45 +322,34 @@ __device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], cons
     return j;
 }
 
-// NS query spheres per lane vs one OBB: branch-free reject (outside and |max(a,0)|^2 >= r^2), exact
-// hinge + gradient only if some sphere of the warp reaches the box.
+// NS query spheres per lane vs one OBB: the exact reject test of every sphere first (straight-line code,
+// independent chains), hinge + gradient only for spheres that reach the box, and nothing at all unless some
+// sphere of the warp does.  Small boxes are first gated by their bounding sphere.  Skipped spheres would add
+// exact zeros: results are unchanged.
 template <bool GRAD, int NS>
 __device__ __forceinline__ float spheres_vs_obb(const float (&w)[NS][3], const float (&rr)[NS], const KObb& B,
                                                 float lam, float (&g)[NS][3], float smooth) {
-    // a box larger than the arm's reach (the table): no broad phase / pre-test, which would rarely reject
-    if (B.rad >= kBroadMaxRad) {
-        float j = 0.f;
+    if (B.rad < kBroadMaxRad) {      // broad phase: bounding sphere of the box (not for boxes larger than the
+        float mb = 1.f;              // arm's reach, e.g. the table, where it would rarely reject)
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
-            j += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, g[k][0], g[k][1], g[k][2], smooth);
-        return j;
+        for (int k = 0; k < NS; ++k) {
+            const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
+            const float R = rr[k] + B.rad;
+            mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+        }
+        if (!__any_sync(FULL, mb < 0.f)) return 0.f;
     }
-    // broad phase: bounding sphere of the box
-    float mb = 1.f;
+    bool hit[NS], any = false;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-        const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
-        const float R = rr[k] + B.rad;
-        mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
-    }
-    if (!__any_sync(FULL, mb < 0.f)) return 0.f;
-    float mn = 1.f;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
-        const float px = fmaf(B.R[0], dx, B.R[3] * dy);
-        const float py = fmaf(B.R[1], dx, B.R[4] * dy);
-        const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(dz) - B.h[2];
-        const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
-        const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
-        const float mx = fmaxf(ax, fmaxf(ay, az));
-        mn = fminf(mn, mx > 0.f ? fmaf(-rr[k], rr[k], s) : -1.f);
+        hit[k] = obb_within(w[k][0], w[k][1], w[k][2], rr[k], B);
+        any = any || hit[k];
     }
     float j = 0.f;
-    if (__any_sync(FULL, mn < 0.f)) {
+    if (__any_sync(FULL, any)) {
 #pragma unroll
         for (int k = 0; k < NS; ++k)
-            j += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, g[k][0], g[k][1], g[k][2], smooth);
+            if (hit[k]) j += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, g[k][0], g[k][1], g[k][2], smooth);
     }
     return j;
 }
