@@ -782,7 +782,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     ejl[u] = ll * LPL + u < TAMP_NJ ? fmaxf(fmaxf(jlo[u] - q[u], q[u] - jhi[u]), 0.f) : 0.f;
                     e2 = fmaf(ejl[u], ejl[u], e2);
                 }
-                jl = sqrtf(gsum<LPF>(e2));
+                // inside the limits (always after the projection, L11) every part is 0: skip the shuffle chain
+                jl = __any_sync(FULL, e2 > 0.f) ? sqrtf(gsum<LPF>(e2)) : 0.f;
                 finish_term<MODE>(P, A, sinkB, K.term_jl, jl, ll, active, p, s_counts, real);
             }
             if (GRAD) {
