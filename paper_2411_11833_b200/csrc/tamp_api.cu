@@ -29,8 +29,8 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
 cudaError_t launch_sample(const KSampleProgram& SP, float* x, float* grasp, int64_t n, int64_t gofs, uint64_t seed,
                           cudaStream_t st);
 cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, const float* grasp, int64_t n, int64_t gofs,
-                      uint64_t seed, int iters, float damping, int n_seeds, int32_t* list, int32_t* list_n,
-                      cudaStream_t st);
+                      uint64_t seed, int iters, float damping, int n_seeds, int32_t* lists, int32_t* list_n,
+                      float* best, cudaStream_t st);
 int particle_kernel_regs(int gs, int threads);
 int serial_kernel_regs();
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
@@ -72,7 +72,7 @@ struct tamp_ctx {
     char* base = nullptr;
     size_t ws_bytes = 0;
     // workspace offsets
-    size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, o_iklist, o_ikn, total;
+    size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, o_iklist, o_ikn, o_ikbest, total;
     int64_t n_keys = 0;
     // shared-memory layout of the particle kernel (floats per particle)
     int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi, off_rsw;
@@ -732,8 +732,9 @@ static void ws_layout(tamp_ctx* c) {
     int n_kin = 0;
     for (int f = 0; f < c->P.n_fk; ++f)
         if ((c->P.fk[f].term_kp >= 0 || c->P.fk[f].term_kr >= 0) && !c->P.fk[f].ghost) ++n_kin;
-    c->o_iklist = take((size_t)n_kin * n * 4);
-    c->o_ikn = take((size_t)(n_kin > 0 ? n_kin : 1) * 4);
+    c->o_iklist = take((size_t)2 * n_kin * n * 4);                 // ping-pong lists of the restart rounds
+    c->o_ikn = take((size_t)(n_kin > 0 ? n_kin : 1) * 8 * 4);      // list lengths, <= 7 rounds + 1
+    c->o_ikbest = take((size_t)n_kin * n * 4);                     // best restart score so far
     c->total = o;
 }
 
@@ -1064,7 +1065,8 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CUDA_TRY(launch_sample(c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, st), "sample");
     CUDA_TRY(launch_ik(c->P, c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, c->ik_iters,
-                       c->ik_damping, c->ik_seeds, c->at<int32_t>(c->o_iklist), c->at<int32_t>(c->o_ikn), st),
+                       c->ik_damping, c->ik_seeds, c->at<int32_t>(c->o_iklist), c->at<int32_t>(c->o_ikn),
+                       c->at<float>(c->o_ikbest), st),
              "sample: IK");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero m");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero v");

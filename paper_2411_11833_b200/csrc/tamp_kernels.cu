@@ -19,6 +19,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "particle.cuh"
@@ -167,6 +168,7 @@ __device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float
 // profiles/README.md.)
 struct KIkStreams { uint32_t stream[TAMP_MAX_FK]; };   // Philox stream of each Kin conf's sampler
 constexpr float kIkTolPos = 1e-3f, kIkTolRot = 1e-3f;  // a restart counts as converged below both
+constexpr int kIkRestartsPerRound = 2;                   // restarts per pair and round of k_ik_restarts
 
 // tool pose of the chain at q, and the Kin errors to T*: e_pos = ||t* - t_ee||, theta = angle(R* R_ee^T)
 __device__ __forceinline__ void ik_fk(const KProgram& P, const float (&q)[TAMP_NJ], M34& T, float (&z)[TAMP_NJ][3],
@@ -285,7 +287,8 @@ __device__ __forceinline__ bool ik_target(const KProgram& P, const float* xp, co
 // does not affect any result).
 __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, float* __restrict__ x,
                                             const float* __restrict__ grasp, int64_t n, int iters, float damp2,
-                                            int32_t* __restrict__ list, int32_t* __restrict__ list_n) {
+                                            int32_t* __restrict__ list, int32_t* __restrict__ list_n,
+                                            float* __restrict__ best) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     float* xp = x + p * P.D;
@@ -308,62 +311,75 @@ __global__ void __launch_bounds__(128) k_ik(const __grid_constant__ KProgram P, 
             if (lane == leader) base = atomicAdd(&list_n[blockIdx.y], __popc(m));
             base = __shfl_sync(m, base, leader);
             list[(int64_t)blockIdx.y * n + base + __popc(m & ((1u << lane) - 1u))] = (int32_t)p;
+            best[(int64_t)blockIdx.y * n + p] = score;      // restart 0's score: the best so far
         }
     }
 }
 
-// Stage B: restarts 1 .. S-1 of the pairs restart 0 left unconverged, on S adjacent lanes (lane 0 re-scores the
-// restart-0 conf).  Kept: the first converged restart, else the smallest e_pos + theta (lowest index on ties);
-// the result equals running all S restarts of every pair and selecting the same way.
-template <int S>
+// Stage B, one round: restarts s0 .. s0+R-1 of the pairs still unconverged (list_in), on R adjacent lanes.  A
+// pair whose round has a converged restart keeps the first one and is done; otherwise the round's best restart
+// replaces the kept conf only if its score is strictly lower than the best so far (earlier restarts win ties,
+// a number beats NaN), and the pair goes on to the next round's list.  Rounds run in restart order, so the
+// result equals running all restarts of every pair and keeping the first converged, else the lowest score
+// (lowest index on ties), while most pairs stop after their first rounds.
+template <int R>
 __global__ void __launch_bounds__(128) k_ik_restarts(const __grid_constant__ KProgram P, const KIkStreams Z,
                                                      float* __restrict__ x, const float* __restrict__ grasp, int64_t n,
-                                                     int64_t gofs, uint64_t seed, int iters, float damp2,
-                                                     const int32_t* __restrict__ list, const int32_t* __restrict__ list_n) {
+                                                     int64_t gofs, uint64_t seed, int iters, float damp2, int s0,
+                                                     const int32_t* __restrict__ list_in, const int32_t* __restrict__ n_in,
+                                                     int32_t* __restrict__ list_out, int32_t* __restrict__ n_out,
+                                                     float* __restrict__ best) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int sd = (int)(threadIdx.x & (S - 1));
-    const int64_t cnt = list_n[blockIdx.y];
-    if ((int64_t)blockIdx.x * blockDim.x / S >= cnt) return;       // block-uniform: past the list
-    const bool active = t / S < cnt;
-    const int64_t e = active ? t / S : cnt - 1;                    // idle lanes mirror the last entry (shuffles)
-    const int64_t p = list[(int64_t)blockIdx.y * n + e];
+    const int sl = (int)(threadIdx.x & (R - 1));
+    const int sd = s0 + sl;                                         // restart index
+    const int64_t cnt = n_in[blockIdx.y];
+    if ((int64_t)blockIdx.x * blockDim.x / R >= cnt) return;       // block-uniform: past the list
+    const bool active = t / R < cnt;
+    const int64_t e = active ? t / R : cnt - 1;                    // idle lanes mirror the last entry (shuffles)
+    const int64_t p = list_in[(int64_t)blockIdx.y * n + e];
     float* xp = x + p * P.D;
     KFk K;
     M34 Ts;
     if (!ik_target(P, xp, grasp, p, K, Ts)) return;
     float q[TAMP_NJ];
-    if (sd == 0) {
-#pragma unroll
-        for (int j = 0; j < TAMP_NJ; ++j) q[j] = xp[K.xoff + j];   // restart 0's result (stage A)
-    } else {                                                         // restart: a fresh uniform conf
+    {
         float u[8];
         uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd, u);
         uniform4(seed, (uint64_t)(gofs + p), Z.stream[blockIdx.y], 2 * sd + 1, u + 4);
 #pragma unroll
         for (int j = 0; j < TAMP_NJ; ++j) q[j] = P.jlo[j] + u[j] * (P.jhi[j] - P.jlo[j]);
-        ik_iterate(P, Ts, q, iters, damp2);
     }
+    ik_iterate(P, Ts, q, iters, damp2);
     float score;
     const bool conv = ik_final(P, Ts, q, score);
-    const unsigned lane0 = threadIdx.x & 31 & ~(unsigned)(S - 1);
-    const unsigned cm = (__ballot_sync(FULL, conv) >> lane0) & ((1u << S) - 1u);
-    int keep;
-    if (cm) {
-        keep = __ffs(cm) - 1;
-    } else {
-        float best = score;
-        int bi = sd;
+    const unsigned lane0 = threadIdx.x & 31 & ~(unsigned)(R - 1);
+    const unsigned cm = (__ballot_sync(FULL, conv) >> lane0) & ((1u << R) - 1u);
+    if (cm) {                                                       // first converged restart of the round
+        if (active && sl == __ffs(cm) - 1) {
 #pragma unroll
-        for (int m = 1; m < S; m <<= 1) {
-            const float ob = __shfl_xor_sync(FULL, best, m, S);
-            const int oi = __shfl_xor_sync(FULL, bi, m, S);
-            if (ob < best || (ob == best && oi < bi) || (best != best && ob == ob)) { best = ob; bi = oi; }
+            for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
         }
-        keep = bi;
+        return;
     }
-    if (active && sd == keep && keep != 0) {
+    float bs = score;
+    int bi = sl;
+#pragma unroll
+    for (int m = 1; m < R; m <<= 1) {
+        const float ob = __shfl_xor_sync(FULL, bs, m, R);
+        const int oi = __shfl_xor_sync(FULL, bi, m, R);
+        if (ob < bs || (ob == bs && oi < bi) || (bs != bs && ob == ob)) { bs = ob; bi = oi; }
+    }
+    if (!active || sl != bi) return;
+    float* bp = best + (int64_t)blockIdx.y * n + p;
+    const float prev = *bp;
+    if (bs < prev || (prev != prev && bs == bs)) {
+        *bp = bs;
 #pragma unroll
         for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
+    }
+    if (list_out) {                                                 // still unconverged: next round
+        const int o = atomicAdd(&n_out[blockIdx.y], 1);
+        list_out[(int64_t)blockIdx.y * n + o] = (int32_t)p;
     }
 }
 
@@ -507,8 +523,8 @@ cudaError_t launch_particle(int mode, int gs, int bsync, int threads, const KPro
 int particle_kernel_regs(int gs, int threads) { return particle_kernel_regs_sm(gs, threads); }
 
 cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, const float* grasp, int64_t n, int64_t gofs,
-                      uint64_t seed, int iters, float damping, int n_seeds, int32_t* list, int32_t* list_n,
-                      cudaStream_t st) {
+                      uint64_t seed, int iters, float damping, int n_seeds, int32_t* lists, int32_t* list_n,
+                      float* best, cudaStream_t st) {
     if (n <= 0 || iters <= 0) return cudaSuccess;
     KIkStreams Z;
     int n_kin = 0;
@@ -524,21 +540,28 @@ cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, con
     if (n_kin > 0) {
         const float d2 = damping * damping;
         const bool restarts = n_seeds > 1;
+        // lists[2][n_kin][n] (ping-pong), list_n[rounds + 1][n_kin]
+        const int rounds = restarts ? (n_seeds - 1 + kIkRestartsPerRound - 1) / kIkRestartsPerRound : 0;
         if (restarts) {
-            const cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int32_t) * n_kin, st);
+            const cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int32_t) * n_kin * (rounds + 1), st);
             if (e != cudaSuccess) return e;
         }
         k_ik<<<dim3((unsigned)((n + 127) / 128), (unsigned)n_kin), 128, 0, st>>>(P, x, grasp, n, iters, d2,
-                                                                                restarts ? list : nullptr, list_n);
+                                                                                restarts ? lists : nullptr, list_n, best);
         counted();
-        if (restarts) {
+        for (int r = 0; r < rounds; ++r) {
+            const int s0 = 1 + r * kIkRestartsPerRound;
+            const int R = std::min(kIkRestartsPerRound, n_seeds - s0);
+            int32_t* lin = lists + (size_t)(r & 1) * n_kin * n;
+            int32_t* lout = r + 1 < rounds ? lists + (size_t)((r + 1) & 1) * n_kin * n : nullptr;
             // grid sized for the worst case (every pair unconverged); blocks past the list exit at once
-            const dim3 grid((unsigned)((n * n_seeds + 127) / 128), (unsigned)n_kin);
-            switch (n_seeds) {
-                case 8: k_ik_restarts<8><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, list, list_n); break;
-                case 4: k_ik_restarts<4><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, list, list_n); break;
-                default: k_ik_restarts<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, list, list_n); break;
-            }
+            const dim3 grid((unsigned)((n * R + 127) / 128), (unsigned)n_kin);
+            if (R == 2)
+                k_ik_restarts<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, s0, lin, list_n + r * n_kin,
+                                                       lout, list_n + (r + 1) * n_kin, best);
+            else
+                k_ik_restarts<1><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, s0, lin, list_n + r * n_kin,
+                                                       lout, list_n + (r + 1) * n_kin, best);
             counted();
         }
     }
