@@ -326,7 +326,7 @@ template <int R>
 __global__ void __launch_bounds__(128) k_ik_restarts(const __grid_constant__ KProgram P, const KIkStreams Z,
                                                      float* __restrict__ x, const float* __restrict__ grasp, int64_t n,
                                                      int64_t gofs, uint64_t seed, int iters, float damp2, int s0,
-                                                     const int32_t* __restrict__ list_in, const int32_t* __restrict__ n_in,
+                                                     int s_end, const int32_t* __restrict__ list_in, const int32_t* __restrict__ n_in,
                                                      int32_t* __restrict__ list_out, int32_t* __restrict__ n_out,
                                                      float* __restrict__ best) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(128) k_ik_restarts(const __grid_constant__ KPr
     KFk K;
     M34 Ts;
     if (!ik_target(P, xp, grasp, p, K, Ts)) return;
+    const bool valid = sd < s_end;                                  // lanes past the last restart pad the round
     float q[TAMP_NJ];
     {
         float u[8];
@@ -349,9 +350,12 @@ __global__ void __launch_bounds__(128) k_ik_restarts(const __grid_constant__ KPr
 #pragma unroll
         for (int j = 0; j < TAMP_NJ; ++j) q[j] = P.jlo[j] + u[j] * (P.jhi[j] - P.jlo[j]);
     }
-    ik_iterate(P, Ts, q, iters, damp2);
-    float score;
-    const bool conv = ik_final(P, Ts, q, score);
+    float score = INFINITY;
+    bool conv = false;
+    if (valid) {
+        ik_iterate(P, Ts, q, iters, damp2);
+        conv = ik_final(P, Ts, q, score);
+    }
     const unsigned lane0 = threadIdx.x & 31 & ~(unsigned)(R - 1);
     const unsigned cm = (__ballot_sync(FULL, conv) >> lane0) & ((1u << R) - 1u);
     if (cm) {                                                       // first converged restart of the round
@@ -361,18 +365,20 @@ __global__ void __launch_bounds__(128) k_ik_restarts(const __grid_constant__ KPr
         }
         return;
     }
-    float bs = score;
+    // the round's best restart: smallest score (NaN and padding lanes count as +inf), lowest index on ties --
+    // a total order, so exactly one lane of the pair wins
+    float bs = score == score ? score : INFINITY;
     int bi = sl;
 #pragma unroll
     for (int m = 1; m < R; m <<= 1) {
         const float ob = __shfl_xor_sync(FULL, bs, m, R);
         const int oi = __shfl_xor_sync(FULL, bi, m, R);
-        if (ob < bs || (ob == bs && oi < bi) || (bs != bs && ob == ob)) { bs = ob; bi = oi; }
+        if (ob < bs || (ob == bs && oi < bi)) { bs = ob; bi = oi; }
     }
     if (!active || sl != bi) return;
     float* bp = best + (int64_t)blockIdx.y * n + p;
-    const float prev = *bp;
-    if (bs < prev || (prev != prev && bs == bs)) {
+    const float prev = *bp == *bp ? *bp : INFINITY;
+    if (bs < prev) {
         *bp = bs;
 #pragma unroll
         for (int j = 0; j < TAMP_NJ; ++j) xp[K.xoff + j] = q[j];
@@ -540,8 +546,10 @@ cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, con
     if (n_kin > 0) {
         const float d2 = damping * damping;
         const bool restarts = n_seeds > 1;
-        // lists[2][n_kin][n] (ping-pong), list_n[rounds + 1][n_kin]
-        const int rounds = restarts ? (n_seeds - 1 + kIkRestartsPerRound - 1) / kIkRestartsPerRound : 0;
+        // lists[2][n_kin][n] (ping-pong), list_n[rounds + 1][n_kin]; rounds of 2 restarts (rounds of 4 measured
+        // no faster at config 2 and slower for 64K-1M pairs: most pairs converge within their first restarts)
+        const int per_round = kIkRestartsPerRound;
+        const int rounds = restarts ? (n_seeds - 1 + per_round - 1) / per_round : 0;
         if (restarts) {
             const cudaError_t e = cudaMemsetAsync(list_n, 0, sizeof(int32_t) * n_kin * (rounds + 1), st);
             if (e != cudaSuccess) return e;
@@ -550,18 +558,18 @@ cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, con
                                                                                 restarts ? lists : nullptr, list_n, best);
         counted();
         for (int r = 0; r < rounds; ++r) {
-            const int s0 = 1 + r * kIkRestartsPerRound;
-            const int R = std::min(kIkRestartsPerRound, n_seeds - s0);
+            const int s0 = 1 + r * per_round;
+            const int R = n_seeds - s0 >= 2 ? 2 : 1;
             int32_t* lin = lists + (size_t)(r & 1) * n_kin * n;
             int32_t* lout = r + 1 < rounds ? lists + (size_t)((r + 1) & 1) * n_kin * n : nullptr;
             // grid sized for the worst case (every pair unconverged); blocks past the list exit at once
             const dim3 grid((unsigned)((n * R + 127) / 128), (unsigned)n_kin);
-            if (R == 2)
-                k_ik_restarts<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, s0, lin, list_n + r * n_kin,
-                                                       lout, list_n + (r + 1) * n_kin, best);
+            int32_t* nin = list_n + r * n_kin;
+            int32_t* nout = list_n + (r + 1) * n_kin;
+            if (R >= 2)
+                k_ik_restarts<2><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, s0, n_seeds, lin, nin, lout, nout, best);
             else
-                k_ik_restarts<1><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, s0, lin, list_n + r * n_kin,
-                                                       lout, list_n + (r + 1) * n_kin, best);
+                k_ik_restarts<1><<<grid, 128, 0, st>>>(P, Z, x, grasp, n, gofs, seed, iters, d2, s0, n_seeds, lin, nin, lout, nout, best);
             counted();
         }
     }
