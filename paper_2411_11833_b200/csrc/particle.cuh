@@ -1080,16 +1080,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             for (int d = gl; d < D; d += GS) bad |= !isfinite(gs[d]);
             bad = ((__ballot_sync(FULL, bad) >> (threadIdx.x & 31 & ~(GS - 1))) & ((1u << GS) - 1u)) != 0u;   // my group
             invalid = invalid || bad;
-            const float bc1 = A.bc1[it];
-            const float bc2 = A.bc2[it];
+            const float rbc1 = A.rbc1[it];
+            const float rbc2 = A.rbc2[it];
             if (!invalid) {
                 for (int d = gl; d < D; d += GS) {
                     const float g = gs[d] * P.grad_scale;
                     const float mm = fmaf(P.beta1, A.m[p * D + d], (1.f - P.beta1) * g);
                     const float vv = fmaf(P.beta2, A.v[p * D + d], (1.f - P.beta2) * g * g);
                     if (active) { A.m[p * D + d] = mm; A.v[p * D + d] = vv; }
-                    const float mh = mm / bc1;
-                    const float vh = vv / bc2;
+                    const float mh = mm * rbc1;
+                    const float vh = vv * rbc2;
                     const float xn = xs[d] - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
                     xs[d] = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
                 }

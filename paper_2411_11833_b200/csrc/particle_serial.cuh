@@ -9,8 +9,8 @@
 // backward sweep over the links 8 -> 1 recovering T_{l-1} = T_l Rz(-q_l) F_l^{-1} while it evaluates
 // that link's spheres and accumulates the suffix wrench (F, M) of all links >= l, so that
 // dJ/dq_l = z_l . (M - o_l x F) is available exactly when joint l is reached.
-// Per-thread state (x, gradient, grasps, instance poses and wrenches) lives in shared memory in
-// thread-major columns (value f of thread t at [f * blockDim + t]: conflict-free).
+// Per-thread state (x, Adam moments, gradient, grasps, instance poses and wrenches) lives in shared memory, one
+// row per thread (field f of thread t at [t * pitch + f], pitch odd: a warp reading one field is conflict-free).
 // Supported: every term except SELF and held objects at knots (tamp_api.cu selects the lane mapping then).
 #pragma once
 #include "particle.cuh"
@@ -38,10 +38,13 @@ __host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool mv
 
 constexpr int kSerialThreads = 512;   // launch bound (blocks of <= 512 threads, <= 128 registers)
 
-// dynamic shared memory of a serial-mapping block of `threads` particles (column pitch threads + 1: the
-// cooperative row <-> column transposes hit distinct banks)
+// floats per thread row of the shared-memory state: the layout's size rounded up to odd, so that the 32 threads
+// of a warp reading the same field (stride = row pitch) hit 32 distinct banks
+__host__ __device__ inline int serial_row_pitch(const SerialLayout& L) { return L.n | 1; }
+
+// dynamic shared memory of a serial-mapping block of `threads` particles (one row per thread)
 __host__ __device__ inline size_t serial_smem_bytes(const KProgram& P, int threads, bool mv) {
-    return (size_t)serial_layout(P, mv).n * (threads + 1) * sizeof(float);
+    return (size_t)serial_row_pitch(serial_layout(P, mv)) * threads * sizeof(float);
 }
 
 // term bookkeeping: warp-aggregated counts (every thread of the warp calls it for the same term)
@@ -73,9 +76,12 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     const int64_t p = active ? pid : (A.n - 1);
     const SerialLayout L = serial_layout(P, MODE == MODE_OPT);
     const int D = P.D;
-    const int PITCH = NT + 1;
-    auto col = [&](int f) -> float& { return S[f * PITCH + tid]; };
-    // block-cooperative, coalesced copy between the block's rows of a [n][w] array and columns c0..c0+w
+    // per-thread state rows (odd pitch: a warp reading one field of its 32 rows is conflict-free); every field
+    // access is my row base + a warp-uniform offset
+    const int ROWP = serial_row_pitch(L);
+    float* const Sr = S + tid * ROWP;
+    auto col = [&](int f) -> float& { return Sr[f]; };
+    // block-cooperative, coalesced copy between the block's rows of a [n][w] array and fields c0..c0+w of the rows
     const int64_t row0 = (int64_t)blockIdx.x * NT;
     const int nrows = (int)min((int64_t)NT, A.n - row0);
     // element e = row * w + c of the block's rows; (row, c) advanced incrementally (no division per element)
@@ -84,7 +90,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         const int dq = NT / w, dr = NT % w;
         int q = tid / w, r = tid % w;
         for (int e = tid; e < nrows * w; e += NT) {
-            S[(c0 + r) * PITCH + q] = base[e];
+            S[q * ROWP + c0 + r] = base[e];
             q += dq; r += dr;
             if (r >= w) { r -= w; ++q; }
         }
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         const int dq = NT / w, dr = NT % w;
         int q = tid / w, r = tid % w;
         for (int e = tid; e < nrows * w; e += NT) {
-            base[e] = S[(c0 + r) * PITCH + q];
+            base[e] = S[q * ROWP + c0 + r];
             q += dq; r += dr;
             if (r >= w) { r -= w; ++q; }
         }
@@ -578,8 +584,8 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             bool bad = !isfinite(Jtot);
             for (int d = 0; d < D; ++d) bad |= !isfinite(gs(d));
             invalid = invalid || bad;
-            const float bc1 = A.bc1[it];
-            const float bc2 = A.bc2[it];
+            const float rbc1 = A.rbc1[it];
+            const float rbc2 = A.rbc2[it];
             if (!invalid) {
                 for (int d = 0; d < D; ++d) {
                     const float g = gs(d) * P.grad_scale;
@@ -587,8 +593,8 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     const float vv = fmaf(P.beta2, col(L.v + d), (1.f - P.beta2) * g * g);
                     col(L.m + d) = mm;
                     col(L.v + d) = vv;
-                    const float mh = mm / bc1;
-                    const float vh = vv / bc2;
+                    const float mh = mm * rbc1;
+                    const float vh = vv * rbc2;
                     const float xn = xs(d) - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
                     xs(d) = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
                 }

@@ -1090,8 +1090,8 @@ tamp_status tamp_optimize_step(tamp_ctx* c, int32_t n_steps, void* stream) {
         A.t0 = c->t;
         for (int i = 0; i < k; ++i) {   // Adam bias corrections (Kingma & Ba): 1 - beta^t, t = t0 + i + 1
             const double t = (double)(c->t + i + 1);
-            A.bc1[i] = (float)(1.0 - std::pow((double)c->P.beta1, t));
-            A.bc2[i] = (float)(1.0 - std::pow((double)c->P.beta2, t));
+            A.rbc1[i] = (float)(1.0 / (1.0 - std::pow((double)c->P.beta1, t)));
+            A.rbc2[i] = (float)(1.0 / (1.0 - std::pow((double)c->P.beta2, t)));
         }
         CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->bsync, c->threads, c->P, A, c->smem,
                                  static_cast<cudaStream_t>(stream)), "optimize");
