@@ -420,6 +420,7 @@ __device__ __forceinline__ unsigned long long make_key(int cls, float cost, int6
 }
 
 constexpr int kSortChunk = 2048;
+constexpr int kSortChunkSmall = 256;
 
 // keys from the check pass (payload = local particle index)
 __global__ void k_make_keys(const uint8_t* __restrict__ cls, const float* __restrict__ cost, int64_t n, int64_t gofs,
@@ -442,29 +443,29 @@ __global__ void k_record_keys(const float* __restrict__ rec, int32_t n, int32_t 
 }
 
 // Sort each chunk of kSortChunk (key, payload) pairs ascending and keep its first k.
-__global__ void __launch_bounds__(1024) k_sort_chunk(const unsigned long long* __restrict__ kin, const int32_t* __restrict__ pin,
+template <int C>   // chunk size (power of two); C / 2 threads, one compare-exchange each per stage
+__global__ void __launch_bounds__(C / 2) k_sort_chunk(const unsigned long long* __restrict__ kin, const int32_t* __restrict__ pin,
                                                      int64_t n, int k, unsigned long long* __restrict__ kout,
                                                      int32_t* __restrict__ pout) {
-    __shared__ unsigned long long sk[kSortChunk];
-    __shared__ int32_t sp[kSortChunk];
-    const int64_t base = (int64_t)blockIdx.x * kSortChunk;
-    for (int i = threadIdx.x; i < kSortChunk; i += blockDim.x) {
+    __shared__ unsigned long long sk[C];
+    __shared__ int32_t sp[C];
+    const int64_t base = (int64_t)blockIdx.x * C;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) {
         const int64_t g = base + i;
         sk[i] = g < n ? kin[g] : ~0ull;
         sp[i] = g < n ? pin[g] : -1;
     }
     __syncthreads();
-    for (int size = 2; size <= kSortChunk; size <<= 1) {
+    for (int size = 2; size <= C; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < kSortChunk / 2; i += blockDim.x) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = ((lo & size) == 0);
-                const unsigned long long a = sk[lo], b = sk[hi];
-                if ((a > b) == up) {
-                    sk[lo] = b; sk[hi] = a;
-                    const int32_t t = sp[lo]; sp[lo] = sp[hi]; sp[hi] = t;
-                }
+            const int i = threadIdx.x;
+            const int lo = 2 * i - (i & (stride - 1));
+            const int hi = lo + stride;
+            const bool up = ((lo & size) == 0);
+            const unsigned long long a = sk[lo], b = sk[hi];
+            if ((a > b) == up) {
+                sk[lo] = b; sk[hi] = a;
+                const int32_t t = sp[lo]; sp[lo] = sp[hi]; sp[hi] = t;
             }
             __syncthreads();
         }
@@ -594,11 +595,17 @@ cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long*
     unsigned long long *ki = ka, *ko = kb;
     int32_t *pi = pa, *po = pb;
     int64_t cnt = n;
+    // small k: 256-key chunks (36 short block-barrier stages, many blocks per pass); else 2048-key chunks
+    const bool small = k <= kSortChunkSmall / 4;
+    const int64_t C = small ? kSortChunkSmall : kSortChunk;
     do {
-        const int64_t chunks = (cnt + kSortChunk - 1) / kSortChunk;
+        const int64_t chunks = (cnt + C - 1) / C;
         const int keep = (int)(cnt < k ? cnt : k);
-        k_sort_chunk<<<(unsigned)chunks, 1024, 0, st>>>(ki, pi, cnt, keep, ko, po);
-    counted();
+        if (small)
+            k_sort_chunk<kSortChunkSmall><<<(unsigned)chunks, kSortChunkSmall / 2, 0, st>>>(ki, pi, cnt, keep, ko, po);
+        else
+            k_sort_chunk<kSortChunk><<<(unsigned)chunks, kSortChunk / 2, 0, st>>>(ki, pi, cnt, keep, ko, po);
+        counted();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         cnt = chunks * keep;
