@@ -509,13 +509,14 @@ def test_ik_restarts_one_iteration_match_oracle():
     np.testing.assert_allclose(x[clear, off:off + 7], xo[clear, off:off + 7], rtol=1e-3, atol=1e-3)
 
 
-def test_ik_restarts_converged_match_oracle():
-    """20 iterations x 8 restarts on the Tetris-4 skeleton (R6): wherever the oracle keeps a converged restart
-    with no earlier restart near the 1e-3 threshold, the GPU keeps a converged conf too (Kin residual < 1e-4);
-    the fraction of particles whose confs satisfy Kin agrees, and rises well above the single-seed sampler's."""
+@pytest.mark.parametrize("seeds", [2, 4, 8])
+def test_ik_restarts_converged_match_oracle(seeds):
+    """20 iterations x 2 / 4 / 8 restarts on the Tetris-4 skeleton (R6; 1, 2 and 4 restart rounds on the GPU):
+    wherever the oracle keeps a converged restart with no earlier restart near the 1e-3 threshold, the GPU keeps
+    a converged conf too; the fraction of particles whose confs satisfy Kin agrees."""
     n = 256
     spec = make_config(3, n=n)
-    spec.ik_iters, spec.ik_seeds = 20, 8
+    spec.ik_iters, spec.ik_seeds = 20, seeds
     csp = O.build_csp(spec)
     ctx = TampContext(spec, n)
     ctx.sample(seed=710)
@@ -531,14 +532,14 @@ def test_ik_restarts_converged_match_oracle():
     unamb = (first >= 0) & np.array([not near[:first[i] + 1, i].any() for i in range(n)])
     kp = [i for i, t in enumerate(csp.terms) if t.kind == "KP"]
     t0 = [i for i in kp if csp.terms[i].action == spec.actions.index(a)] if hasattr(csp.terms[0], "action") else kp[:1]
-    assert unamb.mean() > 0.6, unamb.mean()
+    assert unamb.mean() > {2: 0.3, 4: 0.45, 8: 0.6}[seeds], unamb.mean()
     reached = Jc[unamb, t0[0]] <= 1.2e-3                                  # kept restart converged (<= 1e-3 m)
     assert reached.mean() >= 0.95, (reached.mean(), np.sort(Jc[unamb, t0[0]])[-10:])
     kin = [i for i, t in enumerate(csp.terms) if t.kind in ("KP", "KR")]
     eps = np.array([spec.eps[csp.terms[i].kind] for i in kin])
     ok_gpu = np.all(Jc[:, kin] <= eps, axis=1).mean()
     ok_or = np.all(Jco[:, kin] <= eps, axis=1).mean()
-    assert abs(ok_gpu - ok_or) < 0.08 and ok_or > 0.3, (ok_gpu, ok_or)
+    assert abs(ok_gpu - ok_or) < 0.08 and ok_or > (0.3 if seeds == 8 else 0.02), (ok_gpu, ok_or)
 
 
 @pytest.mark.parametrize("lanes", [4, 8, 16])
