@@ -496,12 +496,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
 
     // particle state -> shared memory
     const float* xg = A.x + p * D;
+#pragma unroll 4
     for (int d = gl; d < D; d += GS) xs[d] = xg[d];
-    for (int i = gl; i < P.n_grasp * 12; i += GS) gT[(i / 12) * 16 + (i % 12)] = A.grasp[(p * P.n_grasp) * 12 + i];
+    const float* gg = A.grasp + (p * P.n_grasp) * 12;
+#pragma unroll 4
+    for (int i = gl; i < P.n_grasp * 12; i += GS) gT[(i / 12) * 16 + (i % 12)] = gg[i];
     bool invalid = A.invalid[p] != 0;
     __syncthreads();
-    if (gl == 0) {
-        for (int k = 0; k < P.n_grasp; ++k) {
+    {   // inverse grasps (held objects at knots): one grasp per lane of the group
+        for (int k = gl; k < P.n_grasp; k += GS) {
             M34 g, gi;
             load_m34(g, gT + 16 * k);
             inv_m34(g, gi);
