@@ -37,9 +37,25 @@ def up_to_date():
 
 
 def build(force=False, verbose=False):
-    """Compile csrc/*.cu into paper_2411_11833_b200/libtamp.so (sm_100a).  Returns the path."""
+    """Compile csrc/*.cu into paper_2411_11833_b200/libtamp.so (sm_100a).  Returns the path.
+
+    Serialised by an exclusive file lock: concurrent callers (one process per GPU under torchrun, pytest
+    workers) wait for the first one's build instead of writing the same objects."""
     if not force and up_to_date():
         return LIB
+    import fcntl
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    with open(os.path.join(OBJ_DIR, ".lock"), "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            if not force and up_to_date():     # built by another process while we waited
+                return LIB
+            return _build(verbose)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
+
+
+def _build(verbose=False):
     os.makedirs(OBJ_DIR, exist_ok=True)
     objs = [os.path.join(OBJ_DIR, os.path.basename(s)[:-3] + ".o") for s in SRCS]
     procs = [subprocess.Popen([nvcc()] + NVCC_FLAGS + (FAST_DIV_SQRT if os.path.basename(s) in FAST_UNITS else [])
