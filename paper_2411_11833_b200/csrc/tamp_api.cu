@@ -730,8 +730,9 @@ static void ws_layout(tamp_ctx* c) {
     c->o_stage = take((size_t)1024 * (D + 4) * 4);
     // IK restarts: per Kin conf, the list of particles whose first IK run did not converge (+ its length)
     int n_kin = 0;
-    for (int f = 0; f < c->P.n_fk; ++f)
-        if ((c->P.fk[f].term_kp >= 0 || c->P.fk[f].term_kr >= 0) && !c->P.fk[f].ghost) ++n_kin;
+    if (c->ik_iters > 0 && c->ik_seeds > 1)
+        for (int f = 0; f < c->P.n_fk; ++f)
+            if ((c->P.fk[f].term_kp >= 0 || c->P.fk[f].term_kr >= 0) && !c->P.fk[f].ghost) ++n_kin;
     c->o_iklist = take((size_t)2 * n_kin * n * 4);                 // ping-pong lists of the restart rounds
     c->o_ikn = take((size_t)(n_kin > 0 ? n_kin : 1) * 8 * 4);      // list lengths, <= 7 rounds + 1
     c->o_ikbest = take((size_t)n_kin * n * 4);                     // best restart score so far
@@ -811,6 +812,8 @@ tamp_status tamp_query_workspace(const tamp_problem_desc* desc, int64_t n_local,
     if (s != TAMP_OK) return s;
     tmp.P = C.P;
     tmp.n = n_local;
+    tmp.ik_iters = desc->ik_iters;
+    tmp.ik_seeds = desc->ik_seeds ? desc->ik_seeds : 1;
     ws_layout(&tmp);
     *bytes = tmp.total;
     return TAMP_OK;
