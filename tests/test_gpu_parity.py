@@ -165,6 +165,25 @@ def test_best_k_exact_on_gpu_costs_and_oracle_order():
         np.testing.assert_array_equal(gidx, sel_o + gofs)
 
 
+@pytest.mark.parametrize("n,k", [(70000, 16), (70000, 64), (9000, 65), (5000, 1024), (300, 300)])
+def test_best_k_sizes_exact(n, k):
+    """best-k across the sort paths (256-key chunks for k <= 64, 2048-key chunks above; several passes; k = n):
+    the selected global indices equal a CPU lexsort of the GPU's own (class, cost, index) keys."""
+    spec = make_config(2, n=n)
+    ctx = TampContext(spec, n, global_offset=123, n_global=n + 123)
+    ctx.sample(seed=77)
+    ctx.optimize(3)
+    rec = ctx.best_k(k)
+    _, _, gidx, _ = decode_records(rec)
+    clsg = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ctx.check(cls=clsg)
+    J, soft, _, _ = ctx.eval()
+    c = clsg.cpu().numpy()
+    costg = np.where(c == 0, soft.cpu().numpy(), np.where(c == 1, J.cpu().numpy(), 0.0)).astype(np.float32)
+    order = np.lexsort((np.arange(n), costg, c))[:k]
+    np.testing.assert_array_equal(gidx, order + 123)
+
+
 def test_merge_best_k_equals_global_best_k():
     """all-gather emulation: per-rank best-k records merged == best-k over the union."""
     cfg, n, k = 1, 256, 8
