@@ -250,6 +250,12 @@ tamp_status tamp_optimize_step(tamp_ctx* ctx, int32_t n_steps, void* stream);
    cls [n_local] u8 and counts [n_hard + 2] i32: device or host. */
 tamp_status tamp_check_satisfied(tamp_ctx* ctx, uint8_t* cls, int32_t* counts, void* stream);
 
+/* tamp_optimize_step(n_steps) followed by tamp_check_satisfied, as one call (Alg. 1's optimise-then-check
+   interval): identical results; with the link mappings the check of the final state runs inside
+   the last optimisation launch (no second launch re-loading the state).  n_steps >= 1; cls may be NULL;
+   buffers as for tamp_check_satisfied. */
+tamp_status tamp_optimize_and_check(tamp_ctx* ctx, int32_t n_steps, uint8_t* cls, int32_t* counts, void* stream);
+
 /* Best k particles of this rank (GetSatisfyingParticles) at the current x, sorted by
    key (class, cost, global index) ascending, cost = soft plan cost if satisfying else J.
    records [k][D + 4] floats (device or host): [class, cost, global_idx_lo, global_idx_hi

@@ -6,6 +6,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "tamp_program.h"
 
 namespace tamp {
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
         s_osph[o][k] = make_float4(P.osph[o][k][0], P.osph[o][k][1], P.osph[o][k][2], P.osph[o][k][3]);
     }
-    if (MODE == MODE_CHECK)
+    if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
     if (threadIdx.x < kGroup * 3) {
         const int l = threadIdx.x / 3, r = threadIdx.x % 3;
@@ -519,8 +521,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     __syncwarp();
 
     const int n_iter = (MODE == MODE_OPT) ? A.n_steps : 1;
-    for (int it = 0; it < n_iter; ++it) {
-        TermSink<MODE> sink;
+    // one optimisation / check / eval iteration; M = MODE, or MODE_CHECK for the check fused after the last step
+    auto iteration = [&](auto mtag, const int it) {
+        constexpr int M = decltype(mtag)::value;
+        constexpr bool G = M != MODE_CHECK;
+        TermSink<M> sink;
         float soft = 0.f;
 
         // ---- phase A: object instances (poses, world sphere centres), zero accumulators ----
@@ -549,17 +554,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     ? make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w)
                     : make_float4(kFar, kFar, kFar, 0.f);
             }
-            if (GRAD)
+            if (G)
                 for (int c = gl; c < 6; c += GS) iwr[8 * i + c] = 0.f;
         }
-        if (GRAD) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
+        if (G) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
         __syncwarp();
 
         // ---- phase B: robot configurations (Pick/Place confs, knots) ----
         // HP = 2: the two halves process the two FK instances of a pair of identical structure concurrently
         // (the compiler pairs them; an unmatched instance is paired with a ghost copy whose results are
         // discarded), so control flow stays warp-uniform.  HP = 1: ghosts are skipped.
-        TermSink<MODE> sinkB;                  // this half's share of the phase-B terms
+        TermSink<M> sinkB;                  // this half's share of the phase-B terms
         for (int f0 = 0; f0 < P.n_fk; f0 += HP) {
             const KFk K = P.fk[f0 + (HP > 1 ? half : 0)];
             const bool real = !K.ghost;
@@ -615,12 +620,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             if (K.term_cf >= 0) {
                 // robot spheres vs OBBs (constant cache)
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, NS>(w, rr, P.obb[b], lam_cf, gw, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS>(w, rr, P.obb[b], lam_cf, gw, smooth);
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    jcf += pairs_vs_instance<GRAD, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw,
-                        [&](Wrench& pw) { flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); },
+                    jcf += pairs_vs_instance<G, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw,
+                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); },
                         smooth);
                 }
             }
@@ -662,21 +667,21 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                             const int t = __ffs(m) - 1;
                             m &= m - 1u;
                             float ux, uy, uz;
-                            const float pen = sphere_sphere<GRAD>(w[s][0], w[s][1], w[s][2], rr[s], rsw[t], lam_self, ux, uy, uz,
+                            const float pen = sphere_sphere<G>(w[s][0], w[s][1], w[s][2], rr[s], rsw[t], lam_self, ux, uy, uz,
                                                                   smooth);
                             if (sid < t) js += pen;
-                            if (GRAD) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
+                            if (G) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
                         }
                     }
                 }
-                finish_term<MODE>(P, A, sinkB, K.term_self, term_sum<MODE, LPF>(js), ll, active, p, s_counts, real);
+                finish_term<M>(P, A, sinkB, K.term_self, term_sum<M, LPF>(js), ll, active, p, s_counts, real);
                 __syncwarp();
             }
             Wrench Wl[LPL];                   // wrench (about the world origin) on each of my links
 #pragma unroll
             for (int u = 0; u < LPL; ++u) {
                 Wl[u].zero();
-                if (GRAD) {
+                if (G) {
 #pragma unroll
                     for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
                         const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
@@ -703,14 +708,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     gh[v][0] = gh[v][1] = gh[v][2] = 0.f;
                 }
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<GRAD, NH>(h, hr, P.obb[b], lam_cf, gh, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH>(h, hr, P.obb[b], lam_cf, gh, smooth);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    jcf += pairs_vs_instance<GRAD, NH>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh,
-                        [&](Wrench& pw) { flush_partner_b<GRAD, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); },
+                    jcf += pairs_vs_instance<G, NH>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh,
+                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); },
                         smooth);
                 }
-                if (GRAD) {   // held-object wrench acts on the tool link (last lane of the segment)
+                if (G) {   // held-object wrench acts on the tool link (last lane of the segment)
                     Wrench hw;
                     hw.zero();
 #pragma unroll
@@ -723,7 +728,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
             }
             if (K.term_cf >= 0)
-                finish_term<MODE>(P, A, sinkB, K.term_cf, term_sum<MODE, LPF>(jcf), ll, active, p, s_counts, real);
+                finish_term<M>(P, A, sinkB, K.term_cf, term_sum<M, LPF>(jcf), ll, active, p, s_counts, real);
 
             // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the segment
             if (K.term_kp >= 0 || K.term_kr >= 0) {
@@ -745,9 +750,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 const float wn2 = fmaf(wx, wx, fmaf(wy, wy, wz * wz));
                 const float wn = sqrtf(wn2);
                 const float erot = fatan2_pos(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
-                if (K.term_kp >= 0) finish_term<MODE>(P, A, sinkB, K.term_kp, epos, ll, active, p, s_counts, real);
-                if (K.term_kr >= 0) finish_term<MODE>(P, A, sinkB, K.term_kr, erot, ll, active, p, s_counts, real);
-                if (GRAD) {
+                if (K.term_kp >= 0) finish_term<M>(P, A, sinkB, K.term_kp, epos, ll, active, p, s_counts, real);
+                if (K.term_kr >= 0) finish_term<M>(P, A, sinkB, K.term_kr, erot, ll, active, p, s_counts, real);
+                if (G) {
                     Wrench tw;   // on the target placement instance
                     tw.zero();
                     if (K.term_kp >= 0 && epos > 0.f) {
@@ -787,9 +792,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
                 // inside the limits (always after the projection, L11) every part is 0: skip the shuffle chain
                 jl = __any_sync(FULL, e2 > 0.f) ? sqrtf(gsum<LPF>(e2)) : 0.f;
-                finish_term<MODE>(P, A, sinkB, K.term_jl, jl, ll, active, p, s_counts, real);
+                finish_term<M>(P, A, sinkB, K.term_jl, jl, ll, active, p, s_counts, real);
             }
-            if (GRAD) {
+            if (G) {
                 // suffix sums of link wrenches over the links after each joint: dJ/dq_j = z_j . (M - o_j x F)
                 Wrench sfx;                               // sum over my links and all later lanes' links
 #pragma unroll
@@ -869,8 +874,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             // pressing object's bottom at the button-face height (R8)
             {
                 const float e = fabsf(pz - Sf.frame[2]);
-                finish_term<MODE>(P, A, sink, Q.term_ss, e, gl, active, p, s_counts);
-                if (GRAD && gl == 0 && e > 0.f) {
+                finish_term<M>(P, A, sink, Q.term_ss, e, gl, active, p, s_counts);
+                if (G && gl == 0 && e > 0.f) {
                     const float g = P.term_lam[Q.term_ss] * (pz > Sf.frame[2] ? 1.f : -1.f);
                     own.add_point(xs[I.xoff], xs[I.xoff + 1], pz, 0.f, 0.f, g);
                 }
@@ -901,7 +906,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     const float ey = fmaxf(fmaxf(loy - ly, ly - hiy), 0.f);
                     const float eu = sqrtf(fmaf(ex, ex, ey * ey));
                     e += eu;
-                    if (GRAD && eu > 0.f) {
+                    if (G && eu > 0.f) {
                         const float k = P.term_lam[Q.term_sc] / eu;
                         const float glx = (lx > hix ? ex : (lx < lox ? -ex : 0.f)) * k;
                         const float gly = (ly > hiy ? ey : (ly < loy ? -ey : 0.f)) * k;
@@ -909,7 +914,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                         gq[u][1] += fmaf(sy, glx, cy * gly);
                     }
                 }
-                finish_term<MODE>(P, A, sink, Q.term_sc, term_sum<MODE, GS>(e), gl, active, p, s_counts);
+                finish_term<M>(P, A, sink, Q.term_sc, term_sum<M, GS>(e), gl, active, p, s_counts);
             }
             // press contact (ValidPress / ValidStickPress, R8): min over the object's spheres of
             // dist_from_bounds(xy in the face frame, lo, hi); the subgradient goes to the arg-min sphere
@@ -939,8 +944,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     const int k2 = __shfl_xor_sync(FULL, kmin, o, GS);
                     if (e2 < emin || (e2 == emin && k2 < kmin)) { emin = e2; kmin = k2; }
                 }
-                finish_term<MODE>(P, A, sink, Q.term_pc, emin, gl, active, p, s_counts);
-                if (GRAD && emin > 0.f) {
+                finish_term<M>(P, A, sink, Q.term_pc, emin, gl, active, p, s_counts);
+                if (G && emin > 0.f) {
                     const float lam = P.term_lam[Q.term_pc];
 #pragma unroll
                     for (int u = 0; u < NSO; ++u)
@@ -958,16 +963,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 for (int u = 0; u < NSO; ++u) rqe[u] = rq[u] + P.eta;
                 float jcp = 0.f;
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<GRAD, NSO>(wq, rqe, P.obb[b], lam_cp, gq, smooth);
+                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO>(wq, rqe, P.obb[b], lam_cp, gq, smooth);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
-                    jcp += pairs_vs_instance<GRAD, NSO>(wq, rqe, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq,
-                        [&](Wrench& pw) { flush_partner<GRAD, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl); },
+                    jcp += pairs_vs_instance<G, NSO>(wq, rqe, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq,
+                        [&](Wrench& pw) { flush_partner<G, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl); },
                         smooth);
                 }
-                finish_term<MODE>(P, A, sink, Q.term_cp, term_sum<MODE, GS>(jcp), gl, active, p, s_counts);
+                finish_term<M>(P, A, sink, Q.term_cp, term_sum<M, GS>(jcp), gl, active, p, s_counts);
             }
-            if (GRAD) {
+            if (G) {
 #pragma unroll
                 for (int u = 0; u < NSO; ++u)
                     if (gl + GS * u < no) own.add_point(wq[u][0], wq[u][1], wq[u][2], gq[u][0], gq[u][1], gq[u][2]);
@@ -985,7 +990,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     const float dx = pa[3] - pb[3], dy = pa[7] - pb[7], dz = pa[11] - pb[11];
                     const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                     soft = fmaf(P.lam_goal, d, soft);
-                    if (GRAD && gl == 0 && d > 0.f) {
+                    if (G && gl == 0 && d > 0.f) {
                         const float k = P.lam_goal / d;
                         const int ia = P.goal_inst[a], ib = P.goal_inst[b];
                         if (P.inst[ia].xoff >= 0) {
@@ -1030,7 +1035,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
                 const float len = sqrtf(gsum<GS>(s2));
                 soft = fmaf(P.lam_traj, len, soft);
-                if (GRAD && len > 0.f) {
+                if (G && len > 0.f) {
                     const int o1 = xoff_of(j + 1), o0 = xoff_of(j);
 #pragma unroll
                     for (int u = 0; u < NJL; ++u) {
@@ -1046,7 +1051,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         const float Jtot = sink.J + soft;
 
         // ---- phase E: instance wrenches -> placement gradients ----
-        if (GRAD) {
+        if (G) {
             __syncwarp();
             for (int i = 0; i < P.n_inst; ++i) {
                 const KInst& I = P.inst[i];
@@ -1062,13 +1067,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             __syncwarp();
         }
 
-        if (MODE == MODE_EVAL) {
+        if (M == MODE_EVAL) {
             if (active) {
                 if (gl == 0 && A.out_J) A.out_J[p] = Jtot;
                 if (gl == 0 && A.out_soft) A.out_soft[p] = soft;
                 if (A.out_grad) for (int d = gl; d < D; d += GS) A.out_grad[p * D + d] = gs[d];
             }
-        } else if (MODE == MODE_CHECK) {
+        } else if (M == MODE_CHECK) {
             const bool inv = invalid || !isfinite(Jtot);
             const int cls = inv ? 2 : (sink.sat ? 0 : 1);
             if (gl == 0 && active) {
@@ -1099,13 +1104,22 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             }
             __syncwarp();
         }
+    };
+    for (int it = 0; it < n_iter; ++it) iteration(std::integral_constant<int, MODE>{}, it);
+    if constexpr (MODE == MODE_OPT) {
+        // Eq. 3 check of the state after the last step, in the same launch (tamp_optimize_and_check): no second
+        // launch re-loading the state and re-building the instances
+        if (A.check_after) {
+            if (BSYNC > 0) __syncthreads();
+            iteration(std::integral_constant<int, MODE_CHECK>{}, n_iter);
+        }
     }
 
     if (MODE == MODE_OPT && active) {
         for (int d = gl; d < D; d += GS) A.x[p * D + d] = xs[d];
         if (gl == 0) A.invalid[p] = invalid ? 1 : 0;
     }
-    if (MODE == MODE_CHECK) {
+    if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after)) {
         __syncthreads();
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x)
             if (s_counts[i]) atomicAdd(&A.out_counts[i], s_counts[i]);

@@ -1080,29 +1080,41 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     return TAMP_OK;
 }
 
+// n_steps fused Adam steps in launches of <= kMaxStepsPerLaunch; with check_last, the last launch also runs the
+// Eq. 3 check of the final state (lane mappings) into the context's class / cost / counts buffers
+static tamp_status run_optimize(tamp_ctx* c, int32_t n_steps, cudaStream_t st, bool check_last) {
+    KArgs A = base_args(c);
+    if (check_last) {
+        A.out_cls = c->at<uint8_t>(c->o_cls);
+        A.out_cost = c->at<float>(c->o_cost);
+        A.out_counts = c->at<int32_t>(c->o_counts);
+        CUDA_TRY(cudaMemsetAsync(A.out_counts, 0, (TAMP_MAX_TERMS + 2) * 4, st), "optimize+check: zero counts");
+    }
+    for (int32_t done = 0; done < n_steps;) {
+        const int32_t k = std::min<int32_t>(n_steps - done, kMaxStepsPerLaunch);
+        A.n_steps = k;
+        A.t0 = c->t;
+        A.check_after = check_last && done + k == n_steps ? 1 : 0;
+        for (int i = 0; i < k; ++i) {   // Adam bias corrections (Kingma & Ba): 1 / (1 - beta^t), t = t0 + i + 1
+            const double t = (double)(c->t + i + 1);
+            A.rbc1[i] = (float)(1.0 / (1.0 - std::pow((double)c->P.beta1, t)));
+            A.rbc2[i] = (float)(1.0 / (1.0 - std::pow((double)c->P.beta2, t)));
+        }
+        CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->bsync, c->threads, c->P, A, c->smem, st), "optimize");
+        c->t += k;
+        c->checked = A.check_after != 0;
+        done += k;
+    }
+    return TAMP_OK;
+}
+
 tamp_status tamp_optimize_step(tamp_ctx* c, int32_t n_steps, void* stream) {
     if (!c) return fail(TAMP_E_INVALID, "null context");
     if (!c->ready) return fail(TAMP_E_STATE, "optimize before sample/set_state");
     if (n_steps < 0) return fail(TAMP_E_INVALID, "n_steps must be >= 0");
     if (n_steps == 0) return TAMP_OK;
     DeviceGuard g(c->device);
-    KArgs A = base_args(c);
-    for (int32_t done = 0; done < n_steps;) {
-        const int32_t k = std::min<int32_t>(n_steps - done, kMaxStepsPerLaunch);
-        A.n_steps = k;
-        A.t0 = c->t;
-        for (int i = 0; i < k; ++i) {   // Adam bias corrections (Kingma & Ba): 1 - beta^t, t = t0 + i + 1
-            const double t = (double)(c->t + i + 1);
-            A.rbc1[i] = (float)(1.0 / (1.0 - std::pow((double)c->P.beta1, t)));
-            A.rbc2[i] = (float)(1.0 / (1.0 - std::pow((double)c->P.beta2, t)));
-        }
-        CUDA_TRY(launch_particle(MODE_OPT, c->gs, c->bsync, c->threads, c->P, A, c->smem,
-                                 static_cast<cudaStream_t>(stream)), "optimize");
-        c->t += k;
-        c->checked = false;
-        done += k;
-    }
-    return TAMP_OK;
+    return run_optimize(c, n_steps, static_cast<cudaStream_t>(stream), false);
 }
 
 static tamp_status run_check(tamp_ctx* c, cudaStream_t st) {
@@ -1124,6 +1136,29 @@ tamp_status tamp_check_satisfied(tamp_ctx* c, uint8_t* cls, int32_t* counts, voi
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     tamp_status s = run_check(c, st);
     if (s != TAMP_OK) return s;
+    const size_t nb = (size_t)(c->P.n_terms + 2) * 4;
+    CUDA_TRY(cudaMemcpyAsync(counts, c->at<int32_t>(c->o_counts), nb, cudaMemcpyDefault, st), "check: counts copy");
+    if (cls) CUDA_TRY(cudaMemcpyAsync(cls, c->at<uint8_t>(c->o_cls), (size_t)c->n, cudaMemcpyDefault, st), "check: cls copy");
+    if (is_host_ptr(counts) || is_host_ptr(cls)) CUDA_TRY(cudaStreamSynchronize(st), "check: sync");
+    return TAMP_OK;
+}
+
+tamp_status tamp_optimize_and_check(tamp_ctx* c, int32_t n_steps, uint8_t* cls, int32_t* counts, void* stream) {
+    if (!c) return fail(TAMP_E_INVALID, "null context");
+    if (!c->ready) return fail(TAMP_E_STATE, "optimize before sample/set_state");
+    if (n_steps < 1) return fail(TAMP_E_INVALID, "n_steps must be >= 1");
+    if (!counts) return fail(TAMP_E_INVALID, "counts must not be NULL");
+    DeviceGuard g(c->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (c->gs == 1) {            // serial mapping: optimisation and check stay separate launches
+        tamp_status s = run_optimize(c, n_steps, st, false);
+        if (s != TAMP_OK) return s;
+        s = run_check(c, st);
+        if (s != TAMP_OK) return s;
+    } else {
+        tamp_status s = run_optimize(c, n_steps, st, true);
+        if (s != TAMP_OK) return s;
+    }
     const size_t nb = (size_t)(c->P.n_terms + 2) * 4;
     CUDA_TRY(cudaMemcpyAsync(counts, c->at<int32_t>(c->o_counts), nb, cudaMemcpyDefault, st), "check: counts copy");
     if (cls) CUDA_TRY(cudaMemcpyAsync(cls, c->at<uint8_t>(c->o_cls), (size_t)c->n, cudaMemcpyDefault, st), "check: cls copy");

@@ -95,7 +95,7 @@ class Info(ctypes.Structure):
 
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
            "tamp_init_problem", "tamp_get_info", "tamp_sample_particles", "tamp_optimize_step",
-           "tamp_check_satisfied", "tamp_best_k", "tamp_merge_best_k", "tamp_eval", "tamp_get_state",
+           "tamp_check_satisfied", "tamp_optimize_and_check", "tamp_best_k", "tamp_merge_best_k", "tamp_eval", "tamp_get_state",
            "tamp_set_state", "tamp_destroy", "tamp_kernel_launches", "tamp_plan_heuristic"]
 
 _lib = None
@@ -122,6 +122,7 @@ def load(path: str = None):
     lib.tamp_sample_particles.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tamp_optimize_step.argtypes = [vp, I32, vp]
     lib.tamp_check_satisfied.argtypes = [vp, vp, vp, vp]
+    lib.tamp_optimize_and_check.argtypes = [vp, I32, vp, vp, vp]
     lib.tamp_best_k.argtypes = [vp, I32, vp, vp]
     lib.tamp_merge_best_k.argtypes = [vp, vp, I32, I32, vp, vp]
     lib.tamp_eval.argtypes = [vp, vp, vp, vp, vp, vp]
@@ -312,6 +313,14 @@ class TampContext:
         """Returns the counts tensor (device unless a host tensor is passed) and cls if given."""
         counts = self.counts_buf if counts is None else counts
         _check(self.lib.tamp_check_satisfied(self.h, _ptr(cls), _ptr(counts), _stream(self.device, stream)))
+        return counts, cls
+
+    def optimize_check(self, n_steps: int, cls: Optional[torch.Tensor] = None, counts: Optional[torch.Tensor] = None,
+                       stream=None):
+        """optimize(n_steps) then check(), one C-ABI call (the check rides on the last optimisation launch)."""
+        counts = self.counts_buf if counts is None else counts
+        _check(self.lib.tamp_optimize_and_check(self.h, int(n_steps), _ptr(cls), _ptr(counts),
+                                                _stream(self.device, stream)))
         return counts, cls
 
     def best_k(self, k: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

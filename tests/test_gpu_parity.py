@@ -184,6 +184,35 @@ def test_best_k_sizes_exact(n, k):
     np.testing.assert_array_equal(gidx, order + 123)
 
 
+@pytest.mark.parametrize("cfg,n,lanes", [(2, 1000, 8), (3, 700, 8), (4, 300, 16), (2, 500, 4), (1, 2000, 1)])
+def test_optimize_and_check_equals_separate_calls(cfg, n, lanes):
+    """tamp_optimize_and_check (the check fused into the last optimisation launch for the link mappings) gives
+    bit-identical particles, counts, classes and best-k records to tamp_optimize_step + tamp_check_satisfied,
+    over several intervals, including a split launch (n_steps > 64)."""
+    spec = make_config(cfg, n=n)
+    spec.ik_iters, spec.ik_seeds = 10, 4
+    a = TampContext(spec, n, lanes_per_particle=lanes)
+    b = TampContext(spec, n, lanes_per_particle=lanes)
+    a.sample(seed=31)
+    b.sample(seed=31)
+    for k in (7, 1, 70, 10):
+        a.optimize(k)
+        cla = torch.empty(n, dtype=torch.uint8, device="cuda")
+        ca, _ = a.check(cls=cla)
+        ca = ca.clone()
+        clb = torch.empty(n, dtype=torch.uint8, device="cuda")
+        cb, _ = b.optimize_check(k, cls=clb)
+        assert torch.equal(ca, cb) and torch.equal(cla, clb)
+        assert torch.equal(a.get_state()["x"], b.get_state()["x"])
+    assert a.t == b.t == 88
+    assert torch.equal(a.best_k(8), b.best_k(8))
+    hc = torch.zeros(a.n_hard + 2, dtype=torch.int32).pin_memory()
+    a.optimize(3)
+    ca, _ = a.check()
+    b.optimize_check(3, counts=hc)                        # host buffer through the C ABI
+    assert np.array_equal(ca.cpu().numpy(), hc.numpy())
+
+
 def test_merge_best_k_equals_global_best_k():
     """all-gather emulation: per-rank best-k records merged == best-k over the union."""
     cfg, n, k = 1, 256, 8
