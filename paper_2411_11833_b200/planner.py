@@ -180,10 +180,13 @@ def cutamp(skeletons, n_particles: int, seed: int = 0, steps_per_pop: int = 200,
         for _ in range(steps_per_pop // check_every):
             if method == "sampling":                 # re-draw instead of optimising
                 ctx.sample(fresh_seed(i))
+                counts, _ = ctx.check()              # IsGoalSatisfied (Eq. 3)
+            elif hasattr(ctx, "optimize_check"):     # OptimizeParticles + IsGoalSatisfied in one launch
+                counts, _ = ctx.optimize_check(check_every)
             else:
-                ctx.optimize(check_every)            # OptimizeParticles
+                ctx.optimize(check_every)
+                counts, _ = ctx.check()
             spent[i] += check_every
-            counts, _ = ctx.check()                  # IsGoalSatisfied (Eq. 3)
             if int(counts[-2].item()) > 0:           # GetSatisfyingParticles (best first)
                 return PlanResult(i, ctx.best_k(k), spent[i], pops, h0, pruned=list(pruned))
         h = plan_heuristic(counts.cpu(), ctx.n_hard, penalty)
