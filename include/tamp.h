@@ -251,8 +251,8 @@ tamp_status tamp_optimize_step(tamp_ctx* ctx, int32_t n_steps, void* stream);
 tamp_status tamp_check_satisfied(tamp_ctx* ctx, uint8_t* cls, int32_t* counts, void* stream);
 
 /* tamp_optimize_step(n_steps) followed by tamp_check_satisfied, as one call (Alg. 1's optimise-then-check
-   interval): identical results; with the link mappings the check of the final state runs inside
-   the last optimisation launch (no second launch re-loading the state).  n_steps >= 1; cls may be NULL;
+   interval): identical results; the check of the final state runs inside the last optimisation
+   launch (no second launch re-loading the state).  n_steps >= 1; cls may be NULL;
    buffers as for tamp_check_satisfied. */
 tamp_status tamp_optimize_and_check(tamp_ctx* ctx, int32_t n_steps, uint8_t* cls, int32_t* counts, void* stream);
 

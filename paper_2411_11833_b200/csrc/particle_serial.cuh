@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         const int l = i / TAMP_MAX_SPHERES_PER_LINK, k = i % TAMP_MAX_SPHERES_PER_LINK;
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3] + P.eta);
     }
-    if (MODE == MODE_CHECK)
+    if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = tid; i < P.n_terms + 2; i += NT) s_counts[i] = 0;
     load_rows(A.x, D, L.x);
     if (MODE == MODE_OPT) {
@@ -181,8 +181,11 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     };
 
     const int n_iter = (MODE == MODE_OPT) ? A.n_steps : 1;
-    for (int it = 0; it < n_iter; ++it) {
-        TermSink<MODE> sink;
+    // one optimisation / check / eval iteration; M = MODE, or MODE_CHECK for the check fused after the last step
+    auto iteration = [&](auto mtag, const int it) {
+        constexpr int M = decltype(mtag)::value;
+        constexpr bool G = M != MODE_CHECK;
+        TermSink<M> sink;
         float soft = 0.f;
 
         // ---- instances: pose, world bounding-sphere centre; zero accumulators ----
@@ -200,10 +203,10 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 ip(i, 6) = fmaf(sy, ob[0], fmaf(cy, ob[1], py));
                 ip(i, 7) = pz + ob[2];
             }
-            if (GRAD)
+            if (G)
                 for (int k = 0; k < 6; ++k) iw(i, k) = 0.f;
         }
-        if (GRAD)
+        if (G)
             for (int d = 0; d < D; ++d) gs(d) = 0.f;
 
         // ---- robot configurations ----
@@ -260,9 +263,9 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 const float wx = Mm[7] - Mm[5], wy = Mm[2] - Mm[6], wz = Mm[3] - Mm[1];
                 const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
                 const float erot = fatan2_pos(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
-                if (K.term_kp >= 0) serial_term<MODE>(P, A, sink, K.term_kp, epos, active, p, s_counts);
-                if (K.term_kr >= 0) serial_term<MODE>(P, A, sink, K.term_kr, erot, active, p, s_counts);
-                if (GRAD) {
+                if (K.term_kp >= 0) serial_term<M>(P, A, sink, K.term_kp, epos, active, p, s_counts);
+                if (K.term_kr >= 0) serial_term<M>(P, A, sink, K.term_kr, erot, active, p, s_counts);
+                if (G) {
                     Wrench tw;
                     tw.zero();
                     if (K.term_kp >= 0 && epos > 0.f) {
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     e2 = fmaf(e, e, e2);
                 }
                 jl = sqrtf(e2);
-                serial_term<MODE>(P, A, sink, K.term_jl, jl, active, p, s_counts);
+                serial_term<M>(P, A, sink, K.term_jl, jl, active, p, s_counts);
             }
             (void)sq; (void)cq;
             // backward sweep over the links 8 -> 1: spheres of link l in T_l, suffix wrench, dJ/dq_l
@@ -345,8 +348,8 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
                         if (!hit[k]) continue;
                         float g[3] = {0.f, 0.f, 0.f};
-                        jcf += sphere_obb<GRAD>(wq[k][0], wq[k][1], wq[k][2], rq[k], B0, lam_cf, g[0], g[1], g[2], smooth);
-                        if (GRAD) sfx.add_point(wq[k][0], wq[k][1], wq[k][2], g[0], g[1], g[2]);
+                        jcf += sphere_obb<G>(wq[k][0], wq[k][1], wq[k][2], rq[k], B0, lam_cf, g[0], g[1], g[2], smooth);
+                        if (G) sfx.add_point(wq[k][0], wq[k][1], wq[k][2], g[0], g[1], g[2]);
                     }
                 } else if (near) {
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                                 const float R = rr + B0.rad;
                                 near = fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f;
                             }
-                            if (near) jcf += sphere_obb<GRAD>(wx, wy, wz, rr, B0, lam_cf, g[0], g[1], g[2], smooth);
+                            if (near) jcf += sphere_obb<G>(wx, wy, wz, rr, B0, lam_cf, g[0], g[1], g[2], smooth);
                         } else {
                             jcf += sphere_vs_obbs(wx, wy, wz, rr, K.obb_mask, lam_cf, g);
                         }
@@ -371,13 +374,13 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                             Wrench pw;
                             pw.zero();
                             jcf += sphere_vs_inst(wx, wy, wz, rr, ii, lam_cf, g, pw);
-                            if (GRAD && P.inst[ii].xoff >= 0 && pw.nonzero()) add_iw(ii, pw);
+                            if (G && P.inst[ii].xoff >= 0 && pw.nonzero()) add_iw(ii, pw);
                         }
-                        if (GRAD) sfx.add_point(wx, wy, wz, g[0], g[1], g[2]);
+                        if (G) sfx.add_point(wx, wy, wz, g[0], g[1], g[2]);
                     }
                 }
                 if (l < TAMP_NJ) {     // joint l+1 rotates frame l+1 (= T here) about its z axis
-                    if (GRAD) {
+                    if (G) {
                         const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
                         const float ox = T.t[0], oy = T.t[1], oz = T.t[2];
                         const float mx = sfx.m[0] - (oy * sfx.f[2] - oz * sfx.f[1]);
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     T = compose(T, Fi);
                 }
             }
-            if (K.term_cf >= 0) serial_term<MODE>(P, A, sink, K.term_cf, jcf, active, p, s_counts);
+            if (K.term_cf >= 0) serial_term<M>(P, A, sink, K.term_cf, jcf, active, p, s_counts);
             // block-synchronous configurations: every warp of the block executes the same (large) code region at
             // a time and the instruction cache is shared (the kernel body is ~100 KB of SASS)
             if (A.bsync) __syncthreads();
@@ -427,8 +430,8 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             {   // support |z_bottom - z_top|
                 const float pz = ip(ii, 4);
                 const float e = fabsf(pz - Sf.frame[2]);
-                serial_term<MODE>(P, A, sink, Q.term_ss, e, active, p, s_counts);
-                if (GRAD && e > 0.f) own.add_point(ip(ii, 2), ip(ii, 3), pz, 0.f, 0.f, P.term_lam[Q.term_ss] * (pz > Sf.frame[2] ? 1.f : -1.f));
+                serial_term<M>(P, A, sink, Q.term_ss, e, active, p, s_counts);
+                if (G && e > 0.f) own.add_point(ip(ii, 2), ip(ii, 3), pz, 0.f, 0.f, P.term_lam[Q.term_ss] * (pz > Sf.frame[2] ? 1.f : -1.f));
             }
             const float sy = Sf.sy, cy = Sf.cy;
             if (Q.term_sc >= 0) {   // containment: sum over spheres of dist_from_bounds(xy, lo + r, hi - r)
@@ -443,14 +446,14 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     const float ey = fmaxf(fmaxf(loy - ly, ly - hiy), 0.f);
                     const float eu = sqrtf(fmaf(ex, ex, ey * ey));
                     e += eu;
-                    if (GRAD && eu > 0.f) {
+                    if (G && eu > 0.f) {
                         const float kk = P.term_lam[Q.term_sc] / eu;
                         const float glx = (lx > hix ? ex : (lx < lox ? -ex : 0.f)) * kk;
                         const float gly = (ly > hiy ? ey : (ly < loy ? -ey : 0.f)) * kk;
                         own.add_point(c.x, c.y, c.z, fmaf(cy, glx, -sy * gly), fmaf(sy, glx, cy * gly), 0.f);
                     }
                 }
-                serial_term<MODE>(P, A, sink, Q.term_sc, e, active, p, s_counts);
+                serial_term<M>(P, A, sink, Q.term_sc, e, active, p, s_counts);
             }
             if (Q.term_pc >= 0) {   // press contact: min over spheres of dist_from_bounds(xy, lo, hi)
                 float emin = kFar, gx = 0.f, gy = 0.f, cx = 0.f, cyy = 0.f, cz = 0.f;
@@ -468,8 +471,8 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         cx = c.x; cyy = c.y; cz = c.z;
                     }
                 }
-                serial_term<MODE>(P, A, sink, Q.term_pc, emin, active, p, s_counts);
-                if (GRAD && emin > 0.f) {
+                serial_term<M>(P, A, sink, Q.term_pc, emin, active, p, s_counts);
+                if (G && emin > 0.f) {
                     const float lam = P.term_lam[Q.term_pc];
                     own.add_point(cx, cyy, cz, lam * fmaf(cy, gx, -sy * gy), lam * fmaf(sy, gx, cy * gy), 0.f);
                 }
@@ -487,13 +490,13 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         Wrench pw;
                         pw.zero();
                         jcp += sphere_vs_inst(c.x, c.y, c.z, rr, jj, lam_cp, g, pw);
-                        if (GRAD && P.inst[jj].xoff >= 0 && pw.nonzero()) add_iw(jj, pw);
+                        if (G && P.inst[jj].xoff >= 0 && pw.nonzero()) add_iw(jj, pw);
                     }
-                    if (GRAD) own.add_point(c.x, c.y, c.z, g[0], g[1], g[2]);
+                    if (G) own.add_point(c.x, c.y, c.z, g[0], g[1], g[2]);
                 }
-                serial_term<MODE>(P, A, sink, Q.term_cp, jcp, active, p, s_counts);
+                serial_term<M>(P, A, sink, Q.term_cp, jcp, active, p, s_counts);
             }
-            if (GRAD) add_iw(ii, own);
+            if (G) add_iw(ii, own);
             if (A.bsync) __syncthreads();
         }
 
@@ -507,7 +510,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     const float dx = ax - bx, dy = ay - by, dz = az - bz;
                     const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                     soft = fmaf(P.lam_goal, d, soft);
-                    if (GRAD && d > 0.f) {
+                    if (G && d > 0.f) {
                         const float k = P.lam_goal / d;
                         Wrench w;
                         if (P.inst[ia].xoff >= 0) { w.zero(); w.add_point(ax, ay, az, dx * k, dy * k, dz * k); add_iw(ia, w); }
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 }
                 const float len = sqrtf(s2);
                 soft = fmaf(P.lam_traj, len, soft);
-                if (GRAD && len > 0.f) {
+                if (G && len > 0.f) {
                     const int o1 = xoff_of(j + 1), o0 = xoff_of(j);
 #pragma unroll
                     for (int jt = 0; jt < TAMP_NJ; ++jt) {
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         const float Jtot = sink.J + soft;
 
         // ---- instance wrenches -> placement gradients: dJ/dt = F, dJ/dyaw = z . (M - t x F) ----
-        if (GRAD)
+        if (G)
             for (int i = 0; i < P.n_inst; ++i) {
                 const KInst& I = P.inst[i];
                 if (I.xoff < 0) continue;
@@ -561,13 +564,13 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 gs(I.xoff + 3) += iw(i, 5) - (xs(I.xoff) * iw(i, 1) - xs(I.xoff + 1) * iw(i, 0));
             }
 
-        if (MODE == MODE_EVAL) {
+        if (M == MODE_EVAL) {
             if (active) {
                 if (A.out_J) A.out_J[p] = Jtot;
                 if (A.out_soft) A.out_soft[p] = soft;
                 if (A.out_grad) for (int d = 0; d < D; ++d) A.out_grad[p * D + d] = gs(d);
             }
-        } else if (MODE == MODE_CHECK) {
+        } else if (M == MODE_CHECK) {
             const bool inv = invalid || !isfinite(Jtot);
             const int cls = inv ? 2 : (sink.sat ? 0 : 1);
             if (active) {
@@ -600,6 +603,13 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 }
             }
         }
+    };
+    for (int it = 0; it < n_iter; ++it) iteration(std::integral_constant<int, MODE>{}, it);
+    if constexpr (MODE == MODE_OPT) {
+        if (A.check_after) {            // Eq. 3 check of the final state in the same launch
+            __syncthreads();
+            iteration(std::integral_constant<int, MODE_CHECK>{}, n_iter);
+        }
     }
 
     if (MODE == MODE_OPT) {
@@ -609,7 +619,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         store_rows(A.m, D, L.m);
         store_rows(A.v, D, L.v);
     }
-    if (MODE == MODE_CHECK) {
+    if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after)) {
         __syncthreads();
         for (int i = tid; i < P.n_terms + 2; i += NT)
             if (s_counts[i]) atomicAdd(&A.out_counts[i], s_counts[i]);

@@ -1150,12 +1150,7 @@ tamp_status tamp_optimize_and_check(tamp_ctx* c, int32_t n_steps, uint8_t* cls, 
     if (!counts) return fail(TAMP_E_INVALID, "counts must not be NULL");
     DeviceGuard g(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (c->gs == 1) {            // serial mapping: optimisation and check stay separate launches
-        tamp_status s = run_optimize(c, n_steps, st, false);
-        if (s != TAMP_OK) return s;
-        s = run_check(c, st);
-        if (s != TAMP_OK) return s;
-    } else {
+    {
         tamp_status s = run_optimize(c, n_steps, st, true);
         if (s != TAMP_OK) return s;
     }
