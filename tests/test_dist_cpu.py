@@ -38,6 +38,10 @@ class OracleCtx:
         _, c, *_ = O.check(self.spec, self.csp, self.st)
         return torch.tensor(c, dtype=torch.int32), cls
 
+    def optimize_check(self, k, cls=None, counts=None):      # tamp_optimize_and_check: optimize, then check
+        self.optimize(k)
+        return self.check(cls, counts)
+
     def best_k(self, k, out=None):
         cls, _, J, soft, _ = O.check(self.spec, self.csp, self.st)
         sel, kc, kcost = O.best_k(cls, J, soft, np.arange(self.gofs, self.gofs + self.n), k)
