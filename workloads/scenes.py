@@ -124,7 +124,7 @@ class ProblemSpec:
     lam: dict
     eps: dict
     lam_goal: float = 0.25      # L7
-    lam_traj: float = 1.0       # L8
+    lam_traj: float = 0.01      # L8, revised: 1.0 let the plan cost overpower the Kin constraints
     eta: float = 0.0            # collision activation distance (L1)
     # Adam (L9)
     beta1: float = 0.9
