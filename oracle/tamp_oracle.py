@@ -495,7 +495,7 @@ def initialize_particles(spec: ProblemSpec, csp: CSP, seed: int, gidx: np.ndarra
             pval = np.broadcast_to(np.asarray(pv.value, float), (N, 4)) if pv.const else \
                 x[:, csp.offsets[a.placement]:csp.offsets[a.placement] + 4]
             Tg = np.concatenate([grasps[:, gslot[a.grasp]], bottom], 1)
-            Tt = (pose_xyzyaw(torch.as_tensor(pval)) @ torch.as_tensor(Tg)).numpy()
+            Tt = (pose_xyzyaw(torch.as_tensor(np.array(pval))) @ torch.as_tensor(Tg)).numpy()
             off = csp.offsets[a.q1]
             x[:, off:off + 7] = ik_restarts(spec, x[:, off:off + 7], Tt, seed, gidx, _stream(V, a.q1))
     for a in spec.actions:
