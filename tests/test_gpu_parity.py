@@ -351,7 +351,7 @@ def test_full_size_sampled_against_oracle(cfg, n):
     assert np.all(close | unstable | kinks[:, None])
 
 
-@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (1, 1 << 20)])
+@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20)])
 def test_full_size_mid_optimisation_against_oracle(cfg, n):
     """The bench's own state: IK-initialised particles (ik_iters = 20, as bench.py) after 3 launches of 10 fused
     steps (contact-rich: the IK puts grippers at their targets), in the auto launch configuration.  On 24
