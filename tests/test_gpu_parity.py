@@ -388,6 +388,41 @@ def test_full_size_mid_optimisation_against_oracle(cfg, n):
     assert np.all(close | unstable | kinks[:, None])
 
 
+
+@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384)])
+def test_full_size_fused_check_against_oracle(cfg, n):
+    """The bench's interval at full size: IK-initialised particles, 20 steps, then 10 more with the Eq. 3 check
+    fused into the last launch (tamp_optimize_and_check).  On 24 sampled particles the oracle's check of the
+    final state gives the same class (epsilon-marginal residuals excepted, L21); over all particles the counts
+    are those of Eq. 3 / Eq. 5 applied to the class vector and to the eval() residuals of the same state."""
+    spec = make_config(cfg, n=n)
+    spec.ik_iters = 20
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, n)
+    ctx.sample(seed=4000 + cfg)
+    ctx.optimize(20)
+    cls = torch.empty(n, dtype=torch.uint8, device="cuda")
+    counts, _ = ctx.optimize_check(10, cls=cls)
+    counts = counts.cpu().numpy().astype(np.int64)
+    cls_all = cls.cpu().numpy()
+    st = ctx.get_state()
+    eps = np.array([spec.eps[t.kind] for t in csp.terms])
+    _, _, Jc_all, _ = ctx.eval()
+    Jc_all = Jc_all.cpu().numpy()
+    assert counts.shape == (len(csp.terms) + 2,)
+    np.testing.assert_array_equal(counts[:-2], (Jc_all <= eps[None, :].astype(np.float32)).sum(axis=0))
+    assert counts[-2] == int((cls_all == 0).sum()) and counts[-1] == int((cls_all == 2).sum())
+    assert np.all(counts[:-2] >= counts[-2])
+    idx = np.sort(np.random.default_rng(7).choice(n, 24, replace=False))
+    x32 = st["x"].cpu().numpy()[idx].astype(np.float64)
+    g32 = st["grasp"].cpu().numpy()[idx].reshape(len(idx), -1, 3, 4).astype(np.float64)
+    so = O.new_state(x32, g32)
+    so.invalid = st["invalid"].cpu().numpy()[idx].astype(bool)
+    cls_o, _, _, _, Jc_o = O.check(spec, csp, so)
+    marginal = ((np.abs(Jc_o - eps[None, :]) <= 1e-4 * eps[None, :] + 1e-6) & (Jc_o > 0)).any(axis=1)
+    np.testing.assert_array_equal(cls_all[idx][~marginal], cls_o[~marginal])
+    assert marginal.sum() <= 2
+
 def test_edge_sizes():
     """N = 1 (a lone particle in a 16-particle block) and k = N."""
     spec, csp, x32, g32 = oracle_inputs(1, 1, seed=80)
