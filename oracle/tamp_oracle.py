@@ -12,7 +12,11 @@ Readings where the paper is silent are SURVEY.md §8(c) L1-L25 (listed in DESIGN
 Implementation style: vectorised over particles with plain PyTorch CPU ops in float64, 4x4
 homogeneous transforms ("b *h 4 4", Listing 2), gradients by torch autograd (reverse
 mode AD of the definition -- independent of the CUDA path's hand-derived backward).
-Parity unpinned: nothing (pins in tests/test_oracle_*.py, listed in DESIGN.md).
+Pins: tests/test_oracle_*.py (listed in DESIGN.md §6).  Every part of the term assembly has a closed-form pin;
+tools/oracle_mutants.py applies one-line mutants (SC shrink signs, TrajLength endpoints, lambda_goal, held-object
+attachment, sphere->link index, CP support exclusions) and each one fails a pin.  Parity unpinned: none.
+TEST INFRASTRUCTURE: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this module; the product path (paper_2411_11833_b200/) never does.
 """
 from __future__ import annotations
 
