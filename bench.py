@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--config", type=int, default=3,
+                   help="BASELINE config (default 3: Tetris-4 + goal at 32,768 particles, the largest single-GPU config)")
     p.add_argument("--n", type=int, default=None, help="particles per rank (default: the config's BASELINE size)")
     p.add_argument("--adam-steps", type=int, default=100)
     p.add_argument("--check-every", type=int, default=10)
@@ -63,6 +64,9 @@ def parse():
     p.add_argument("--ik-iters", type=int, default=20,
                    help="conditional IK sampler iterations in InitializeParticles (P:521); 0 = uniform confs")
     p.add_argument("--ik-seeds", type=int, default=8, help="IK restarts per conf (1, 2, 4, 8; DESIGN.md R6)")
+    p.add_argument("--repeats", type=int, default=5, help="timed regions of exactly --steps steps; value = median")
+    p.add_argument("--no-extra", action="store_true", help="skip the extra workloads (config 2, config 1 at 1M, SELF)")
+    p.add_argument("--no-overlap", action="store_true", help="all-reduce of the counts on the launching stream")
     return p.parse_args()
 
 
@@ -199,10 +203,31 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
+def free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def spawn_ranks(n, argv, script=None, env=None):
+    """One process per GPU of this node: re-launch `script` (default: this file) with argv under
+    torch.distributed.run, n ranks, rendezvous on 127.0.0.1.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script or os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd, env=env)
+
+
 def dist_init(args):
+    """RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* from the environment (torchrun, or spawn_ranks).  NCCL over
+    NVLink for the product path, gloo for the (host-only) reference arm."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world} (launch one process per GPU)")
     if world > 1:
         import torch.distributed as dist
         if args.impl == "ours":
@@ -214,26 +239,50 @@ def dist_init(args):
     return 1, 0, 0, None
 
 
-def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_rec=None):
-    """One bench step (see module docstring).  Returns the merged global best-k records."""
+def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_rec=None, side=None):
+    """One bench step (see module docstring).  Returns the merged global best-k records.
+
+    With `side` (a CUDA stream) and NCCL, the SUM all-reduce of each interval's counts (C1) runs on the side
+    stream while the next optimisation launch runs on the launching stream (particles never couple, Eq. 4,
+    P:461-467, so nothing in the next launch waits for the counts); two count buffers alternate, and a buffer
+    is only rewritten after its all-reduce finished.  The counts are the same bytes either way."""
     ctx.sample(seed)
-    for _ in range(args.adam_steps // args.check_every):
+    n_int = args.adam_steps // args.check_every
+    direct = host_counts is not None and world == 1
+    overlap = side is not None and dist is not None and not direct
+    bufs = getattr(ctx, "_bench_counts", None)
+    if overlap and bufs is None:
+        bufs = ctx._bench_counts = [torch.zeros_like(ctx.counts_buf) for _ in range(2)]
+    main_s = torch.cuda.current_stream() if overlap else None
+    for i in range(n_int):
         # check_every fused Adam steps + the Eq. 3 check of the final state: one C-ABI call, one launch for the
         # link mappings (tamp_optimize_and_check; the serial mapping launches the check separately)
-        direct = host_counts is not None and world == 1
         if events is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        counts, _ = ctx.optimize_check(args.check_every, counts=host_counts if direct else None)
+        if overlap:
+            if i >= 2:
+                main_s.wait_stream(side)                  # buffer i % 2 free again (its all-reduce is done)
+            counts, _ = ctx.optimize_check(args.check_every, counts=bufs[i % 2])
+        else:
+            counts, _ = ctx.optimize_check(args.check_every, counts=host_counts if direct else None)
         if events is not None:
             e1.record()
             events.append((e0, e1))
-        if not direct:                                    # (direct: D2H through the C ABI into the host buffer)
+        if overlap:
+            side.wait_stream(main_s)
+            with torch.cuda.stream(side):
+                dist.all_reduce(counts)                   # NCCL SUM of satisfied counts (C1), overlapped
+            if host_counts is not None:
+                host_counts.copy_(counts)
+        elif not direct:                                  # (direct: D2H through the C ABI into the host buffer)
             if dist is not None:
                 dist.all_reduce(counts)                   # NCCL SUM of satisfied counts (C1)
             if host_counts is not None:
                 host_counts.copy_(counts)                 # D2H
+    if overlap:
+        main_s.wait_stream(side)
     if host_rec is not None and world == 1:
         ctx.best_k(args.k, out=host_rec)
         return host_rec
@@ -256,8 +305,10 @@ def max_over_ranks(v, dist):
     return float(t.item())
 
 
-def cpu_baseline(args, spec, budget_s):
-    """The float64 oracle (as it stands) on the host cores: bounded sample of the same workload."""
+def cpu_baseline(args, spec, budget_s, ctx=None):
+    """The float64 oracle (as it stands) on the host cores: bounded sample of the same workload.  The same leg
+    re-verifies parity in this run: the first 256 particles of the bench context's current state
+    (the end of the timed rounds) are re-evaluated by the oracle -- cost, per-term costs, gradient."""
     from oracle import tamp_oracle as O
     cores = os.cpu_count() or 1
     torch.set_num_threads(cores)
@@ -284,11 +335,41 @@ def cpu_baseline(args, spec, budget_s):
         if time.perf_counter() - t1 >= budget_s / 3 and steps1 >= 1:
             break
     dt1 = time.perf_counter() - t1
-    return {"value": n * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "value_1core": n * steps1 / dt1,
-            "sample": f"{n} particles x {steps} Adam steps of {CONFIG_NAMES[args.config]} "
-                      f"(float64 oracle, torch autograd, {cores} threads), {dt:.1f} s; "
-                      f"value_1core: {steps1} steps on 1 thread, {dt1:.1f} s"}
+    out = {"value": n * steps / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "value_1core": n * steps1 / dt1,
+           "sample": f"{n} particles x {steps} Adam steps of {CONFIG_NAMES[args.config]} "
+                     f"(float64 oracle, torch autograd, {cores} threads), {dt:.1f} s; "
+                     f"value_1core: {steps1} steps on 1 thread, {dt1:.1f} s"}
+    if ctx is not None:
+        torch.set_num_threads(cores)
+        out["parity_recheck"] = parity_recheck(O, spec, csp, ctx, min(256, ctx.n))
+    return out
+
+
+def parity_recheck(O, spec, csp, ctx, m):
+    """Oracle vs the GPU on the first m particles of the bench context's state (north_star tolerances: cost and
+    per-term costs rel 1e-4, gradient rel 1e-3).  Particles whose oracle gradient is not smooth within +-1e-5
+    (second-difference kink test) are reported, not failed."""
+    st = ctx.get_state()
+    J, soft, Jc, grad = (t.cpu().numpy()[:m] for t in ctx.eval())
+    x = st["x"].cpu().numpy()[:m].astype(np.float64)
+    g = st["grasp"].cpu().numpy()[:m].reshape(m, -1, 3, 4).astype(np.float64)
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x, g)
+    cost_ok = (np.abs(J - Jo) <= 1e-4 * np.abs(Jo) + 1e-6) & np.all(np.abs(Jc - Jco) <= 1e-4 * np.abs(Jco) + 1e-6, 1)
+    gerr = np.abs(grad - grado).max(axis=1)
+    gscale = np.abs(grado).max(axis=1)
+    grad_ok = gerr <= 1e-3 * gscale + 1e-6
+    kink = np.zeros(m, bool)
+    bad = np.where(~grad_ok)[0]
+    if len(bad):
+        r = np.random.default_rng(0).normal(size=(len(bad), x.shape[1]))
+        r /= np.linalg.norm(r, axis=1, keepdims=True)
+        _, _, _, gp = O.cost_and_grad(spec, csp, x[bad] + 1e-5 * r, g[bad])
+        _, _, _, gm = O.cost_and_grad(spec, csp, x[bad] - 1e-5 * r, g[bad])
+        kink[bad] = np.abs(gp - 2 * grado[bad] + gm).max(axis=1) > 1e-4 * gscale[bad]
+    return {"particles": m, "cost_match": int(cost_ok.sum()), "grad_match": int(grad_ok.sum()),
+            "grad_kinks_excluded": int((~grad_ok & kink).sum()), "grad_mismatch_smooth": int((~grad_ok & ~kink).sum()),
+            "state": f"bench context after the timed rounds (t = {st['t']})"}
 
 
 def bench_reference(args, world, rank, dist):
@@ -301,7 +382,6 @@ def bench_reference(args, world, rank, dist):
     spec = make_config(args.config)
     csp = O.build_csp(spec)
     n, adam = 128, 4
-    x, g = O.initialize_particles(spec, csp, 7, np.arange(n))
 
     def step(seed):
         xs, gs = O.initialize_particles(spec, csp, seed, np.arange(n))
@@ -318,11 +398,11 @@ def bench_reference(args, world, rank, dist):
     dt = time.perf_counter() - t0
     value = n * adam * args.steps / dt
     sample = f"{n} particles x {adam} Adam steps (+ sample, check, best-k) per step, float64 oracle, {cores} threads"
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config{args.config}:{CONFIG_NAMES[args.config]}", "particles_per_step": n,
-                       "adam_steps_per_step": adam},
+                       "adam_steps_per_step": adam, "parallelism": f"dp{world} (rank 0 runs the oracle)"},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -346,73 +426,33 @@ def ttfs(ctx, args, dist, world, seed, budget_steps=1000):
     return {"s": None, "steps": steps, "satisfying": 0, "note": "not reached within budget"}
 
 
-def main():
-    args = parse()
-    world, rank, local, dist = dist_init(args)
-    if args.impl == "reference":
-        bench_reference(args, world, rank, dist)
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-    from paper_2411_11833_b200 import TampContext, kernel_launches
-    import paper_2411_11833_b200.build as bld
-    bld.build()
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    torch.set_num_threads(1)
-    cfg = args.config
-    n = args.n or CONFIG_SIZES[cfg]
-    if cfg == 4 and args.n is None:
-        n = 131072 // 8                              # config 4: 128K particles over 8 GPUs (per-rank share)
+def make_spec(args, cfg, n, self_collision=None):
     spec = make_config(cfg, n=n)
     spec.ik_iters = args.ik_iters
     spec.ik_seeds = args.ik_seeds
-    spec.self_collision = args.self_collision
-    n_global = n * world
-    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes,
-                      block_threads=args.block_threads, block_sync=args.block_sync)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
-    for w in range(args.warmup):
-        run_round(ctx, 10_000 + w, args, dist, world)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    launches0 = kernel_launches()
-    opt_events, round_events = [], []
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-        for s in range(args.steps):
-            flush.zero_()                             # L2 flush between timed steps (not timed)
-            r0 = torch.cuda.Event(enable_timing=True)
-            r1 = torch.cuda.Event(enable_timing=True)
-            r0.record()
-            run_round(ctx, 20_000 + s, args, dist, world, events=opt_events)
-            r1.record()
-            round_events.append((r0, r1))
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-    launches = kernel_launches() - launches0
-    t_round = sum(a.elapsed_time(b) for a, b in round_events) / 1e3
-    t_round = max_over_ranks(t_round, dist)
-    opt_ms = [a.elapsed_time(b) for a, b in opt_events]
-    opt_avg = statistics.mean(opt_ms) / 1e3
-    opt_avg = max_over_ranks(opt_avg, dist)
-    ps = n_global * args.adam_steps * args.steps
-    value = ps / t_round
-    clocks = clk.summary()
+    spec.self_collision = args.self_collision if self_collision is None else self_collision
+    return spec
 
-    # roofline of the dominant kernel (k_particle, fused Adam steps): ALU/FP32-pipe bound
+
+def default_n(args, cfg):
+    if args.n and cfg == args.config:
+        return args.n
+    if cfg == 4:
+        return 131072 // 8                           # config 4: 128K particles over 8 GPUs (per-rank share)
+    return CONFIG_SIZES[cfg]
+
+
+def roofline(ctx, args, opt_avg, clocks=None, cfg=None, n=None):
+    """Roofline of the dominant kernel (k_particle / k_serial: check_every fused Adam steps + the fused Eq. 3 check
+    per launch): algorithmic FP32-pipe instructions per launch / the launch's measured duration (CUDA events on
+    the launching stream), against 148 SM x 128 lanes x sm_max_mhz (ALU / issue bound)."""
     pk, src = peaks()
     w = dict(ctx.work)
     instr = algorithmic_instr(w)
     instr_check = algorithmic_instr_check(w)
-    # one timed launch = check_every fused Adam steps + the check of the final state (fused into the launch)
-    achieved = (instr * args.check_every + instr_check) * n / opt_avg / 1e12     # T instr/s per GPU
+    achieved = (instr * args.check_every + instr_check) * ctx.n / opt_avg / 1e12     # T instr/s per GPU
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    nsm = torch.cuda.get_device_properties(ctx.device).multi_processor_count
     peak = nsm * 128 * sm_max * 1e6 / 1e12
     traffic = None
     try:
@@ -423,35 +463,121 @@ def main():
     except Exception:
         pass
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tinstr/s", "frac": achieved / peak,
-            "traffic": traffic, "traffic_unit": "bytes per launch (ncu, profiles/ncu_traffic.json)",
-            "algorithmic_bytes_per_launch": n * (2 * 3 * ctx.D * 4 + 48 * ctx.n_grasp),
+            "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu --set full capture of this config / N, "
+                                                "profiles/ncu_traffic.json; null if none)",
+            "algorithmic_bytes_per_launch": ctx.n * (2 * 3 * ctx.D * 4 + 48 * ctx.n_grasp),
             "kernel": "k_serial<MODE_OPT>" if ctx.lanes_per_particle == 1 else "k_particle<MODE_OPT>",
             "note": f"FP32-pipe instructions (FFMA=1) of the minimal per-unit evaluation, {instr} per particle-step "
                     f"x {args.check_every} steps + {instr_check} for the Eq. 3 check fused into the launch; "
                     f"peak = {nsm} SM x 128 lanes x {sm_max:.0f} MHz ({src} sm_max_mhz)"}
     if clocks:
         roof["frac_at_measured_clock"] = achieved / (nsm * 128 * clocks["sm_mhz"] * 1e6 / 1e12)
+    return roof
+
+
+def timed_rounds(ctx, args, dist, world, flush, steps, seed0, side, opt_events=None):
+    """Exactly `steps` bench steps between a barrier + synchronize on both sides; returns the max-over-ranks
+    device time (s) of the steps (CUDA events on the launching stream, L2 flushed before each step, untimed)."""
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev = []
+    for s in range(steps):
+        flush.zero_()                                 # L2 flush between timed steps (not timed)
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record()
+        run_round(ctx, seed0 + s, args, dist, world, events=opt_events, side=side)
+        r1.record()
+        ev.append((r0, r1))
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / 1e3, dist)
+
+
+def extra_workload(args, cfg, n, dist, world, rank, dev, flush, side, self_collision=False, steps=3):
+    """A further workload of the same metric (not the headline): value, kernel rate and roofline fraction."""
+    spec = make_spec(args, cfg, n, self_collision)
+    from paper_2411_11833_b200 import TampContext
+    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n * world, device=dev)
+    for w in range(2):
+        run_round(ctx, 50_000 + w, args, dist, world, side=side)
+    ev = []
+    t = timed_rounds(ctx, args, dist, world, flush, steps, 60_000, side, ev)
+    opt_avg = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ev) / 1e3, dist)
+    roof = roofline(ctx, args, opt_avg, cfg=cfg, n=n)
+    return {"workload": f"config{cfg}:{CONFIG_NAMES[cfg]}" + (" + SELF" if self_collision else ""),
+            "particles_per_gpu": n, "value": n * world * args.adam_steps * steps / t, "unit": UNIT,
+            "ms_per_step": t / steps * 1e3, "kernel_ms_per_launch": opt_avg * 1e3,
+            "kernel_particle_steps_per_s": n * world * args.check_every / opt_avg,
+            "roofline_frac": roof["frac"], "lanes_per_particle": ctx.lanes_per_particle,
+            "block_threads": ctx.block_threads, "steps": steps}
+
+
+def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (the driver launches torchrun itself)
+        if args.impl == "ours" and torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA device(s)")
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    world, rank, local, dist = dist_init(args)
+    if args.impl == "reference":
+        bench_reference(args, world, rank, dist)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    from paper_2411_11833_b200 import TampContext, kernel_launches, lib_path
+    import paper_2411_11833_b200.build as bld
+    bld.build()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    torch.set_num_threads(1)
+    cfg = args.config
+    n = default_n(args, cfg)
+    spec = make_spec(args, cfg, n)
+    n_global = n * world
+    ctx = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev, lanes_per_particle=args.lanes,
+                      block_threads=args.block_threads, block_sync=args.block_sync)
+    side = None if (args.no_overlap or dist is None) else torch.cuda.Stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
+    for w in range(args.warmup):
+        run_round(ctx, 10_000 + w, args, dist, world, side=side)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    launches0 = kernel_launches()
+    opt_events, reps = [], []
+    with ClockSampler(local) as clk:
+        for r in range(args.repeats):
+            t_round = timed_rounds(ctx, args, dist, world, flush, args.steps, 20_000 + 1000 * r, side, opt_events)
+            reps.append((t_round, n_global * args.adam_steps * args.steps / t_round))
+    launches = (kernel_launches() - launches0) // args.repeats
+    t_round, value = sorted(reps, key=lambda tv: tv[1])[len(reps) // 2]        # median of the repeats
+    opt_avg = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in opt_events) / 1e3, dist)
+    clocks = clk.summary()
+    roof = roofline(ctx, args, opt_avg, clocks, cfg, n)
 
     # end-to-end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
         host_counts = torch.zeros(ctx.n_hard + 2, dtype=torch.int32).pin_memory()
         host_rec = torch.zeros(args.k, ctx.D + 4, dtype=torch.float32).pin_memory()
+
+        def fresh():
+            return TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
+                               lanes_per_particle=args.lanes, block_threads=args.block_threads,
+                               block_sync=args.block_sync)                 # host descriptor in, every step
         for w_ in range(2):
-            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
-                             lanes_per_particle=args.lanes,
-                      block_threads=args.block_threads, block_sync=args.block_sync)
-            run_round(c2, 30_000 + w_, args, dist, world, host_counts=host_counts, host_rec=host_rec)
+            run_round(fresh(), 30_000 + w_, args, dist, world, host_counts=host_counts, host_rec=host_rec, side=side)
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
         e2e_steps = max(3, min(args.steps, 10))
         for s in range(e2e_steps):
-            c2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
-                             lanes_per_particle=args.lanes,
-                      block_threads=args.block_threads, block_sync=args.block_sync)                 # host descriptor in
-            run_round(c2, 40_000 + s, args, dist, world, host_counts=host_counts, host_rec=host_rec)
+            run_round(fresh(), 40_000 + s, args, dist, world, host_counts=host_counts, host_rec=host_rec, side=side)
         torch.cuda.synchronize()
         te = max_over_ranks(time.perf_counter() - t0, dist)
         import ctypes
@@ -461,10 +587,19 @@ def main():
         e2e = {"value": n_global * args.adam_steps * e2e_steps / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
 
+    extra = []
+    if not args.no_extra:
+        for ecfg, en, eself in ((2, 8192, False), (1, 1 << 20, False), (cfg, n, True)):
+            if ecfg == cfg and not eself:
+                continue
+            extra.append(extra_workload(args, ecfg, en, dist, world, rank, dev, flush, side, self_collision=eself))
+
     tt = None if args.no_ttfs else ttfs(ctx, args, dist, world, seed=1000 * cfg)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, make_config(cfg, n=256), args.cpu_seconds)
+        # the oracle leg re-checks parity on the bench context: bring it back to the timed rounds' state
+        run_round(ctx, 20_000, args, dist, world)
+        cpu = cpu_baseline(args, make_config(cfg, n=256), args.cpu_seconds, ctx=ctx)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -476,13 +611,16 @@ def main():
                            "check_every": args.check_every, "best_k": args.k, "l2": "flushed between steps",
                            "ik_iters": args.ik_iters, "ik_seeds": args.ik_seeds, "self_collision": args.self_collision,
                            "lanes_per_particle": ctx.lanes_per_particle, "block_threads": ctx.block_threads,
-                           "block_sync": ctx.block_sync,
+                           "block_sync": ctx.block_sync, "allreduce": "side stream, overlapped" if side else "inline",
                            "parallelism": f"dp{world}"},
+                "repeats": {"n": len(reps), "values": [v for _, v in reps], "reported": "median"},
                 "kernel_ms_per_launch": opt_avg * 1e3, "kernel_steps_per_launch": args.check_every,
                 "kernel_launch": "check_every fused Adam steps + the Eq. 3 check of the final state",
                 "kernel_particle_steps_per_s": n_global * args.check_every / opt_avg,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "ttfs": tt}
+                "clocks": clocks, "ttfs": tt, "extra": extra, "lib": os.path.relpath(lib_path(), ROOT),
+                "scaling_note": "weak scaling (particles per GPU fixed); no multi-GPU curve exists until a driver "
+                                "SCALE run" if world == 1 else "weak scaling, max over ranks"}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -455,19 +455,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     const int64_t pid = (int64_t)blockIdx.x * (blockDim.x / GS) + grp;
     const bool active = pid < A.n;
     const int64_t p = active ? pid : (A.n - 1);
-    float* S = reinterpret_cast<float*>(smem4) + (size_t)grp * A.stride;
+    // dynamic shared memory: [constant instances, shared by the block | per-particle areas of A.stride floats]
+    float* const cinst = reinterpret_cast<float*>(smem4);
+    float* S = cinst + A.const_floats + (size_t)grp * A.stride;
     float* xs = S;
     float* gs = S + A.off_g;
-    float* ipose = S + A.off_ipose;
-    float4* isph = reinterpret_cast<float4*>(S + A.off_isph);
-    float* iwr = S + A.off_iwr;
+    float* const minst = S + A.off_inst;
     float* gT = S + A.off_gT;
     float* gTi = S + A.off_gTi;
+    // an object instance's block of kInstFloats floats: [pose rows 3x4 | world bounding sphere | 8 world sphere
+    // centres (float4) | wrench (movable only)]; constant instances live once per block, movable ones per particle
+    auto inst = [&](int i) -> float* {
+        const KInst& I = P.inst[i];
+        return (I.xoff >= 0 ? minst : cinst) + kInstFloats * I.slot;
+    };
+    auto ipose = [&](int i) -> float* { return inst(i); };
+    auto isph = [&](int i) -> float4* { return reinterpret_cast<float4*>(inst(i) + 16); };
+    auto iwr = [&](int i) -> float* { return inst(i) + 48; };
     const int D = P.D;
     auto phase_sync = [&]() {
         if (BSYNC > 0) __syncthreads(); else __syncwarp();
     };
-    auto ibound = [&](int i) { return *reinterpret_cast<const float4*>(ipose + 16 * i + 12); };
+    auto ibound = [&](int i) { return *reinterpret_cast<const float4*>(inst(i) + 12); };
 
     for (int i = threadIdx.x; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += blockDim.x) {
         const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
@@ -502,15 +511,41 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     for (int d = gl; d < D; d += GS) xs[d] = xg[d];
     const float* gg = A.grasp + (p * P.n_grasp) * 12;
 #pragma unroll 4
-    for (int i = gl; i < P.n_grasp * 12; i += GS) gT[(i / 12) * 16 + (i % 12)] = gg[i];
+    for (int i = gl; i < P.n_grasp * 12; i += GS) gT[i] = gg[i];
     bool invalid = A.invalid[p] != 0;
+    // constant object instances (bold p0 constants): pose and world spheres, once per block
+    for (int i = 0; i < P.n_inst; ++i) {
+        const KInst& I = P.inst[i];
+        if (I.xoff >= 0) continue;
+        float sy, cy;
+        fsincos(I.pose[3], &sy, &cy);
+        float* ip = cinst + kInstFloats * I.slot;
+        const float px = I.pose[0], py = I.pose[1], pz = I.pose[2];
+        for (int k = threadIdx.x; k <= TAMP_MAX_OBJ_SPHERES; k += blockDim.x) {
+            if (k == TAMP_MAX_OBJ_SPHERES) {
+                ip[0] = cy; ip[1] = -sy; ip[2] = 0.f; ip[3] = px;
+                ip[4] = sy; ip[5] = cy; ip[6] = 0.f; ip[7] = py;
+                ip[8] = 0.f; ip[9] = 0.f; ip[10] = 1.f; ip[11] = pz;
+                const float* ob = P.obound[I.obj];
+                ip[12] = fmaf(cy, ob[0], fmaf(-sy, ob[1], px));
+                ip[13] = fmaf(sy, ob[0], fmaf(cy, ob[1], py));
+                ip[14] = pz + ob[2];
+                ip[15] = ob[3];
+            } else {
+                const float* c = P.osph[I.obj][k];
+                reinterpret_cast<float4*>(ip + 16)[k] = k < P.osph_n[I.obj]
+                    ? make_float4(fmaf(cy, c[0], fmaf(-sy, c[1], px)), fmaf(sy, c[0], fmaf(cy, c[1], py)), pz + c[2], c[3])
+                    : make_float4(kFar, kFar, kFar, 0.f);
+            }
+        }
+    }
     __syncthreads();
-    {   // inverse grasps (held objects at knots): one grasp per lane of the group
+    if (A.off_gTi >= 0) {   // inverse grasps (held objects at knots): one grasp per lane of the group
         for (int k = gl; k < P.n_grasp; k += GS) {
             M34 g, gi;
-            load_m34(g, gT + 16 * k);
+            load_m34(g, gT + 12 * k);
             inv_m34(g, gi);
-            float* o = gTi + 16 * k;
+            float* o = gTi + 12 * k;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 o[4 * i] = gi.r[3 * i]; o[4 * i + 1] = gi.r[3 * i + 1]; o[4 * i + 2] = gi.r[3 * i + 2];
@@ -528,16 +563,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         TermSink<M> sink;
         float soft = 0.f;
 
-        // ---- phase A: object instances (poses, world sphere centres), zero accumulators ----
+        // ---- phase A: movable object instances (poses, world sphere centres), zero accumulators ----
         for (int i = 0; i < P.n_inst; ++i) {
             const KInst& I = P.inst[i];
-            if (I.xoff < 0 && it > 0) continue;      // constant instances: set up once per launch
-            float px, py, pz, yaw;
-            if (I.xoff >= 0) { px = xs[I.xoff]; py = xs[I.xoff + 1]; pz = xs[I.xoff + 2]; yaw = xs[I.xoff + 3]; }
-            else { px = I.pose[0]; py = I.pose[1]; pz = I.pose[2]; yaw = I.pose[3]; }
+            if (I.xoff < 0) continue;      // constant instances: set up once per block (prologue)
+            const float px = xs[I.xoff], py = xs[I.xoff + 1], pz = xs[I.xoff + 2], yaw = xs[I.xoff + 3];
             float sy, cy;
             fsincos(yaw, &sy, &cy);
-            float* ip = ipose + 16 * i;      // [R row0 | t0, R row1 | t1, R row2 | t2, bounding sphere]
+            float* ip = minst + kInstFloats * I.slot;   // [R row0 | t0, R row1 | t1, R row2 | t2, bounding sphere]
             if (gl == 0) {
                 ip[0] = cy; ip[1] = -sy; ip[2] = 0.f; ip[3] = px;
                 ip[4] = sy; ip[5] = cy; ip[6] = 0.f; ip[7] = py;
@@ -550,12 +583,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             }
             for (int k = gl; k < TAMP_MAX_OBJ_SPHERES; k += GS) {
                 const float4 c = s_osph[I.obj][k];
-                isph[i * TAMP_MAX_OBJ_SPHERES + k] = k < P.osph_n[I.obj]
+                reinterpret_cast<float4*>(ip + 16)[k] = k < P.osph_n[I.obj]
                     ? make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w)
                     : make_float4(kFar, kFar, kFar, 0.f);
             }
             if (G)
-                for (int c = gl; c < 6; c += GS) iwr[8 * i + c] = 0.f;
+                for (int c = gl; c < 6; c += GS) ip[48 + c] = 0.f;
         }
         if (G) for (int d = gl; d < D; d += GS) gs[d] = 0.f;
         __syncwarp();
@@ -624,8 +657,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    jcf += pairs_vs_instance<G, NS>(w, rr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gw,
-                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); },
+                    jcf += pairs_vs_instance<G, NS>(w, rr, isph(ii), ibound(ii), lam_cf, gw,
+                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr(ii), ll, half, real); },
                         smooth);
                 }
             }
@@ -694,7 +727,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             // held object at a MoveHold knot: attached spheres T_ee T(g)^-1 c (CFreeTrajHold)
             if (K.held_grasp >= 0 && K.term_cf >= 0) {
                 M34 Gi, Tobj;
-                load_m34(Gi, gTi + 16 * K.held_grasp);
+                load_m34(Gi, gTi + 12 * K.held_grasp);
                 Tobj = compose(Tee, Gi);
                 const int ho = K.held_obj;
                 float h[NH][3], gh[NH][3], hr[NH];
@@ -711,8 +744,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH>(h, hr, P.obb[b], lam_cf, gh, smooth);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    jcf += pairs_vs_instance<G, NH>(h, hr, isph + ii * TAMP_MAX_OBJ_SPHERES, ibound(ii), lam_cf, gh,
-                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr + 8 * ii, ll, half, real); },
+                    jcf += pairs_vs_instance<G, NH>(h, hr, isph(ii), ibound(ii), lam_cf, gh,
+                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr(ii), ll, half, real); },
                         smooth);
                 }
                 if (G) {   // held-object wrench acts on the tool link (last lane of the segment)
@@ -733,8 +766,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             // Kin(q, o, g, p): FK(q) = T(p) T(g); residuals on every lane of the segment
             if (K.term_kp >= 0 || K.term_kr >= 0) {
                 M34 Tg;
-                load_m34(Tg, gT + 16 * K.kin_grasp);
-                const M34 Ts = compose_rz(ipose + 16 * K.kin_inst, Tg);
+                load_m34(Tg, gT + 12 * K.kin_grasp);
+                const M34 Ts = compose_rz(ipose(K.kin_inst), Tg);
                 // position error e = ||t_ee - t*||  (L5)
                 const float dx = Tee.t[0] - Ts.t[0], dy = Tee.t[1] - Ts.t[1], dz = Tee.t[2] - Ts.t[2];
                 const float e2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
@@ -773,7 +806,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     const bool movable = P.inst[K.kin_inst].xoff >= 0;
 #pragma unroll
                     for (int h = 0; h < HP; ++h) {      // halves add one after the other (deterministic)
-                        if (half == h && ll == 0 && real && movable) add_wrench(iwr + 8 * K.kin_inst, tw);
+                        if (half == h && ll == 0 && real && movable) add_wrench(iwr(K.kin_inst), tw);
                         if (HP > 1) __syncwarp();
                     }
                 }
@@ -885,7 +918,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
 #pragma unroll
             for (int u = 0; u < NSO; ++u) {
                 const int k = gl + GS * u;
-                const float4 c = k < TAMP_MAX_OBJ_SPHERES ? isph[ii * TAMP_MAX_OBJ_SPHERES + k]   // padded slots: far
+                const float4 c = k < TAMP_MAX_OBJ_SPHERES ? isph(ii)[k]   // padded slots: far
                                                           : make_float4(kFar, kFar, kFar, 0.f);
                 wq[u][0] = c.x; wq[u][1] = c.y; wq[u][2] = c.z;
                 rq[u] = c.w;
@@ -966,8 +999,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO>(wq, rqe, P.obb[b], lam_cp, gq, smooth);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
-                    jcp += pairs_vs_instance<G, NSO>(wq, rqe, isph + jj * TAMP_MAX_OBJ_SPHERES, ibound(jj), lam_cp, gq,
-                        [&](Wrench& pw) { flush_partner<G, GS>(pw, P.inst[jj].xoff >= 0, iwr + 8 * jj, gl); },
+                    jcp += pairs_vs_instance<G, NSO>(wq, rqe, isph(jj), ibound(jj), lam_cp, gq,
+                        [&](Wrench& pw) { flush_partner<G, GS>(pw, P.inst[jj].xoff >= 0, iwr(jj), gl); },
                         smooth);
                 }
                 finish_term<M>(P, A, sink, Q.term_cp, term_sum<M, GS>(jcp), gl, active, p, s_counts);
@@ -977,7 +1010,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 for (int u = 0; u < NSO; ++u)
                     if (gl + GS * u < no) own.add_point(wq[u][0], wq[u][1], wq[u][2], gq[u][0], gq[u][1], gq[u][2]);
                 own.template group_sum<GS>();
-                if (gl == 0) add_wrench(iwr + 8 * ii, own);
+                if (gl == 0) add_wrench(iwr(ii), own);
             }
         }
 
@@ -985,8 +1018,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         if (P.n_goal > 1) {   // MinimizeObjDist: sum_{i<j} ||P_i - P_j||  (Listing 2 obj_dist)
             for (int a = 0; a < P.n_goal; ++a) {
                 for (int b = a + 1; b < P.n_goal; ++b) {
-                    const float* pa = ipose + 16 * P.goal_inst[a];
-                    const float* pb = ipose + 16 * P.goal_inst[b];
+                    const float* pa = ipose(P.goal_inst[a]);
+                    const float* pb = ipose(P.goal_inst[b]);
                     const float dx = pa[3] - pb[3], dy = pa[7] - pb[7], dz = pa[11] - pb[11];
                     const float d = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                     soft = fmaf(P.lam_goal, d, soft);
@@ -994,14 +1027,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                         const float k = P.lam_goal / d;
                         const int ia = P.goal_inst[a], ib = P.goal_inst[b];
                         if (P.inst[ia].xoff >= 0) {
-                            float* t = iwr + 8 * ia;
+                            float* t = iwr(ia);
                             t[0] += dx * k; t[1] += dy * k; t[2] += dz * k;
                             t[3] += pa[7] * dz * k - pa[11] * dy * k;
                             t[4] += pa[11] * dx * k - pa[3] * dz * k;
                             t[5] += pa[3] * dy * k - pa[7] * dx * k;
                         }
                         if (P.inst[ib].xoff >= 0) {
-                            float* t = iwr + 8 * ib;
+                            float* t = iwr(ib);
                             t[0] -= dx * k; t[1] -= dy * k; t[2] -= dz * k;
                             t[3] -= pb[7] * dz * k - pb[11] * dy * k;
                             t[4] -= pb[11] * dx * k - pb[3] * dz * k;
@@ -1056,7 +1089,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             for (int i = 0; i < P.n_inst; ++i) {
                 const KInst& I = P.inst[i];
                 if (I.xoff < 0) continue;
-                const float* wr = iwr + 8 * i;
+                const float* wr = iwr(i);
                 if (gl < 3) {
                     gs[I.xoff + gl] += wr[gl];
                 } else if (gl == 3) {   // d/dyaw = z . (M - t x F)

@@ -75,7 +75,7 @@ struct tamp_ctx {
     size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, o_iklist, o_ikn, o_ikbest, total;
     int64_t n_keys = 0;
     // shared-memory layout of the particle kernel (floats per particle)
-    int stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi, off_rsw;
+    int stride, off_g, off_inst, off_gT, off_gTi, off_rsw, const_floats;
     size_t smem = 0;
     int gs = 8;                  // lanes per particle in the particle kernel
     int ik_iters = 0;            // conditional IK sampler iterations
@@ -412,6 +412,9 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
         KInst& I = P.inst[n_inst];
         I.obj = (int16_t)V.obj;
         I.xoff = (int16_t)(V.is_const ? -1 : xoff[v]);
+        int slot = 0;
+        for (int j = 0; j < n_inst; ++j) slot += (P.inst[j].xoff < 0) == (I.xoff < 0);
+        I.slot = (int16_t)slot;
         for (int k = 0; k < 4; ++k) I.pose[k] = V.is_const ? V.value[k] : 0.f;
         if (V.is_const && init_inst[V.obj] < 0) init_inst[V.obj] = n_inst;
         inst_of[v] = n_inst++;
@@ -690,16 +693,18 @@ static void smem_layout(tamp_ctx* c) {
     off += r4(P.D);
     c->off_g = off;
     off += r4(P.D);
-    c->off_ipose = off;
-    off += 16 * P.n_inst;
-    c->off_isph = off;
-    off += 4 * TAMP_MAX_OBJ_SPHERES * P.n_inst;
-    c->off_iwr = off;
-    off += 8 * P.n_inst;
-    c->off_gT = off;
-    off += 16 * P.n_grasp;
-    c->off_gTi = off;
-    off += 16 * P.n_grasp;
+    int n_mov = 0, n_const = 0;
+    bool held = false;
+    for (int i = 0; i < P.n_inst; ++i) (P.inst[i].xoff >= 0 ? n_mov : n_const)++;
+    for (int f = 0; f < P.n_fk; ++f) held |= P.fk[f].held_grasp >= 0;
+    c->off_inst = off;                                // movable instances (kInstFloats each, 16-byte aligned)
+    off += kInstFloats * n_mov;
+    c->off_gT = off;                                  // grasps 3x4
+    off += 12 * P.n_grasp;
+    c->off_gTi = held ? off : -1;                     // inverse grasps (held objects at knots only)
+    off += held ? 12 * P.n_grasp : 0;
+    off = r4(off);
+    c->const_floats = kInstFloats * n_const;          // constant instances: once per block
     c->off_rsw = off;                                 // robot sphere centres for the SELF term (2 FK halves)
     off += P.has_self ? 2 * 4 * (kGroup * TAMP_MAX_SPHERES_PER_LINK + kGroup) : 0;   // + link bounding spheres
     // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
@@ -778,9 +783,8 @@ static KArgs base_args(tamp_ctx* c) {
     A.gofs = c->gofs;
     A.stride = c->stride;
     A.off_g = c->off_g;
-    A.off_ipose = c->off_ipose;
-    A.off_isph = c->off_isph;
-    A.off_iwr = c->off_iwr;
+    A.off_inst = c->off_inst;
+    A.const_floats = c->const_floats;
     A.off_gT = c->off_gT;
     A.off_gTi = c->off_gTi;
     A.off_rsw = c->off_rsw;
@@ -886,7 +890,9 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         cudaGetLastError();
         const bool many_waves = n_local > (int64_t)n_sm * 4 * (768 / 8);
-        if (many_waves && 128 * c->stride_bytes + 4096 <= smem_optin) c->gs = 4;
+        // (small skeletons only: on the Tetris skeletons the 4-lane blocks were 1.6x slower than 8 lanes in
+        // 896-thread blocks, profiles/r2_sweep_cfg5_262k.txt)
+        if (many_waves && c->P.D <= 32 && 128 * c->stride_bytes + 4 * c->const_floats + 4096 <= smem_optin) c->gs = 4;
     }
     if (c->gs == 1) {
         // serial mapping (particle_serial.cuh): one thread per particle, per-thread state in shared memory
@@ -937,23 +943,23 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         cudaGetLastError();
         const int ppw = 32 / c->gs;                                     // particles per warp
-        const int static_smem = 4096;
-        const int max_threads = c->gs == 8 ? 768 : 512;                // __launch_bounds__ of the variants
+        const int static_smem = 4096 + 4 * c->const_floats;   // + block-shared constant instances
+        // __launch_bounds__ of the variants: 8 lanes up to 1024 threads (hinge; 768 for the smooth cost), else 512
+        const int max_threads = c->gs == 8 ? (C.P.smooth > 0.f ? 768 : 1024) : 512;
         int max_pp = std::min(max_threads / c->gs, (smem_optin - static_smem) / c->stride_bytes);
         max_pp = (max_pp / ppw) * ppw;
         if (desc->block_threads) {
             if (desc->block_threads % 32 || desc->block_threads < 32 || desc->block_threads > max_threads) {
                 delete c;
-                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 768] (512 for 4 / 16 lanes)");
+                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024] for 8 lanes (768 with "
+                                            "the smooth cost; 512 for 4 / 16 lanes)");
             }
             c->threads = desc->block_threads;
         } else {
             // measured (profiles/README.md, sweeps 8-10):
             //  - if every particle of the launch is resident at once with one block per SM holding that SM's
             //    share, that block with phase-level barriers is best (config 2 at 8K);
-            //  - otherwise the block size that maximises resident warps per SM (registers, shared memory),
-            //    ties broken toward 2 blocks per SM, with phase-level barriers (config 3: 608 threads,
-            //    config 1: 384 threads).
+            //  - otherwise the block size with the lowest estimated launch time over balanced waves (below).
             int64_t pp = (n_local + n_sm - 1) / n_sm;                      // this SM's share
             pp = ((pp + ppw - 1) / ppw) * ppw;
             c->bsync = 1;
@@ -967,18 +973,28 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
                     const int by_smem = (smem_optin + 1024) / (ppb * c->stride_bytes + static_smem + 1024);
                     return std::min(std::min(by_regs, by_smem), 32);
                 };
-                if (384 <= max_threads && 384 / c->gs <= max_pp && blocks_per_sm(384) >= 2) {
-                    c->threads = 384;                                       // config 1 sweet spot
-                } else {                                                    // max resident warps per SM
-                    int best_t = 128, best_w = -1;
-                    for (int t = 128; t <= max_threads; t += 32) {
-                        const int ppb = t / c->gs;
-                        if (ppb % ppw || ppb > max_pp) continue;
-                        const int w = blocks_per_sm(t) * (t / 32);
-                        if (w >= best_w) { best_w = w; best_t = t; }
-                    }
-                    c->threads = best_t;
+                // multi-wave: the block size whose launch is estimated fastest.  Each wave is balanced (the block
+                // shrunk so every wave is equally full) and costs W x (w + 20) for W waves of w resident warps per
+                // SM: the rate per SM grows as w / (w + 20), fitted to config 3 (76 particles per SM = 19 warps,
+                // 3 waves: 2.29 ms; 96 = 24 warps, 3 waves: 2.59 ms).  Fewer, fuller waves win: config 3 at
+                // 32,768 runs 2 waves of 111 particles (888 threads, the 896-bound variant) instead of 3 of 74.
+                double best_cost = 1e300;
+                int best_t = 128, best_b = 1, best_W = 1;
+                for (int t = 128; t <= max_threads; t += 32) {
+                    const int ppb = t / c->gs;
+                    if (ppb % ppw || ppb > max_pp) continue;
+                    const int bps = blocks_per_sm(t);
+                    if (bps < 1) continue;
+                    const int64_t cap = (int64_t)n_sm * bps * ppb;              // particles per wave
+                    const int64_t W = (n_local + cap - 1) / cap;
+                    const int64_t p_sm = (n_local + (int64_t)n_sm * W - 1) / ((int64_t)n_sm * W);
+                    const double w = (double)p_sm * c->gs / 32.0;
+                    const double cost = (double)W * (w + 20.0);
+                    if (cost < best_cost - 1e-9) { best_cost = cost; best_t = t; best_b = bps; best_W = (int)W; }
                 }
+                int64_t ppb = (n_local + (int64_t)n_sm * best_W * best_b - 1) / ((int64_t)n_sm * best_W * best_b);
+                ppb = ((ppb + ppw - 1) / ppw) * ppw;
+                c->threads = (int)std::min<int64_t>(ppb * c->gs, best_t);
             }
         }
         if (c->threads / c->gs > max_pp) {
@@ -991,7 +1007,7 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         }
         if (desc->block_threads && desc->block_sync < 0) c->bsync = 2;
         if (desc->block_sync >= 0) c->bsync = desc->block_sync;
-        c->smem = (size_t)(c->threads / c->gs) * c->stride_bytes;
+        c->smem = (size_t)(c->threads / c->gs) * c->stride_bytes + 4 * (size_t)c->const_floats;
     }
     if (ws_bytes < c->total) {
         delete c;

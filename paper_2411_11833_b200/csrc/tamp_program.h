@@ -17,6 +17,7 @@ constexpr int kMaxPartners = 1024;    // collision partner instance references
 constexpr int kMaxConstConf = 8;      // constant confs referenced by trajectories (q0)
 constexpr int kGroup = 8;             // lanes per particle: one per link frame (7 joints + tool)
 constexpr int kMaxStepsPerLaunch = 64; // fused Adam steps per particle-kernel launch
+constexpr int kInstFloats = 56;        // shared memory per object instance: pose 3x4, bounding sphere, 8 spheres, wrench
 
 // One robot configuration evaluated per particle-step: a Pick/Place conf or a trajectory knot.
 struct KFk {
@@ -37,6 +38,8 @@ struct KFk {
 struct KInst {
     int16_t obj;
     int16_t xoff;
+    int16_t slot;                     // index among the movable (xoff >= 0, per particle) or the constant (per block)
+                                      // instances: the kernel keeps kInstFloats floats of shared memory for each
     float pose[4];                    // x y z yaw (constant instances)
 };
 
@@ -127,7 +130,9 @@ struct KArgs {
     const float* hi;       // [D]
     int64_t n;
     int64_t gofs;
-    int32_t stride, off_g, off_ipose, off_isph, off_iwr, off_gT, off_gTi, off_rsw;
+    int32_t stride, off_g, off_inst, off_gT, off_gTi, off_rsw;   // per-particle shared memory (floats); off_gTi < 0:
+                                                               // no held object at a knot, no inverse grasps
+    int32_t const_floats;  // block-shared constant instances at the start of dynamic shared memory
     int32_t n_steps, t0;
     int32_t bsync;         // serial mapping: block barriers per configuration / phase (shared i-cache)
     int32_t check_after;   // MODE_OPT: run the Eq. 3 check of the final state in the same launch

@@ -99,18 +99,28 @@ EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_size
            "tamp_set_state", "tamp_destroy", "tamp_kernel_launches", "tamp_plan_heuristic"]
 
 _lib = None
+_lib_path = None
+
+
+def lib_path() -> str:
+    """Path of the libtamp.so this process loaded (or would load)."""
+    return _lib_path or LIB_PATH
 
 
 def load(path: str = None):
-    """Load libtamp.so (raises if absent: the product path has no fallback).  TAMP_LIB selects another build
-    of the same library (A/B kernel experiments)."""
-    global _lib
+    """Load the in-tree libtamp.so (raises if absent: the product path has no fallback).  `path` may name another
+    in-tree build of the same library (A/B kernel experiments); it must live inside this repository."""
+    global _lib, _lib_path
     if _lib is not None:
         return _lib
-    path = path or os.environ.get("TAMP_LIB") or LIB_PATH
+    path = os.path.abspath(path or LIB_PATH)
+    root = os.path.dirname(HERE)
+    if os.path.commonpath([path, root]) != root or os.path.basename(path) != "libtamp.so":
+        raise RuntimeError(f"refusing to load {path}: only in-tree builds of libtamp.so")
     if not os.path.exists(path):
         raise RuntimeError(f"libtamp.so not built ({path}); run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
+    _lib_path = path
     vp, sz = ctypes.c_void_p, ctypes.c_size_t
     lib.tamp_abi_version.restype = I32
     lib.tamp_last_error.restype = ctypes.c_char_p

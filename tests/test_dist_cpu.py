@@ -115,3 +115,53 @@ def test_two_rank_round_matches_single_process():
     np.testing.assert_array_equal(counts, c1.numpy())
     np.testing.assert_array_equal(merged[:, :4], ref[:, :4])
     np.testing.assert_allclose(merged[:, 4:], ref[:, 4:], rtol=0, atol=0)
+
+
+def _single_process_reference():
+    spec = make_config(1, n=N_PER_RANK * WORLD)
+    one = OracleCtx(spec, N_PER_RANK * WORLD, 0, N_PER_RANK * WORLD)
+    one.sample(123)
+    one.optimize(STEPS)
+    c1, _ = one.check()
+    return c1.numpy(), one.best_k(K).numpy()
+
+
+def test_bench_launcher_two_ranks(tmp_path):
+    """The launcher of `bench.py --gpus N` (bench.spawn_ranks: torch.distributed.run, one process per rank,
+    127.0.0.1) starting a world of 2 gloo ranks that run bench.run_round: same counts and best-k as one process."""
+    import bench
+    out = str(tmp_path / "r.npz")
+    rc = bench.spawn_ranks(WORLD, [out], script=os.path.join(os.path.dirname(__file__), "dist_round_worker.py"))
+    assert rc == 0
+    r = np.load(out)
+    assert int(r["world"]) == WORLD
+    c1, ref = _single_process_reference()
+    np.testing.assert_array_equal(r["counts"], c1)
+    np.testing.assert_array_equal(r["merged"], ref)
+
+
+def test_bench_gpus_2_reference_arm_through_the_launcher():
+    """`python bench.py --gpus 2 --impl reference` without torchrun: bench spawns 2 ranks itself (gloo for the
+    host-only reference arm); rank 0 prints the JSON line with n_gpus = 2, the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "1", "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+
+
+def test_bench_refuses_mismatched_world_size():
+    """--gpus N under a launcher that started a different number of ranks fails loudly."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

@@ -1,0 +1,108 @@
+"""GPU parity at the method's degenerate points, through the C ABI against the oracle.
+
+* rotation error theta within 1e-3 of pi and at pi (L4: the atan2 form of the geodesic angle; cost only, the
+  gradient direction is not unique there);
+* coincident sphere centres (L13: hinge r_a + r_b, zero gradient from that pair);
+* a residual exactly at its tolerance, J_c = eps_c, is satisfying, one float32 ulp beyond is not (Eq. 3 "<=",
+  L21).
+"""
+import copy
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tamp_oracle as O
+from paper_2411_11833_b200 import TampContext
+from paper_2411_11833_b200 import build as b
+from workloads import make_config
+from workloads.scenes import PLACEMENT
+
+from parity_utils import COST_ATOL, COST_RTOL, grad_ok, to_ctx_grasp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    b.build()
+    torch.cuda.set_device(0)
+
+
+def _ctx(spec, x32, g32):
+    n = x32.shape[0]
+    ctx = TampContext(spec, n)
+    ctx.set_state(torch.from_numpy(x32).cuda(), grasp=to_ctx_grasp(g32).cuda())
+    return ctx
+
+
+def test_rotation_error_near_pi_cost():
+    """Constructed satisfying pick-place particles (T(g) := T(p0)^-1 FK(q)) with the place target's yaw turned by
+    psi = pi - {1e-3, 3e-4, 1e-4, 0}: R_ee^T R* = R_g^T Rz(psi) R_g, so KR = psi exactly in the oracle; the GPU's
+    KR and every other J_c agree to the cost tolerance."""
+    from test_oracle_csp import _clear_pickplace, satisfying_particle
+    spec = _clear_pickplace()
+    csp = O.build_csp(spec)
+    rng = np.random.default_rng(11)
+    offs = [math.pi - 1e-3, math.pi - 3e-4, math.pi - 1e-4, math.pi, -(math.pi - 1e-3)]
+    xs, gs = [], []
+    for d in offs:
+        x, Tg = satisfying_particle(spec, csp, rng)
+        x[csp.offsets[csp.terms[8].placement] + 3] += d
+        xs.append(x)
+        gs.append(Tg[None])
+    x32, g32 = np.array(xs, np.float32), np.array(gs, np.float32)
+    ctx = _ctx(spec, x32, g32)
+    J, soft, Jc, _ = (t.cpu().numpy() for t in ctx.eval())
+    Jo, Jco, softo, _ = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    np.testing.assert_allclose(Jco[:, 7], np.abs(np.float32(offs)).astype(np.float64), atol=2e-6)
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+
+
+def test_coincident_sphere_centres():
+    """Config 2 with both obstructors placed at exactly the same pose: every sphere of A coincides with the same
+    sphere of B.  The CFreePlace hinge of such a pair is r_a + r_b and its gradient is 0 (L13); the other pairs
+    between the two are ordinary.  Cost, per-term costs and gradient agree with the oracle."""
+    n = 8
+    spec = make_config(2, n=n)
+    csp = O.build_csp(spec)
+    x, g = O.initialize_particles(spec, csp, 91, np.arange(n))
+    pa, pb = [vi for vi, v in enumerate(spec.variables) if v.kind == PLACEMENT and not v.const][:2]
+    x[:, csp.offsets[pb]:csp.offsets[pb] + 4] = x[:, csp.offsets[pa]:csp.offsets[pa] + 4]
+    x32, g32 = x.astype(np.float32), g.astype(np.float32)
+    ctx = _ctx(spec, x32, g32)
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    i_cp = [i for i, t in enumerate(csp.terms) if t.kind == "CP"][1]       # obstructor B placed next to A
+    r = spec.objects[1].spheres[:, 3]
+    assert np.all(Jco[:, i_cp] >= 2 * r.sum() - 1e-7)                       # 8 coincident pairs at r_a + r_b
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    assert grad_ok(grad, grado).all()
+
+
+def test_residual_exactly_at_tolerance_is_satisfying():
+    """StablePlace support |z_bottom - z_top| = eps_SS exactly (the region's surface lowered by eps_SS, a float32
+    number, the block at z = 0) is satisfying on the GPU as in the oracle ("5 mm exactly is satisfying");
+    lowering the surface by one more float32 ulp makes that term, and the particle, unsatisfied."""
+    from test_oracle_csp import _clear_pickplace, satisfying_particle
+    spec = _clear_pickplace()
+    csp = O.build_csp(spec)
+    rng = np.random.default_rng(12)
+    x, Tg = satisfying_particle(spec, csp, rng)
+    x32 = x[None].astype(np.float32)
+    g32 = Tg[None, None].astype(np.float32)
+    e = np.float32(spec.eps["SS"])
+    for z_top, sat in ((-e, True), (-np.nextafter(e, np.float32(1.0)), False)):
+        s2 = copy.deepcopy(spec)
+        s2.surfaces[0].frame[2] = float(z_top)
+        ctx = _ctx(s2, x32, g32)
+        cls = torch.empty(1, dtype=torch.uint8, device="cuda")
+        counts, _ = ctx.check(cls=cls)
+        counts = counts.cpu().numpy()
+        cls_o, counts_o, _, _, Jc_o = O.check(s2, csp, O.new_state(x32.astype(np.float64), g32.astype(np.float64)))
+        assert (cls.cpu().numpy()[0] == 0) == sat and (cls_o[0] == 0) == sat
+        assert counts[8] == (1 if sat else 0) and counts_o[8] == counts[8]
+        np.testing.assert_array_equal(counts, counts_o)

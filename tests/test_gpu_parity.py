@@ -140,14 +140,14 @@ def test_constructed_satisfying_particles_are_class0():
     assert np.all(Jc <= 1e-5)
 
 
-def test_best_k_exact_on_gpu_costs_and_oracle_order():
+def test_best_k_exact_on_gpu_costs():
+    """K4 selects exactly the lexsort of the GPU's own (class, cost, global index) keys."""
     cfg, n, k = 2, 301, 16
     spec, csp, x32, g32 = oracle_inputs(cfg, n, seed=40)
     gofs = 5000
     ctx = _ctx(spec, n, x32, g32, gofs=gofs, n_global=8192)
     rec = ctx.best_k(k)
     cls, cost, gidx, xk = decode_records(rec)
-    # exact against selection on the GPU's own (class, cost) arrays
     clsg = torch.empty(n, dtype=torch.uint8, device="cuda")
     ctx.check(cls=clsg)
     J, soft, _, _ = ctx.eval()
@@ -156,13 +156,54 @@ def test_best_k_exact_on_gpu_costs_and_oracle_order():
     order = np.lexsort((np.arange(n), costg, c))[:k]
     np.testing.assert_array_equal(gidx, order + gofs)
     np.testing.assert_array_equal(xk, x32[order])
-    # oracle selection agrees where neighbouring keys are separated by more than the cost tolerance
+
+
+def _assert_topk_matches_oracle(gidx, cls_sel, sel_o, cls_o, cost_o, k):
+    """The GPU's top-k equals the oracle's (L19 key): the class sequence exactly; the selected set exactly
+    (the boundary between positions k-1 and k must be separated by more than the cost tolerance -- asserted, so
+    the comparison can never be skipped); the order exactly across every separated neighbour pair (runs of
+    keys closer than the tolerance are compared as sets)."""
+    tol = lambda a, b: abs(a - b) > COST_RTOL * max(abs(a), abs(b)) + COST_ATOL
+    np.testing.assert_array_equal(cls_sel, cls_o[:k])
+    if k < len(cost_o):
+        assert cls_o[k] != cls_o[k - 1] or tol(cost_o[k], cost_o[k - 1]), "unseparated boundary: choose another k"
+        np.testing.assert_array_equal(np.sort(gidx), np.sort(sel_o[:k]))
+    start = 0
+    for i in range(1, k + 1):
+        if i == k or cls_o[i] != cls_o[i - 1] or tol(cost_o[i], cost_o[i - 1]):
+            np.testing.assert_array_equal(np.sort(gidx[start:i]), np.sort(sel_o[start:i]))
+            start = i
+
+
+@pytest.mark.parametrize("k", [16, 64, 301])
+def test_best_k_matches_oracle_with_satisfying_particles(k):
+    """Best-k against the oracle's best_k on the same particles: 40 hand-constructed satisfying particles
+    (class 0, soft cost = lambda_traj * psi, psi on a shuffled grid; tests/constructed.py), 259 sampled ones
+    (class 1, key J) and 2 invalid ones (NaN, class 2, last, by index).  k = 16 compares satisfying particles by
+    their soft cost, k = 64 also the 24 lowest J of the rest, k = n every particle's rank."""
+    from constructed import pickplace_hold_knots, satisfying_pickplace
+    n, gofs = 301, 5000
+    spec = pickplace_hold_knots(n=n)
+    csp = O.build_csp(spec)
+    x, g = O.initialize_particles(spec, csp, 41, np.arange(gofs, gofs + n))
+    rng = np.random.default_rng(3)
+    pos = rng.choice(n, 40, replace=False)
+    for p, psi in zip(pos, rng.permutation(np.linspace(0.1, 0.7, 40))):
+        x[p], g[p, 0] = satisfying_pickplace(spec, csp, rng, psi)
+    x32, g32 = x.astype(np.float32), g.astype(np.float32)
+    x32[[7, 200], 0] = np.nan
+    ctx = _ctx(spec, n, x32, g32, gofs=gofs, n_global=n + gofs)
+    rec = ctx.best_k(k)
+    cls_k, cost_k, gidx, xk = decode_records(rec)
     so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
-    cls_o, _, Jo, softo, _ = O.check(spec, csp, so)
-    sel_o, _, cost_o = O.best_k(cls_o, Jo, softo, np.arange(n) + gofs, k)
-    sep = np.diff(np.sort(cost_o)) > 1e-3 * np.abs(cost_o[1:])
-    if sep.all():
-        np.testing.assert_array_equal(gidx, sel_o + gofs)
+    cls_o, counts_o, Jo, softo, _ = O.check(spec, csp, so)
+    assert counts_o[-2] == 40 and counts_o[-1] == 2
+    sel_o, c_o, cost_o = O.best_k(cls_o, Jo, softo, np.arange(n) + gofs, n)
+    _assert_topk_matches_oracle(gidx, cls_k, sel_o + gofs, c_o, cost_o, k)      # O.best_k returns positions
+    fin = cls_k < 2
+    np.testing.assert_allclose(cost_k[fin], cost_o[:k][fin], rtol=COST_RTOL, atol=COST_ATOL)
+    if k == n:
+        np.testing.assert_array_equal(gidx[-2:], [gofs + 7, gofs + 200])
 
 
 @pytest.mark.parametrize("n,k", [(70000, 16), (70000, 64), (9000, 65), (5000, 1024), (300, 300)])
@@ -319,18 +360,29 @@ def test_host_buffers_through_the_c_abi():
     assert np.array_equal(ctx.get_state()["x"].cpu().numpy(), x32)
 
 
+N_SAMPLED = 48          # sampled particles the oracle recomputes at full size
+
+
+def _bounded_exclusions(kinks):
+    """At most 10 % of the sampled particles may sit on a kink (excluded from gradient / step parity), so at least
+    43 of 48 are compared element by element."""
+    assert kinks.mean() <= 0.1, f"{kinks.sum()} of {len(kinks)} sampled particles excluded as kinks"
+    assert (~kinks).sum() >= 20
+
+
 @pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20)])
 def test_full_size_sampled_against_oracle(cfg, n):
     """BASELINE sizes (config 4: its per-GPU share of 128K over 8 GPUs; config 1: the 1M throughput run) in
-    the auto launch configuration bench uses: sample + eval + 1 fused step on all particles; 24 sampled
-    particles recomputed by the oracle one by one from the same start (particles never couple)."""
+    the auto launch configuration bench uses: sample + eval + 1 fused step on all particles; 48 sampled
+    particles recomputed by the oracle one by one from the same start (particles never couple); at most
+    10 % of them excluded as kinks."""
     spec = make_config(cfg, n=n)
     csp = O.build_csp(spec)
     ctx = TampContext(spec, n)
     ctx.sample(seed=2000 + cfg)
     st0 = ctx.get_state()
     J, soft, Jc, grad = ctx.eval()
-    idx = np.sort(np.random.default_rng(5).choice(n, 24, replace=False))
+    idx = np.sort(np.random.default_rng(5).choice(n, N_SAMPLED, replace=False))
     J, soft, Jc, grad = (t.cpu().numpy()[idx] for t in (J, soft, Jc, grad))
     ctx.optimize(1)
     x1 = ctx.get_state()["x"].cpu().numpy()[idx]
@@ -344,6 +396,7 @@ def test_full_size_sampled_against_oracle(cfg, n):
     ok = grad_ok(grad, grado)
     kinks = kink_mask(spec, csp, x32, g32, grado, np.random.default_rng(2)) if not ok.all() else ~ok
     assert np.all(ok | kinks)
+    _bounded_exclusions(kinks)
     so = O.new_state(x32, g32)
     O.optimize(spec, csp, so, 1, 1.0 / n)
     unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
@@ -354,7 +407,7 @@ def test_full_size_sampled_against_oracle(cfg, n):
 @pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20)])
 def test_full_size_mid_optimisation_against_oracle(cfg, n):
     """The bench's own state: IK-initialised particles (ik_iters = 20, as bench.py) after 3 launches of 10 fused
-    steps (contact-rich: the IK puts grippers at their targets), in the auto launch configuration.  On 24
+    steps (contact-rich: the IK puts grippers at their targets), in the auto launch configuration.  On 48
     sampled particles the oracle recomputes cost, per-term costs and gradient at that state, and one more
     Adam step from the GPU's own moments (m, v, t): the state the bench's timed launches work on."""
     spec = make_config(cfg, n=n)
@@ -365,7 +418,7 @@ def test_full_size_mid_optimisation_against_oracle(cfg, n):
     for _ in range(3):
         ctx.optimize(10)
     st = ctx.get_state()
-    idx = np.sort(np.random.default_rng(6).choice(n, 24, replace=False))
+    idx = np.sort(np.random.default_rng(6).choice(n, N_SAMPLED, replace=False))
     x32 = st["x"].cpu().numpy()[idx].astype(np.float64)
     g32 = st["grasp"].cpu().numpy()[idx].reshape(len(idx), -1, 3, 4).astype(np.float64)
     m32, v32 = st["m"].cpu().numpy()[idx].astype(np.float64), st["v"].cpu().numpy()[idx].astype(np.float64)
@@ -377,6 +430,7 @@ def test_full_size_mid_optimisation_against_oracle(cfg, n):
     ok = grad_ok(grad, grado)
     kinks = kink_mask(spec, csp, x32, g32, grado, np.random.default_rng(3)) if not ok.all() else ~ok
     assert np.all(ok | kinks)
+    _bounded_exclusions(kinks)
     assert ctx.t == 30
     ctx.optimize(1)
     x1 = ctx.get_state()["x"].cpu().numpy()[idx]
@@ -392,7 +446,7 @@ def test_full_size_mid_optimisation_against_oracle(cfg, n):
 @pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384)])
 def test_full_size_fused_check_against_oracle(cfg, n):
     """The bench's interval at full size: IK-initialised particles, 20 steps, then 10 more with the Eq. 3 check
-    fused into the last launch (tamp_optimize_and_check).  On 24 sampled particles the oracle's check of the
+    fused into the last launch (tamp_optimize_and_check).  On 48 sampled particles the oracle's check of the
     final state gives the same class (epsilon-marginal residuals excepted, L21); over all particles the counts
     are those of Eq. 3 / Eq. 5 applied to the class vector and to the eval() residuals of the same state."""
     spec = make_config(cfg, n=n)
@@ -413,15 +467,22 @@ def test_full_size_fused_check_against_oracle(cfg, n):
     np.testing.assert_array_equal(counts[:-2], (Jc_all <= eps[None, :].astype(np.float32)).sum(axis=0))
     assert counts[-2] == int((cls_all == 0).sum()) and counts[-1] == int((cls_all == 2).sum())
     assert np.all(counts[:-2] >= counts[-2])
-    idx = np.sort(np.random.default_rng(7).choice(n, 24, replace=False))
+    idx = np.sort(np.random.default_rng(7).choice(n, N_SAMPLED, replace=False))
     x32 = st["x"].cpu().numpy()[idx].astype(np.float64)
     g32 = st["grasp"].cpu().numpy()[idx].reshape(len(idx), -1, 3, 4).astype(np.float64)
     so = O.new_state(x32, g32)
     so.invalid = st["invalid"].cpu().numpy()[idx].astype(bool)
     cls_o, _, _, _, Jc_o = O.check(spec, csp, so)
-    marginal = ((np.abs(Jc_o - eps[None, :]) <= 1e-4 * eps[None, :] + 1e-6) & (Jc_o > 0)).any(axis=1)
+    marg_c = (np.abs(Jc_o - eps[None, :]) <= 1e-4 * eps[None, :] + 1e-6) & (Jc_o > 0)
+    marginal = marg_c.any(axis=1)
     np.testing.assert_array_equal(cls_all[idx][~marginal], cls_o[~marginal])
-    assert marginal.sum() <= 2
+    assert marginal.sum() <= 0.1 * len(idx)
+    # per-term satisfied masks (the Eq. 5 counts' summands) of the sampled particles, epsilon-marginal entries
+    # excepted: the GPU's residuals of the fused check's state against the oracle's
+    m_gpu = Jc_all[idx] <= eps[None, :].astype(np.float32)
+    m_or = Jc_o <= eps[None, :]
+    np.testing.assert_array_equal(m_gpu[~marg_c], m_or[~marg_c])
+    assert marg_c.sum() <= 0.01 * marg_c.size
 
 def test_edge_sizes():
     """N = 1 (a lone particle in a 16-particle block) and k = N."""
@@ -474,11 +535,11 @@ def test_serial_mapping_launch_configuration_invariance_bit_exact():
 
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_register_budget_variants_bit_exact(cfg):
-    """8 lanes: blocks of <= 512 threads run the 512-bound (register-rich) instantiation, larger blocks the
-    768-bound one -- same arithmetic, bit-identical results."""
+    """8 lanes: blocks of <= 512 threads run the 512-bound (register-rich) instantiation, <= 768 the 768-bound one,
+    <= 896 / 1024 the 896- / 1024-bound ones (72 / 64 registers) -- same arithmetic, bit-identical results."""
     spec = make_config(cfg, n=600)
     ref = None
-    for threads in (256, 640):
+    for threads in (256, 640, 896, 1024):
         c = TampContext(spec, 600, lanes_per_particle=8, block_threads=threads, block_sync=1)
         c.sample(seed=9)
         c.optimize(5)
