@@ -67,6 +67,7 @@ def parse():
     p.add_argument("--repeats", type=int, default=5, help="timed regions of exactly --steps steps; value = median")
     p.add_argument("--no-extra", action="store_true", help="skip the extra workloads (config 2, config 1 at 1M, SELF)")
     p.add_argument("--no-overlap", action="store_true", help="all-reduce of the counts on the launching stream")
+    p.add_argument("--lib", default=None, help="A/B experiments: another in-tree build of libtamp.so (exp/<name>/)")
     return p.parse_args()
 
 
@@ -528,9 +529,12 @@ def main():
         if dist is not None:
             dist.destroy_process_group()
         return
-    from paper_2411_11833_b200 import TampContext, kernel_launches, lib_path
+    from paper_2411_11833_b200 import TampContext, kernel_launches, lib_path, load
     import paper_2411_11833_b200.build as bld
-    bld.build()
+    if args.lib:
+        load(args.lib)
+    else:
+        bld.build()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     torch.set_num_threads(1)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TAMP_ABI_VERSION 3
+#define TAMP_ABI_VERSION 4
 
 /* compiled limits of the sm_100a kernels (exceeding one returns TAMP_E_UNSUPPORTED) */
 #define TAMP_NJ 7                     /* 7-DOF arm */
@@ -105,8 +105,10 @@ typedef struct {
                                                      the SELF term (symmetric; typically non-adjacent links) */
 } tamp_robot_desc;
 
-/* static oriented box: centre, yaw about world z, half extents > 0 */
-typedef struct { float center[3]; float yaw; float half[3]; } tamp_obb_desc;
+/* static oriented box ("oriented bounding boxes"): centre, half extents > 0 and its orientation:
+   rot = the box-to-world rotation (3x3, row-major; must be orthonormal with det +1 to 1e-4, else TAMP_E_INVALID),
+   or all nine entries 0: the rotation Rz(yaw) about the world z axis */
+typedef struct { float center[3]; float yaw; float half[3]; float rot[9]; } tamp_obb_desc;
 
 /* movable object as spheres in its frame (origin = bottom centre, L15); sampler parameters:
    footprint = radius shrinking placement regions; top-down grasp TCP at (u*grasp_xy, v*grasp_y, grasp_z),

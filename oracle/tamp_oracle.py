@@ -140,6 +140,10 @@ def box_signed_distance(w, center, R, half):
 
 
 def obb_arrays(obb):
+    """Centre, box-to-world rotation and half extents of an oriented box: the full rotation R if the
+    scene gives one, else Rz(yaw) about the world z axis."""
+    if getattr(obb, "R", None) is not None:
+        return _t(obb.center), _t(np.asarray(obb.R, float)), _t(obb.half)
     c, s = math.cos(obb.yaw), math.sin(obb.yaw)
     R = _t([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
     return _t(obb.center), R, _t(obb.half)

@@ -55,11 +55,18 @@ def build(force=False, verbose=False):
             fcntl.flock(lock, fcntl.LOCK_UN)
 
 
-def _build(verbose=False):
-    os.makedirs(OBJ_DIR, exist_ok=True)
-    objs = [os.path.join(OBJ_DIR, os.path.basename(s)[:-3] + ".o") for s in SRCS]
+def build_variant(name, defines, verbose=False):
+    """A/B build of the same sources with extra -D defines into exp/<name>/libtamp.so (in-tree, git-ignored; bench
+    --lib loads it).  Not part of the product build."""
+    out = os.path.join(ROOT, "exp", name)
+    return _build(verbose, defines=defines, obj_dir=os.path.join(out, "obj"), lib=os.path.join(out, "libtamp.so"))
+
+
+def _build(verbose=False, defines=(), obj_dir=OBJ_DIR, lib=LIB):
+    os.makedirs(obj_dir, exist_ok=True)
+    objs = [os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o") for s in SRCS]
     procs = [subprocess.Popen([nvcc()] + NVCC_FLAGS + (FAST_DIV_SQRT if os.path.basename(s) in FAST_UNITS else [])
-                              + ["-c", "-o", o, s], stdout=subprocess.PIPE,
+                              + [f"-D{d}" for d in defines] + ["-c", "-o", o, s], stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True) for s, o in zip(SRCS, objs)]
     logs, failed = [], []
     for s, p in zip(SRCS, procs):
@@ -69,16 +76,16 @@ def _build(verbose=False):
             failed.append(s)
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(logs))
-    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"]
+    res = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib + ".tmp"]
                          + objs, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+    os.replace(lib + ".tmp", lib)
+    with open(os.path.join(os.path.dirname(lib), "ptxas_info.txt"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

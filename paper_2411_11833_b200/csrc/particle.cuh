@@ -10,6 +10,21 @@
 
 #include "tamp_program.h"
 
+// build-time variants of the sphere tests (A/B experiments, tools/build_variants.py; the defaults are the product):
+//   TAMP_PACK_XFORM   1: robot sphere centres transformed in packed pairs (FFMA2), 0: scalar
+//   TAMP_PACK_OBB     0: scalar sphere-box reject test (FMNMX), 1: packed pairs with a + |a| on the FMA pipe,
+//                     2: packed offsets / rotation, scalar max
+//   TAMP_PACK_NARROW  1: sphere-sphere pair tests in packed pairs (one predicate, bit masks only on a hit), 0: scalar
+#ifndef TAMP_PACK_XFORM
+#define TAMP_PACK_XFORM 1
+#endif
+#ifndef TAMP_PACK_OBB
+#define TAMP_PACK_OBB 1
+#endif
+#ifndef TAMP_PACK_NARROW
+#define TAMP_PACK_NARROW 1
+#endif
+
 namespace tamp {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -181,11 +196,15 @@ __device__ __forceinline__ float smooth_cost(float p, float s, float& gsc) {
 template <bool GRAD>
 __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float rr, const KObb& B, float lam,
                                             float& gx, float& gy, float& gz, float smooth = 0.f) {
-    // boxes are yawed about the world z axis (tamp_obb_desc): R = Rz(yaw), p = R^T (w - c)
+    // oriented box: p = R^T (w - c) with R the box's full rotation (row-major); for a box yawed
+    // about z (R[2] = R[5] = R[6] = R[7] = 0, R[8] = 1) the extra terms are exact zeros
     const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
-    const float px = fmaf(B.R[0], dx, B.R[3] * dy);
-    const float py = fmaf(B.R[1], dx, B.R[4] * dy);
-    const float pz = dz;
+    float px = dx, py = dy, pz = dz;                     // axis-aligned box: R = I (the same values, exactly)
+    if (!B.aligned) {
+        px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
+        py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
+        pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
+    }
     const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(pz) - B.h[2];
     const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
     const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
@@ -214,9 +233,9 @@ __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float 
     pen = smooth_cost(pen, smooth, gsc);
     lam *= gsc;
     if (GRAD) {   // dJ/dw = -R grad_p
-        gx = fmaf(-lam, fmaf(B.R[0], gpx, B.R[1] * gpy), gx);
-        gy = fmaf(-lam, fmaf(B.R[3], gpx, B.R[4] * gpy), gy);
-        gz = fmaf(-lam, gpz, gz);
+        gx = fmaf(-lam, fmaf(B.R[0], gpx, fmaf(B.R[1], gpy, B.R[2] * gpz)), gx);
+        gy = fmaf(-lam, fmaf(B.R[3], gpx, fmaf(B.R[4], gpy, B.R[5] * gpz)), gy);
+        gz = fmaf(-lam, fmaf(B.R[6], gpx, fmaf(B.R[7], gpy, B.R[8] * gpz)), gz);
     }
     return pen;
 }
@@ -226,9 +245,13 @@ __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float 
 // spheres whose hinges are all zero.
 __device__ __forceinline__ bool obb_within(float wx, float wy, float wz, float r, const KObb& B) {
     const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
-    const float px = fmaf(B.R[0], dx, B.R[3] * dy);
-    const float py = fmaf(B.R[1], dx, B.R[4] * dy);
-    const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(dz) - B.h[2];
+    float px = dx, py = dy, pz = dz;                     // axis-aligned box: R = I (the same values, exactly)
+    if (!B.aligned) {
+        px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
+        py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
+        pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
+    }
+    const float ax = fabsf(px) - B.h[0], ay = fabsf(py) - B.h[1], az = fabsf(pz) - B.h[2];
     const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
     const float s = fmaf(qx, qx, fmaf(qy, qy, qz * qz));
     return !(fmaxf(ax, fmaxf(ay, az)) > 0.f && s >= r * r);
@@ -264,94 +287,248 @@ __device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, flo
 constexpr float kFar = 1e18f;   // position of padded (absent) spheres: never within reach of anything
 constexpr float kBroadMaxRad = 0.5f;   // OBBs with a larger bounding sphere skip the broad phase and pre-test
 
-// NS query spheres per lane (registers) vs the 8 (padded) spheres of one object instance (shared memory,
-// broadcast to the group).  Fast path: branch-free test of all NS x 8 pairs (d^2 - (ra+rb)^2 < 0 ?), no
-// square roots; only if some pair of the warp is active are the hinges and gradients evaluated.
-// Returns the hinge sum; if GRAD accumulates dJ/dw_a (x lam) into g and the partner's wrench into pw.
-template <bool GRAD, int NS, class OnWrench>
-__device__ __forceinline__ float pairs_vs_instance(const float (&w)[NS][3], const float (&rr)[NS], const float4* Bs,
-                                                   const float4 bound, float lam, float (&g)[NS][3], OnWrench&& on_wrench,
-                                                   float smooth) {
-    // broad phase: skip the instance unless some query sphere of the warp reaches its bounding sphere
-    float mb = 1.f;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        const float dx = w[k][0] - bound.x, dy = w[k][1] - bound.y, dz = w[k][2] - bound.z;
-        const float R = rr[k] + bound.w;
-        mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+// ------------------------------------------------------------------------------------------------
+// packed fp32x2 arithmetic: FADD2 / FMUL2 / FFMA2 of sm_100a do two IEEE fp32 operations (round to nearest, each
+// half exactly the scalar FADD / FMUL / FFMA) in one issued instruction; a scalar operand packed as {a, a} is a
+// free broadcast.  The sphere tests below run on pairs of spheres: half the issue slots of the scalar code with
+// bit-identical results (measured issue rates on the B200: 3.8 FFMA vs 2.0 FFMA2 warp-instructions per cycle per
+// SM, i.e. the same FMA throughput for half the issue slots; tools/micro/pipe_rate.cu)
+// ------------------------------------------------------------------------------------------------
+struct F2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ F2 pk(float a, float b) {
+    F2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ F2 bc(float a) { return pk(a, a); }
+__device__ __forceinline__ float lo(F2 x) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+    return a;
+}
+__device__ __forceinline__ float hi(F2 x) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v));
+    return b;
+}
+__device__ __forceinline__ F2 add2(F2 a, F2 b) {
+    F2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 sub2(F2 a, F2 b) {
+    F2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 mul2(F2 a, F2 b) {
+    F2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+    F2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+// |d|^2 - R^2 with R = ra + rb, as fmaf(-R, R, |d|^2) per half (the scalar code's exact reject quantity);
+// -R = (-rb) - ra is exact, and both negations fold into the FADD2's operand modifiers
+__device__ __forceinline__ F2 reach2(F2 dx, F2 dy, F2 dz, F2 ra, float rb) {
+    return fma2(add2(ra, bc(rb)), sub2(bc(-rb), ra), fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
+}
+
+// NS query spheres of a lane, packed in pairs: sphere 2j in the low half of x[j] / y[j] / z[j], 2j + 1 in the high
+// half; r = radius + eta.  For odd NS the last high half is a far, radius-0 dummy (never reaches anything).
+template <int NS>
+struct QSet {
+    static constexpr int NP = (NS + 1) / 2;
+    F2 x[NP], y[NP], z[NP], r[NP];
+    __device__ __forceinline__ float sx(int k) const { return (k & 1) ? hi(x[k >> 1]) : lo(x[k >> 1]); }
+    __device__ __forceinline__ float sy(int k) const { return (k & 1) ? hi(y[k >> 1]) : lo(y[k >> 1]); }
+    __device__ __forceinline__ float sz(int k) const { return (k & 1) ? hi(z[k >> 1]) : lo(z[k >> 1]); }
+    __device__ __forceinline__ float sr(int k) const { return (k & 1) ? hi(r[k >> 1]) : lo(r[k >> 1]); }
+    __device__ __forceinline__ void set(int k, float px, float py, float pz, float pr) {   // k compile-time
+        if (k & 1) {
+            x[k >> 1] = pk(lo(x[k >> 1]), px); y[k >> 1] = pk(lo(y[k >> 1]), py);
+            z[k >> 1] = pk(lo(z[k >> 1]), pz); r[k >> 1] = pk(lo(r[k >> 1]), pr);
+        } else {
+            x[k >> 1] = pk(px, hi(x[k >> 1])); y[k >> 1] = pk(py, hi(y[k >> 1]));
+            z[k >> 1] = pk(pz, hi(z[k >> 1])); r[k >> 1] = pk(pr, hi(r[k >> 1]));
+        }
     }
-    if (!__any_sync(FULL, mb < 0.f)) return 0.f;
-    // narrow phase, branch-free: which of the NS x 8 pairs reach (d^2 < (ra + rb)^2)?
+    __device__ __forceinline__ void finish() {               // the odd dummy far away
+        if (NS & 1) {
+            x[NP - 1] = pk(lo(x[NP - 1]), kFar); y[NP - 1] = pk(lo(y[NP - 1]), kFar);
+            z[NP - 1] = pk(lo(z[NP - 1]), kFar); r[NP - 1] = pk(lo(r[NP - 1]), 0.f);
+        }
+    }
+};
+
+// does some query sphere reach the sphere (c, rad)?  (d^2 - (r + rad)^2 < 0, the scalar broad-phase test)
+template <int NS>
+__device__ __forceinline__ bool qset_near(const QSet<NS>& q, float cx, float cy, float cz, float rad) {
+    bool near = false;
+#pragma unroll
+    for (int j = 0; j < QSet<NS>::NP; ++j) {
+        const F2 t = reach2(sub2(q.x[j], bc(cx)), sub2(q.y[j], bc(cy)), sub2(q.z[j], bc(cz)), q.r[j], rad);
+        near = near || lo(t) < 0.f || hi(t) < 0.f;
+    }
+    return near;
+}
+
+// NS query spheres per lane vs the 8 (padded) spheres of one object instance (shared memory, SoA x[8] y[8] z[8]
+// r[8], broadcast to the group).  Fast path: the branch-free test of all NS x 8 pairs (d^2 - (ra+rb)^2 < 0 ?) on
+// packed sphere pairs (or, for one query sphere, on packed partner pairs), no square roots, recorded as one bit
+// per pair; only if some lane of the warp has an active pair are the exact hinges and gradients of the active
+// pairs evaluated.  Returns the hinge sum; if GRAD accumulates dJ/dw_a (x lam) into g and the partner's wrench
+// into pw.
+template <int NS, class F>
+__device__ __forceinline__ void instance_pair_tests(const QSet<NS>& q, const float* X, F&& on) {
+    if (!TAMP_PACK_NARROW) {    // scalar: d^2 - R^2 per pair
+#pragma unroll
+        for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
+            const float bx = X[b], by = X[8 + b], bz = X[16 + b], br = X[24 + b];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const float dx = q.sx(k) - bx, dy = q.sy(k) - by, dz = q.sz(k) - bz;
+                const float R = q.sr(k) + br;
+                on(k, b, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+            }
+        }
+    } else if (NS == 1) {      // one query sphere: packed over the partner's sphere pairs (adjacent in the SoA rows)
+        const float qx = lo(q.x[0]), qy = lo(q.y[0]), qz = lo(q.z[0]), qr = lo(q.r[0]);
+#pragma unroll
+        for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; b += 2) {
+            const F2 bx = *reinterpret_cast<const F2*>(X + b), by = *reinterpret_cast<const F2*>(X + 8 + b);
+            const F2 bz = *reinterpret_cast<const F2*>(X + 16 + b), br = *reinterpret_cast<const F2*>(X + 24 + b);
+            const F2 t = reach2(sub2(bx, bc(qx)), sub2(by, bc(qy)), sub2(bz, bc(qz)), br, qr);
+            on(0, b, lo(t));
+            on(0, b + 1, hi(t));
+        }
+    } else {
+#pragma unroll 2
+        for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
+            const F2 bx = bc(X[b]), by = bc(X[8 + b]), bz = bc(X[16 + b]);
+            const float br = X[24 + b];
+#pragma unroll
+            for (int j = 0; j < QSet<NS>::NP; ++j) {
+                const F2 t = reach2(sub2(q.x[j], bx), sub2(q.y[j], by), sub2(q.z[j], bz), q.r[j], br);
+                on(2 * j, b, lo(t));
+                if (2 * j + 1 < NS) on(2 * j + 1, b, hi(t));
+            }
+        }
+    }
+}
+
+template <bool GRAD, int NS, class OnWrench>
+__device__ __forceinline__ float pairs_vs_instance(const QSet<NS>& q, const float* X, const float4 bound, float lam,
+                                                   float (&g)[NS][3], OnWrench&& on_wrench, float smooth) {
+    // broad phase: skip the instance unless some query sphere of the warp reaches its bounding sphere
+    if (!__any_sync(FULL, qset_near(q, bound.x, bound.y, bound.z, bound.w))) return 0.f;
+    // which pairs are active: bit b of act[k] = sign of d^2 - R^2 of pair (k, b) (a -0 or a NaN with the sign bit
+    // set only sends an inactive pair to the exact test below, which rejects it again)
     uint32_t act[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) act[k] = 0u;
-#pragma unroll
-    for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
-        const float4 B = Bs[b];
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const float dx = w[k][0] - B.x, dy = w[k][1] - B.y, dz = w[k][2] - B.z;
-            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            const float R = rr[k] + B.w;
-            act[k] |= (fmaf(-R, R, d2) < 0.f ? 1u : 0u) << b;
-        }
-    }
+    instance_pair_tests(q, X, [&](int k, int b, float t) { act[k] |= (__float_as_uint(t) >> 31) << b; });
     uint32_t any = 0u;
 #pragma unroll
     for (int k = 0; k < NS; ++k) any |= act[k];
+    if (!__any_sync(FULL, any != 0u)) return 0.f;
+    // exact hinges and gradients of the active pairs
     float j = 0.f;
-    if (__any_sync(FULL, any != 0u)) {
-        // hinges and gradients of the active pairs only
-        Wrench pw;
-        pw.zero();
+    Wrench pw;
+    pw.zero();
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            uint32_t m = act[k];
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1u;
-                const float4 B = Bs[b];
-                float ux, uy, uz;
-                j += sphere_sphere<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, ux, uy, uz, smooth);
-                if (GRAD) {
-                    g[k][0] -= ux; g[k][1] -= uy; g[k][2] -= uz;
-                    pw.add_point(B.x, B.y, B.z, ux, uy, uz);
-                }
+    for (int k = 0; k < NS; ++k) {
+        uint32_t m = act[k];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1u;
+            const float4 B = make_float4(X[b], X[8 + b], X[16 + b], X[24 + b]);
+            float ux, uy, uz;
+            j += sphere_sphere<GRAD>(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B, lam, ux, uy, uz, smooth);
+            if (GRAD) {
+                g[k][0] -= ux; g[k][1] -= uy; g[k][2] -= uz;
+                pw.add_point(B.x, B.y, B.z, ux, uy, uz);
             }
         }
-        on_wrench(pw);   // warp-uniform: reduce / store the partner's wrench
     }
+    on_wrench(pw);   // warp-uniform: reduce / store the partner's wrench
     return j;
 }
 
-// NS query spheres per lane vs one OBB: the exact reject test of every sphere first (straight-line code,
-// independent chains), hinge + gradient only for spheres that reach the box, and nothing at all unless some
-// sphere of the warp does.  Small boxes are first gated by their bounding sphere.  Skipped spheres would add
-// exact zeros: results are unchanged.
+// NS query spheres per lane vs one OBB: the exact reject test of every sphere first (packed straight-line code),
+// hinge + gradient only for spheres that reach the box, and nothing at all unless some sphere of the warp does.
+// Small boxes are first gated by their bounding sphere.  The reject test is sphere_obb's own, s >= r^2 with
+// s = ||max(|R^T (w - c)| - h, 0)||^2, evaluated as 4 s = ||a + |a|||^2 >= (2r)^2 (a = |p| - h; scaling by 4 is
+// exact) on the FMA pipe; skipped spheres would add exact zeros: results are unchanged.
 template <bool GRAD, int NS>
-__device__ __forceinline__ float spheres_vs_obb(const float (&w)[NS][3], const float (&rr)[NS], const KObb& B,
-                                                float lam, float (&g)[NS][3], float smooth) {
+__device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B, float lam, float (&g)[NS][3],
+                                                float smooth) {
     if (B.rad < kBroadMaxRad) {      // broad phase: bounding sphere of the box (not for boxes larger than the
-        float mb = 1.f;              // arm's reach, e.g. the table, where it would rarely reject)
-#pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const float dx = w[k][0] - B.c[0], dy = w[k][1] - B.c[1], dz = w[k][2] - B.c[2];
-            const float R = rr[k] + B.rad;
-            mb = fminf(mb, fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
-        }
-        if (!__any_sync(FULL, mb < 0.f)) return 0.f;
+                                     // arm's reach, e.g. the table, where it would rarely reject)
+        if (!__any_sync(FULL, qset_near(q, B.c[0], B.c[1], B.c[2], B.rad))) return 0.f;
     }
     bool hit[NS], any = false;
+    if (TAMP_PACK_OBB == 0) {         // scalar: obb_within per sphere
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        hit[k] = obb_within(w[k][0], w[k][1], w[k][2], rr[k], B);
-        any = any || hit[k];
+        for (int k = 0; k < NS; ++k) {
+            hit[k] = obb_within(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B);
+            any = any || hit[k];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < QSet<NS>::NP; ++j) {
+            const F2 dx = sub2(q.x[j], bc(B.c[0])), dy = sub2(q.y[j], bc(B.c[1])), dz = sub2(q.z[j], bc(B.c[2]));
+            F2 px = dx, py = dy, pz = dz;
+            if (!B.aligned) {            // p = R^T (w - c)
+                px = fma2(bc(B.R[0]), dx, fma2(bc(B.R[3]), dy, mul2(bc(B.R[6]), dz)));
+                py = fma2(bc(B.R[1]), dx, fma2(bc(B.R[4]), dy, mul2(bc(B.R[7]), dz)));
+                pz = fma2(bc(B.R[2]), dx, fma2(bc(B.R[5]), dy, mul2(bc(B.R[8]), dz)));
+            }
+            if (TAMP_PACK_OBB == 1) {   // 2 max(a, 0) = a + |a| on the FMA pipe; 4 s >= (2r)^2 (scaling by 4 exact)
+                float qq[2][3];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float ax = fabsf(h ? hi(px) : lo(px)) - B.h[0];
+                    const float ay = fabsf(h ? hi(py) : lo(py)) - B.h[1];
+                    const float az = fabsf(h ? hi(pz) : lo(pz)) - B.h[2];
+                    qq[h][0] = ax + fabsf(ax);  qq[h][1] = ay + fabsf(ay);  qq[h][2] = az + fabsf(az);
+                }
+                const F2 qx = pk(qq[0][0], qq[1][0]), qy = pk(qq[0][1], qq[1][1]), qz = pk(qq[0][2], qq[1][2]);
+                const F2 s4 = fma2(qx, qx, fma2(qy, qy, mul2(qz, qz)));
+                const F2 r2 = add2(q.r[j], q.r[j]);
+                const F2 r4 = mul2(r2, r2);
+                hit[2 * j] = !(lo(s4) >= lo(r4));
+                any = any || hit[2 * j];
+                if (2 * j + 1 < NS) {
+                    hit[2 * j + 1] = !(hi(s4) >= hi(r4));
+                    any = any || hit[2 * j + 1];
+                }
+            } else {                    // obb_within's own formula on the packed offsets
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (2 * j + h >= NS) continue;
+                    const float r = h ? hi(q.r[j]) : lo(q.r[j]);
+                    const float ax = fabsf(h ? hi(px) : lo(px)) - B.h[0];
+                    const float ay = fabsf(h ? hi(py) : lo(py)) - B.h[1];
+                    const float az = fabsf(h ? hi(pz) : lo(pz)) - B.h[2];
+                    const float qx = fmaxf(ax, 0.f), qy = fmaxf(ay, 0.f), qz = fmaxf(az, 0.f);
+                    const bool out = fmaxf(ax, fmaxf(ay, az)) > 0.f && fmaf(qx, qx, fmaf(qy, qy, qz * qz)) >= r * r;
+                    hit[2 * j + h] = !out;
+                    any = any || !out;
+                }
+            }
+        }
     }
     float j = 0.f;
     if (__any_sync(FULL, any)) {
 #pragma unroll
         for (int k = 0; k < NS; ++k)
-            if (hit[k]) j += sphere_obb<GRAD>(w[k][0], w[k][1], w[k][2], rr[k], B, lam, g[k][0], g[k][1], g[k][2], smooth);
+            if (hit[k]) j += sphere_obb<GRAD>(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B, lam, g[k][0], g[k][1], g[k][2], smooth);
     }
     return j;
 }
@@ -446,6 +623,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     __shared__ int s_counts[TAMP_MAX_TERMS + 2];
     __shared__ float4 s_F[kGroup][3];                              // fixed transform of each joint (7: tool)
     __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];   // spheres of each link frame
+    __shared__ __align__(16) float s_rsoa[kGroup][4 * TAMP_MAX_SPHERES_PER_LINK];   // the same, SoA x[4] y[4] z[4] r[4]
     __shared__ uint32_t s_selfmask[kGroup * TAMP_MAX_SPHERES_PER_LINK];
 
     const int gl = threadIdx.x & (GS - 1);          // lane within the particle group
@@ -470,13 +648,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         return (I.xoff >= 0 ? minst : cinst) + kInstFloats * I.slot;
     };
     auto ipose = [&](int i) -> float* { return inst(i); };
-    auto isph = [&](int i) -> float4* { return reinterpret_cast<float4*>(inst(i) + 16); };
     auto iwr = [&](int i) -> float* { return inst(i) + 48; };
     const int D = P.D;
     auto phase_sync = [&]() {
         if (BSYNC > 0) __syncthreads(); else __syncwarp();
     };
-    auto ibound = [&](int i) { return *reinterpret_cast<const float4*>(inst(i) + 12); };
 
     for (int i = threadIdx.x; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += blockDim.x) {
         const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
@@ -491,6 +667,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     if (threadIdx.x < kGroup * TAMP_MAX_SPHERES_PER_LINK) {
         const int l = threadIdx.x / TAMP_MAX_SPHERES_PER_LINK, k = threadIdx.x % TAMP_MAX_SPHERES_PER_LINK;
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s_rsoa[l][TAMP_MAX_SPHERES_PER_LINK * c + k] = P.rsph[l][k][c];
         s_selfmask[threadIdx.x] = P.self_mask[threadIdx.x];
     }
     float4* rsw = reinterpret_cast<float4*>(S + A.off_rsw) + (HP > 1 ? half : 0) * (kGroup * TAMP_MAX_SPHERES_PER_LINK + kGroup);
@@ -531,11 +709,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 ip[13] = fmaf(sy, ob[0], fmaf(cy, ob[1], py));
                 ip[14] = pz + ob[2];
                 ip[15] = ob[3];
-            } else {
+            } else {                                  // spheres SoA: x[8] y[8] z[8] r[8]
                 const float* c = P.osph[I.obj][k];
-                reinterpret_cast<float4*>(ip + 16)[k] = k < P.osph_n[I.obj]
-                    ? make_float4(fmaf(cy, c[0], fmaf(-sy, c[1], px)), fmaf(sy, c[0], fmaf(cy, c[1], py)), pz + c[2], c[3])
-                    : make_float4(kFar, kFar, kFar, 0.f);
+                const bool in = k < P.osph_n[I.obj];
+                ip[16 + k] = in ? fmaf(cy, c[0], fmaf(-sy, c[1], px)) : kFar;
+                ip[24 + k] = in ? fmaf(sy, c[0], fmaf(cy, c[1], py)) : kFar;
+                ip[32 + k] = in ? pz + c[2] : kFar;
+                ip[40 + k] = in ? c[3] : 0.f;
             }
         }
     }
@@ -583,9 +763,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             }
             for (int k = gl; k < TAMP_MAX_OBJ_SPHERES; k += GS) {
                 const float4 c = s_osph[I.obj][k];
-                reinterpret_cast<float4*>(ip + 16)[k] = k < P.osph_n[I.obj]
-                    ? make_float4(fmaf(cy, c.x, fmaf(-sy, c.y, px)), fmaf(sy, c.x, fmaf(cy, c.y, py)), pz + c.z, c.w)
-                    : make_float4(kFar, kFar, kFar, 0.f);
+                const bool in = k < P.osph_n[I.obj];     // spheres SoA: x[8] y[8] z[8] r[8]
+                ip[16 + k] = in ? fmaf(cy, c.x, fmaf(-sy, c.y, px)) : kFar;
+                ip[24 + k] = in ? fmaf(sy, c.x, fmaf(cy, c.y, py)) : kFar;
+                ip[32 + k] = in ? pz + c.z : kFar;
+                ip[40 + k] = in ? c.w : 0.f;
             }
             if (G)
                 for (int c = gl; c < 6; c += GS) ip[48 + c] = 0.f;
@@ -636,30 +818,56 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 T[LPL - 1] = Sc;
             }
             const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
-            // my links' spheres in the world
-            float w[NS][3], gw[NS][3], rr[NS];
+            // my links' spheres in the world, transformed in packed pairs (w = T c, the xform order)
+            QSet<NS> rs;
+            float gw[NS][3];
 #pragma unroll
-            for (int u = 0; u < LPL; ++u)
+            for (int u = 0; u < LPL; ++u) {
+                const float* cs = s_rsoa[ll * LPL + u];          // x[4] y[4] z[4] r[4] in the link frame
 #pragma unroll
-                for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
-                    const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
-                    const float4 c4 = s_rsph[ll * LPL + u][k];
-                    xform(T[u], c4.x, c4.y, c4.z, w[s][0], w[s][1], w[s][2]);
-                    if (k >= nsph[u]) w[s][0] = w[s][1] = w[s][2] = kFar;      // absent sphere slot
-                    rr[s] = c4.w + P.eta;
-                    gw[s][0] = gw[s][1] = gw[s][2] = 0.f;
+                for (int kp = 0; kp < TAMP_MAX_SPHERES_PER_LINK / 2; ++kp) {
+                    const int j = u * (TAMP_MAX_SPHERES_PER_LINK / 2) + kp;
+                    if (!TAMP_PACK_XFORM) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float wx, wy, wz;
+                            xform(T[u], cs[2 * kp + h], cs[4 + 2 * kp + h], cs[8 + 2 * kp + h], wx, wy, wz);
+                            rs.set(2 * j + h, wx, wy, wz, cs[12 + 2 * kp + h] + P.eta);
+                        }
+                        continue;
+                    }
+                    const F2 cx = *reinterpret_cast<const F2*>(cs + 2 * kp);
+                    const F2 cy = *reinterpret_cast<const F2*>(cs + 4 + 2 * kp);
+                    const F2 cz = *reinterpret_cast<const F2*>(cs + 8 + 2 * kp);
+                    const F2 cr = *reinterpret_cast<const F2*>(cs + 12 + 2 * kp);
+                    rs.x[j] = fma2(bc(T[u].r[0]), cx, fma2(bc(T[u].r[1]), cy, fma2(bc(T[u].r[2]), cz, bc(T[u].t[0]))));
+                    rs.y[j] = fma2(bc(T[u].r[3]), cx, fma2(bc(T[u].r[4]), cy, fma2(bc(T[u].r[5]), cz, bc(T[u].t[1]))));
+                    rs.z[j] = fma2(bc(T[u].r[6]), cx, fma2(bc(T[u].r[7]), cy, fma2(bc(T[u].r[8]), cz, bc(T[u].t[2]))));
+                    rs.r[j] = add2(cr, bc(P.eta));
                 }
+                if (nsph[u] < TAMP_MAX_SPHERES_PER_LINK) {         // absent sphere slots: far away
+#pragma unroll
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
+                        const int s2 = u * TAMP_MAX_SPHERES_PER_LINK + k;
+                        if (k >= nsph[u]) rs.set(s2, kFar, kFar, kFar, rs.sr(s2));
+                    }
+                }
+            }
+            rs.finish();
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2) gw[s2][0] = gw[s2][1] = gw[s2][2] = 0.f;
             float jcf = 0.f;
             if (K.term_cf >= 0) {
                 // robot spheres vs OBBs (constant cache)
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS>(w, rr, P.obb[b], lam_cf, gw, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS>(rs, P.obb[b], lam_cf, gw, smooth);
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    jcf += pairs_vs_instance<G, NS>(w, rr, isph(ii), ibound(ii), lam_cf, gw,
-                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr(ii), ll, half, real); },
-                        smooth);
+                    float* ip = inst(ii);
+                    const bool mov = P.inst[ii].xoff >= 0;
+                    jcf += pairs_vs_instance<G, NS>(rs, ip + 16, *reinterpret_cast<const float4*>(ip + 12), lam_cf, gw,
+                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, mov, ip + 48, ll, half, real); }, smooth);
                 }
             }
             // robot self-collision: every lane tests its own spheres against their pair
@@ -668,7 +876,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             if (K.term_self >= 0) {
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
-                    rsw[ll * NS + s] = make_float4(w[s][0], w[s][1], w[s][2], rr[s] - P.eta);
+                    rsw[ll * NS + s] = make_float4(rs.sx(s), rs.sy(s), rs.sz(s), rs.sr(s) - P.eta);
 #pragma unroll
                 for (int u = 0; u < LPL; ++u) {
                     const float* lb = P.lbound[ll * LPL + u];
@@ -700,8 +908,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                             const int t = __ffs(m) - 1;
                             m &= m - 1u;
                             float ux, uy, uz;
-                            const float pen = sphere_sphere<G>(w[s][0], w[s][1], w[s][2], rr[s], rsw[t], lam_self, ux, uy, uz,
-                                                                  smooth);
+                            const float pen = sphere_sphere<G>(rs.sx(s), rs.sy(s), rs.sz(s), rs.sr(s), rsw[t], lam_self, ux, uy,
+                                                                  uz, smooth);
                             if (sid < t) js += pen;
                             if (G) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
                         }
@@ -718,7 +926,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
 #pragma unroll
                     for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
                         const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
-                        Wl[u].add_point(w[s][0], w[s][1], w[s][2], gw[s][0], gw[s][1], gw[s][2]);
+                        Wl[u].add_point(rs.sx(s), rs.sy(s), rs.sz(s), gw[s][0], gw[s][1], gw[s][2]);
                     }
                 }
             }
@@ -730,29 +938,33 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 load_m34(Gi, gTi + 12 * K.held_grasp);
                 Tobj = compose(Tee, Gi);
                 const int ho = K.held_obj;
-                float h[NH][3], gh[NH][3], hr[NH];
+                QSet<NH> hq;
+                float gh[NH][3];
 #pragma unroll
                 for (int v = 0; v < NH; ++v) {
                     const int k = ll + LPF * v;
                     const float4 c = s_osph[ho][k];
-                    xform(Tobj, c.x, c.y, c.z, h[v][0], h[v][1], h[v][2]);
-                    if (k >= P.osph_n[ho]) h[v][0] = h[v][1] = h[v][2] = kFar;
-                    hr[v] = c.w + P.eta;
+                    float hx, hy, hz;
+                    xform(Tobj, c.x, c.y, c.z, hx, hy, hz);
+                    if (k >= P.osph_n[ho]) hx = hy = hz = kFar;
+                    hq.set(v, hx, hy, hz, c.w + P.eta);
                     gh[v][0] = gh[v][1] = gh[v][2] = 0.f;
                 }
+                hq.finish();
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH>(h, hr, P.obb[b], lam_cf, gh, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH>(hq, P.obb[b], lam_cf, gh, smooth);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
-                    jcf += pairs_vs_instance<G, NH>(h, hr, isph(ii), ibound(ii), lam_cf, gh,
-                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, P.inst[ii].xoff >= 0, iwr(ii), ll, half, real); },
-                        smooth);
+                    float* ip = inst(ii);
+                    const bool mov = P.inst[ii].xoff >= 0;
+                    jcf += pairs_vs_instance<G, NH>(hq, ip + 16, *reinterpret_cast<const float4*>(ip + 12), lam_cf, gh,
+                        [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, mov, ip + 48, ll, half, real); }, smooth);
                 }
                 if (G) {   // held-object wrench acts on the tool link (last lane of the segment)
                     Wrench hw;
                     hw.zero();
 #pragma unroll
-                    for (int v = 0; v < NH; ++v) hw.add_point(h[v][0], h[v][1], h[v][2], gh[v][0], gh[v][1], gh[v][2]);
+                    for (int v = 0; v < NH; ++v) hw.add_point(hq.sx(v), hq.sy(v), hq.sz(v), gh[v][0], gh[v][1], gh[v][2]);
                     hw.template group_sum<LPF>();
                     if (ll == LPF - 1) {
 #pragma unroll
@@ -914,14 +1126,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
             }
             const int no = P.osph_n[I.obj];
+            float* const oip = minst + kInstFloats * I.slot;      // the placed object's instance (movable)
             float wq[NSO][3], rq[NSO], gq[NSO][3];
 #pragma unroll
             for (int u = 0; u < NSO; ++u) {
                 const int k = gl + GS * u;
-                const float4 c = k < TAMP_MAX_OBJ_SPHERES ? isph(ii)[k]   // padded slots: far
-                                                          : make_float4(kFar, kFar, kFar, 0.f);
-                wq[u][0] = c.x; wq[u][1] = c.y; wq[u][2] = c.z;
-                rq[u] = c.w;
+                const bool in = k < TAMP_MAX_OBJ_SPHERES;           // padded slots: far
+                wq[u][0] = in ? oip[16 + k] : kFar;
+                wq[u][1] = in ? oip[24 + k] : kFar;
+                wq[u][2] = in ? oip[32 + k] : kFar;
+                rq[u] = in ? oip[40 + k] : 0.f;
                 gq[u][0] = gq[u][1] = gq[u][2] = 0.f;
             }
             // containment: sum over spheres of dist_from_bounds(xy in surface frame, lo + r, hi - r)
@@ -991,17 +1205,19 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             // CFreePlace: placed-object spheres vs OBBs (support excluded) and other objects
             if (Q.term_cp >= 0) {
                 const float lam_cp = P.term_lam[Q.term_cp];
-                float rqe[NSO];
+                QSet<NSO> qe;
 #pragma unroll
-                for (int u = 0; u < NSO; ++u) rqe[u] = rq[u] + P.eta;
+                for (int u = 0; u < NSO; ++u) qe.set(u, wq[u][0], wq[u][1], wq[u][2], rq[u] + P.eta);
+                qe.finish();
                 float jcp = 0.f;
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO>(wq, rqe, P.obb[b], lam_cp, gq, smooth);
+                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO>(qe, P.obb[b], lam_cp, gq, smooth);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
-                    jcp += pairs_vs_instance<G, NSO>(wq, rqe, isph(jj), ibound(jj), lam_cp, gq,
-                        [&](Wrench& pw) { flush_partner<G, GS>(pw, P.inst[jj].xoff >= 0, iwr(jj), gl); },
-                        smooth);
+                    float* jp = inst(jj);
+                    const bool mov = P.inst[jj].xoff >= 0;
+                    jcp += pairs_vs_instance<G, NSO>(qe, jp + 16, *reinterpret_cast<const float4*>(jp + 12), lam_cp, gq,
+                        [&](Wrench& pw) { flush_partner<G, GS>(pw, mov, jp + 48, gl); }, smooth);
                 }
                 finish_term<M>(P, A, sink, Q.term_cp, term_sum<M, GS>(jcp), gl, active, p, s_counts);
             }
@@ -1010,7 +1226,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 for (int u = 0; u < NSO; ++u)
                     if (gl + GS * u < no) own.add_point(wq[u][0], wq[u][1], wq[u][2], gq[u][0], gq[u][1], gq[u][2]);
                 own.template group_sum<GS>();
-                if (gl == 0) add_wrench(iwr(ii), own);
+                if (gl == 0) add_wrench(oip + 48, own);
             }
         }
 

@@ -319,10 +319,32 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
     for (int b = 0; b < d.n_obb; ++b) {
         const tamp_obb_desc& o = d.obb[b];
         for (int k = 0; k < 3; ++k) REQUIRE(o.half[k] > 0.f, TAMP_E_INVALID, "OBB half extents must be > 0 (S:32)");
-        const double c = cos((double)o.yaw), s = sin((double)o.yaw);
         KObb& B = P.obb[b];
-        const double Rm[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
-        for (int k = 0; k < 9; ++k) B.R[k] = (float)Rm[k];
+        bool given = false;
+        for (int k = 0; k < 9; ++k) given |= o.rot[k] != 0.f;
+        double Rm[9];
+        if (given) {            // full orientation: orthonormal, det +1
+            for (int k = 0; k < 9; ++k) Rm[k] = o.rot[k];
+            double err = 0.0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    double d = 0.0;
+                    for (int k = 0; k < 3; ++k) d += Rm[3 * k + i] * Rm[3 * k + j];
+                    err = std::max(err, std::fabs(d - (i == j ? 1.0 : 0.0)));
+                }
+            const double det = Rm[0] * (Rm[4] * Rm[8] - Rm[5] * Rm[7]) - Rm[1] * (Rm[3] * Rm[8] - Rm[5] * Rm[6]) +
+                               Rm[2] * (Rm[3] * Rm[7] - Rm[4] * Rm[6]);
+            REQUIRE(err < 1e-4 && std::fabs(det - 1.0) < 1e-4, TAMP_E_INVALID, "OBB rot must be a rotation matrix");
+        } else {                // Rz(yaw)
+            const double c = cos((double)o.yaw), s = sin((double)o.yaw);
+            const double Rz[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
+            for (int k = 0; k < 9; ++k) Rm[k] = Rz[k];
+        }
+        B.aligned = 1;
+        for (int k = 0; k < 9; ++k) {
+            B.R[k] = (float)Rm[k];
+            B.aligned &= B.R[k] == ((k % 4 == 0) ? 1.f : 0.f);
+        }
         for (int k = 0; k < 3; ++k) { B.c[k] = o.center[k]; B.h[k] = o.half[k]; }
         B.rad = (float)(std::sqrt((double)o.half[0] * o.half[0] + (double)o.half[1] * o.half[1] +
                                   (double)o.half[2] * o.half[2]) * (1.0 + 1e-6));

@@ -60,7 +60,13 @@ struct KTraj {
 };
 
 struct KSurface { float frame[4]; float lo[2], hi[2]; float cy, sy; };   // cy, sy: cos / sin of the frame yaw
-struct KObb { float R[9]; float c[3]; float h[3]; float rad; };   // R = Rz(yaw) (the kernels rely on it); rad = |h|
+struct KObb {                          // oriented box: world pose R (row-major), centre c, half extents h
+    float R[9];
+    float c[3];
+    float h[3];
+    float rad;                         // |h|: bounding-sphere radius
+    int32_t aligned;                   // R is exactly the identity (axis-aligned fast path)
+};
 
 struct KProgram {
     int32_t D, n_terms, n_fk, n_inst, n_place, n_traj, n_goal, n_grasp, n_obb;

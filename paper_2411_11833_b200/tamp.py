@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtamp.so")
 
 # ---- limits / enums (include/tamp.h) ----
-ABI_VERSION = 3
+ABI_VERSION = 4
 NJ = 7
 MAX_ROBOT_SPHERES = 32
 MAX_OBB = 16
@@ -46,7 +46,7 @@ class RobotDesc(ctypes.Structure):
 
 
 class ObbDesc(ctypes.Structure):
-    _fields_ = [("center", F * 3), ("yaw", F), ("half", F * 3)]
+    _fields_ = [("center", F * 3), ("yaw", F), ("half", F * 3), ("rot", F * 9)]
 
 
 class ObjectDesc(ctypes.Structure):
@@ -202,6 +202,10 @@ def build_desc(spec, grad_scale: float = 0.0, lanes_per_particle: int = 0, block
             d.obb[b].center[k] = float(o.center[k])
             d.obb[b].half[k] = float(o.half[k])
         d.obb[b].yaw = float(o.yaw)
+        R = getattr(o, "R", None)
+        if R is not None:                         # full orientation (box-to-world rotation, row-major)
+            for k, v in enumerate(np.asarray(R, dtype=np.float32).reshape(9)):
+                d.obb[b].rot[k] = float(v)
     d.n_objects = len(spec.objects)
     for i, o in enumerate(spec.objects):
         d.object[i].n_spheres = len(o.spheres)

@@ -60,3 +60,158 @@ def satisfying_pickplace(spec, csp, rng, psi):
     for j in range(K):
         x[off + 7 * j:off + 7 * j + 7] = q + (j + 1) / (K + 1) * (q2 - q)
     return x, Tg
+
+
+# ---------------------------------------------------------------------------------------------------
+# Tetris (configs 3 / 4): an exactly tiled satisfying particle ("feasible by construction")
+# ---------------------------------------------------------------------------------------------------
+def _rot_cells(cells, k):
+    c = np.asarray(cells, float)
+    R = np.array([[0.0, -1.0], [1.0, 0.0]])
+    for _ in range(k):
+        c = c @ R.T
+    return c
+
+
+def tile_grid(W, H, shapes):
+    """Backtracking tiling of a W x H cell grid with the given tetrominoes (rotations only, no reflection).
+    Returns [(k, ox, oy)] per piece: rotation by k quarter turns, then translation so the cells start at (ox, oy)."""
+    from workloads.scenes import TETROMINOES
+    grid = -np.ones((W, H), int)
+    sol = []
+
+    def rec(i):
+        if i == len(shapes):
+            return True
+        for k in range(4):
+            r = _rot_cells(TETROMINOES[shapes[i]], k)
+            r = np.rint(r - r.min(axis=0)).astype(int)
+            for ox in range(W):
+                for oy in range(H):
+                    c = r + [ox, oy]
+                    if (c[:, 0] >= W).any() or (c[:, 1] >= H).any() or (grid[c[:, 0], c[:, 1]] >= 0).any():
+                        continue
+                    grid[c[:, 0], c[:, 1]] = i
+                    sol.append((k, ox, oy))
+                    if rec(i + 1):
+                        return True
+                    grid[c[:, 0], c[:, 1]] = -1
+                    sol.pop()
+        return False
+
+    assert rec(0), "no tiling"
+    return sol
+
+
+def tetris_tiled_placements(spec, W, H, shapes):
+    """Placements (x, y, z, yaw) of the pieces tiling the W x H grid centred in the goal region.  A piece's object
+    frame has its cells centred on their mean (workloads.tetromino), so yaw k pi/2 maps them onto R^k c - R^k mean,
+    and the centroid lands at R^k mean - min(R^k c) + offset (cell units)."""
+    from workloads.scenes import TETROMINOES, CELL
+    sf = [s for s in spec.surfaces if s.name == "tetris_region"][0]
+    cx, cy = sf.frame[0], sf.frame[1]
+    out = []
+    for shape, (k, ox, oy) in zip(shapes, tile_grid(W, H, shapes)):
+        c = np.asarray(TETROMINOES[shape], float)
+        rc = _rot_cells(c, k)
+        t = _rot_cells(c.mean(axis=0)[None], k)[0] - rc.min(axis=0) + [ox, oy]
+        out.append(np.array([cx + (t[0] - (W - 1) / 2) * CELL, cy + (t[1] - (H - 1) / 2) * CELL, sf.frame[2],
+                             k * math.pi / 2]))
+    return out
+
+
+def _ik(spec, T, rng, tries=24, iters=300):
+    """A conf reaching T exactly (errors < 1e-7), from random starts: the oracle's DLS IK (pinned)."""
+    rob = spec.robot
+    for _ in range(tries):
+        q0 = rng.uniform(rob.joint_lo, rob.joint_hi)[None]
+        q = O.ik_dls(rob, q0, T[None], iters, 0.05)
+        ep, th = O.ik_errors(rob, q, T[None])
+        if ep[0] < 1e-7 and th[0] < 1e-7:
+            yield q[0]
+
+
+def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2):
+    """Hand-constructed satisfying particle of a Tetris skeleton: pieces on an exact tiling of the grid (z on the
+    region, yaws multiples of pi/2), top-down grasps over each piece's centroid with the gripper turned so its
+    fingers lie along the piece's own cells (searched over 24 yaws), pick / place confs by exact IK
+    (T(g) := placement-consistent, FK(q) = T(p) T(g)), each chosen among IK solutions so that its own CF terms are
+    exactly 0; knots (config 4) at confs reaching the same TCP poses lifted by `lift`.  Every pick / place and knot
+    is checked with the oracle (CF, JL; Kin by construction); returns (x [D], grasps [G, 3, 4])."""
+    V = spec.variables
+    vid = {v.name: i for i, v in enumerate(V)}
+    x = np.zeros(csp.D)
+    G = np.zeros((len(csp.grasp_vars), 3, 4))
+    G[:, 0, 0] = G[:, 1, 1] = G[:, 2, 2] = 1.0
+    places = tetris_tiled_placements(spec, W, H, shapes)
+    names = [o.name for o in spec.objects]
+    terms_of = {}
+    for ti, t in enumerate(csp.terms):
+        terms_of.setdefault(t.action, []).append(ti)
+    eps = np.array([spec.eps[t.kind] for t in csp.terms])
+
+    def eval_terms(tids):
+        with torch.no_grad():
+            _, Jc, _ = O.evaluate(spec, csp, torch.as_tensor(x[None]), torch.as_tensor(G[None]))
+        return Jc.numpy()[0, tids]
+
+    def set_conf(vi, q):
+        x[csp.offsets[vi]:csp.offsets[vi] + 7] = q
+
+    def up(T):
+        T = T.copy()
+        T[2, 3] += lift
+        return T
+
+    for i, nm in enumerate(names):
+        # Listing 1 order per piece: MoveFree, Pick, MoveHold, Place
+        ai = 4 * i
+        a_pick, a_place = spec.actions[ai + 1], spec.actions[ai + 3]
+        vp = a_place.placement
+        x[csp.offsets[vp]:csp.offsets[vp] + 4] = places[i]
+        gslot = csp.grasp_vars.index(a_pick.grasp)
+        o = spec.objects[i]
+        done = False
+        for gamma in rng.permutation(np.arange(24) * math.pi / 12):
+            Tg = O.top_down_grasp(torch.tensor([0.0]), torch.tensor([0.0]), torch.tensor([o.grasp_z]),
+                                  torch.tensor([gamma]))[0].numpy()
+            G[gslot] = Tg[:3]
+            T_pick = (O.pose_xyzyaw(torch.tensor(V[a_pick.placement].value)).numpy() @ Tg)
+            T_place = (O.pose_xyzyaw(torch.tensor(places[i])).numpy() @ Tg)
+            ok = True
+            for a_idx, T in ((ai + 1, T_pick), (ai + 3, T_place)):
+                a = spec.actions[a_idx]
+                good = False
+                for q in _ik(spec, T, rng):
+                    set_conf(a.q1, q)
+                    tids = [t for t in terms_of[a_idx] if csp.terms[t].kind in ("JL", "CF")]
+                    if np.all(eval_terms(tids) == 0.0):
+                        good = True
+                        break
+                if not good:
+                    ok = False
+                    break
+            if ok:
+                done = True
+                break
+        assert done, f"no collision-free grasp / IK for {nm}"
+        # knots: lifted TCP poses (config 4), checked like the confs
+        for a_idx in (ai, ai + 2):
+            a = spec.actions[a_idx]
+            if a.traj < 0 or V[a.traj].n_knots == 0:
+                continue
+            K = V[a.traj].n_knots
+            if a_idx == ai:      # MoveFree into the pick: lifted above the pick
+                poses = [up(T_pick)] * K
+            else:                # MoveHold: lifted above the pick, then above the place
+                poses = [up(T_pick)] + [up(T_place)] * (K - 1)
+            for j, T in enumerate(poses):
+                good = False
+                for q in _ik(spec, T, rng):
+                    x[csp.offsets[a.traj] + 7 * j:csp.offsets[a.traj] + 7 * j + 7] = q
+                    tids = [t for t in terms_of[a_idx] if csp.terms[t].conf == ("knot", a.traj, j)]
+                    if np.all(eval_terms(tids) == 0.0):
+                        good = True
+                        break
+                assert good, f"no collision-free knot {j} for action {a_idx}"
+    return x, G

@@ -5,7 +5,7 @@ OUT=gpurun_out/sweep_$TAG.txt
 : > $OUT
 for item in $LIST; do
   IFS=: read L T S <<< "$item"
-  line=$(timeout 300 python bench.py --config $CFG --steps 5 --warmup 3 --no-e2e --no-ttfs --no-cpu-baseline --no-extra \
+  line=$(timeout 300 python bench.py ${LIB:+--lib $LIB} --config $CFG --steps 5 --warmup 3 --no-e2e --no-ttfs --no-cpu-baseline --no-extra \
          --lanes $L --block-threads $T --block-sync $S "$@" 2>/dev/null | grep '^{')
   python - "$item" "$line" >> $OUT <<'PY'
 import json, sys

@@ -48,11 +48,13 @@ class Robot:
 
 @dataclasses.dataclass
 class OBB:
-    """Static oriented box: world pose (center xyz, yaw about z) and half extents."""
+    """Static oriented box: world pose and half extents.  Orientation: R (3x3 box-to-world rotation)
+    if given, else Rz(yaw) about the world z axis."""
     center: np.ndarray        # (3,)
     yaw: float
     half: np.ndarray          # (3,)
     name: str = ""
+    R: Optional[np.ndarray] = None   # (3, 3) full orientation; None = Rz(yaw)
 
 
 @dataclasses.dataclass
