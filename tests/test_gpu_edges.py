@@ -106,3 +106,52 @@ def test_residual_exactly_at_tolerance_is_satisfying():
         assert (cls.cpu().numpy()[0] == 0) == sat and (cls_o[0] == 0) == sat
         assert counts[8] == (1 if sat else 0) and counts_o[8] == counts[8]
         np.testing.assert_array_equal(counts, counts_o)
+
+
+def _tilted_scene(cfg, n):
+    """Config `cfg` with two fully rotated boxes where the arm and the objects move (P:489 oriented boxes): a slab
+    tilted 35 degrees about x over the work area and a box turned about an oblique axis beside it."""
+    from scipy.spatial.transform import Rotation
+    from workloads.scenes import OBB
+    from workloads.scenes import _f32
+    spec = make_config(cfg, n=n)
+    R1 = Rotation.from_euler("x", 35, degrees=True).as_matrix()
+    R2 = Rotation.from_rotvec(0.8 * np.array([0.3, -0.5, 0.81]) / np.linalg.norm([0.3, -0.5, 0.81])).as_matrix()
+    spec.obbs = spec.obbs + [_f32(OBB(np.array([0.45, 0.05, 0.30]), 0.0, np.array([0.12, 0.15, 0.02]), "slab", R1)),
+                             _f32(OBB(np.array([0.35, -0.25, 0.15]), 0.0, np.array([0.05, 0.08, 0.10]), "tilt", R2))]
+    return spec
+
+
+@pytest.mark.parametrize("cfg,lanes", [(2, 8), (2, 4), (2, 16), (1, 1), (4, 16), (3, 8)])
+def test_tilted_boxes_cost_gradient_and_step(cfg, lanes):
+    """Full-orientation OBBs through the C ABI (tamp_obb_desc.rot): per-term costs, gradients and one Adam step
+    against the oracle on every mapping (serial included)."""
+    from parity_utils import STEP_RTOL, kink_mask
+    n = 97 if cfg != 4 else 40
+    spec = _tilted_scene(cfg, n)
+    csp = O.build_csp(spec)
+    x, g = O.initialize_particles(spec, csp, 70 + cfg, np.arange(n))
+    x32, g32 = x.astype(np.float32), g.astype(np.float32)
+    ctx = TampContext(spec, n, n_global=1000, lanes_per_particle=lanes)
+    ctx.set_state(torch.from_numpy(x32).cuda(), grasp=to_ctx_grasp(g32).cuda())
+    J, soft, Jc, grad = (t.cpu().numpy() for t in ctx.eval())
+    Jo, Jco, softo, grado = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+    # the tilted boxes are hit (otherwise this tests nothing)
+    cf = [i for i, t in enumerate(csp.terms) if t.kind in ("CF", "CP")]
+    spec0 = make_config(cfg, n=n)
+    _, Jc0, _ = O.evaluate(spec0, O.build_csp(spec0), torch.as_tensor(x32.astype(np.float64)),
+                           torch.as_tensor(g32.astype(np.float64)))
+    assert (Jco[:, cf] > Jc0.detach().numpy()[:, cf] + 1e-6).any(axis=1).mean() > 0.1
+    np.testing.assert_allclose(Jc, Jco, rtol=COST_RTOL, atol=COST_ATOL)
+    np.testing.assert_allclose(J, Jo, rtol=COST_RTOL, atol=COST_ATOL)
+    ok = grad_ok(grad, grado)
+    kinks = kink_mask(spec, csp, x32.astype(np.float64), g32.astype(np.float64), grado, np.random.default_rng(0)) \
+        if not ok.all() else ~ok
+    assert np.all(ok | kinks) and kinks.mean() <= 0.1
+    ctx.optimize(1)
+    x1 = ctx.get_state()["x"].cpu().numpy()
+    so = O.new_state(x32.astype(np.float64), g32.astype(np.float64))
+    O.optimize(spec, csp, so, 1, 1.0 / 1000)
+    unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
+    close = np.abs(x1 - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
+    assert np.all(close | unstable | kinks[:, None])

@@ -122,3 +122,20 @@ def test_plan_heuristic_matches_oracle(lib):
         c = rng.integers(0, 5, size=rng.integers(1, 40))
         assert pkg.plan_heuristic(c, len(c), -1e3) == pytest.approx(O.plan_heuristic(c, -1e3), rel=1e-12)
     assert pkg.plan_heuristic([10, 5, 0, 0], 2, -1.0) == 7.5
+
+
+def test_obb_rotation_validated(lib):
+    """tamp_obb_desc.rot: all zeros -> Rz(yaw); a rotation matrix is accepted; a non-orthonormal or reflecting
+    matrix is TAMP_E_INVALID (include/tamp.h)."""
+    spec = make_config(1, n=4)
+    d = T.build_desc(spec)
+    c, s = math.cos(0.3), math.sin(0.3)
+    for k, v in enumerate([1, 0, 0, 0, c, -s, 0, s, c]):
+        d.obb[0].rot[k] = v
+    assert _query(lib, d, 10)[0] == 0
+    d.obb[0].rot[0] = 1.1
+    st, _, msg = _query(lib, d, 10)
+    assert st == 1 and "rot" in msg
+    for k, v in enumerate([-1, 0, 0, 0, 1, 0, 0, 0, 1]):       # det -1
+        d.obb[0].rot[k] = v
+    assert _query(lib, d, 10)[0] == 1

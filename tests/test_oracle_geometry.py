@@ -227,3 +227,49 @@ def test_top_down_grasp_frame():
     np.testing.assert_allclose(R[:, 2], [0, 0, -1], atol=1e-14)
     np.testing.assert_allclose(T[:3, 3], [0.01, -0.02, 0.03], atol=1e-15)
     assert math.atan2(R[1, 0], R[0, 0]) == pytest.approx(0.4, abs=1e-14)
+
+
+def _rx(a):
+    c, s = math.cos(a), math.sin(a)
+    return np.array([[1, 0, 0], [0, c, -s], [0, s, c]], float)
+
+
+def test_full_orientation_box_closed_forms():
+    """Oriented boxes with a full rotation.  (a) A box turned by Rx(pi/2) with half extents (a, b, c)
+    occupies the same points as the axis-aligned box with half extents (a, c, b): the sphere cost of any sphere is
+    the same.  (b) A unit cube turned 45 degrees about x: a sphere straight above the centre at height z sees the
+    top edge at sqrt(2)/2, so its hinge is r - (z - sqrt(2)/2).  (c) The full-rotation form with R = Rz(yaw) equals
+    the yaw form."""
+    rng = np.random.default_rng(3)
+    half = np.array([0.3, 0.1, 0.2])
+    tilted = OBB(center=np.array([0.1, 0.2, 0.3]), yaw=0.0, half=half, R=_rx(math.pi / 2))
+    flat = OBB(center=np.array([0.1, 0.2, 0.3]), yaw=0.0, half=half[[0, 2, 1]])
+    w = torch.tensor(rng.uniform(-0.6, 0.8, (1, 200, 3)))
+    r = torch.tensor(rng.uniform(0.02, 0.15, 200))
+    a = O.sphere_obb_cost(w, r, [tilted], 0.0).item()
+    b_ = O.sphere_obb_cost(w, r, [flat], 0.0).item()
+    assert a > 0.1 and a == pytest.approx(b_, rel=1e-12)
+    cube = OBB(center=np.zeros(3), yaw=0.0, half=np.full(3, 0.5), R=_rx(math.pi / 4))
+    for z, rad in ((0.8, 0.2), (1.0, 0.4), (0.75, 0.1)):
+        v = _sphere_box([0.0, 0.0, z], rad, cube)
+        assert v == pytest.approx(max(0.0, rad - (z - math.sqrt(0.5))), abs=1e-12)
+    yawed = OBB(center=np.array([0.2, -0.1, 0.0]), yaw=0.6, half=half)
+    c, s = math.cos(0.6), math.sin(0.6)
+    full = OBB(center=yawed.center, yaw=0.0, half=half, R=np.array([[c, -s, 0], [s, c, 0], [0, 0, 1.0]]))
+    assert O.sphere_obb_cost(w, r, [yawed], 0.0).item() == pytest.approx(O.sphere_obb_cost(w, r, [full], 0.0).item(),
+                                                                           rel=1e-12)
+
+
+def test_full_orientation_rigid_invariance():
+    """Sphere-box costs are invariant under a rigid motion of the spheres and a fully rotated box."""
+    rng = np.random.default_rng(7)
+    w = rng.normal(0, 0.3, (1, 30, 3))
+    r = rng.uniform(0.02, 0.1, 30)
+    R0 = Rotation.random(random_state=8).as_matrix()
+    box = OBB(center=np.array([0.05, -0.1, 0.1]), yaw=0.0, half=np.array([0.25, 0.1, 0.3]), R=R0)
+    base = O.sphere_obb_cost(torch.tensor(w), torch.tensor(r), [box], 0.0).item()
+    Q = Rotation.random(random_state=9).as_matrix()
+    t = np.array([0.3, -1.0, 0.2])
+    box2 = OBB(center=Q @ box.center + t, yaw=0.0, half=box.half, R=Q @ R0)
+    moved = O.sphere_obb_cost(torch.tensor(w @ Q.T + t), torch.tensor(r), [box2], 0.0).item()
+    assert base > 0 and moved == pytest.approx(base, rel=1e-12)

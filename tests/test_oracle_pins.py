@@ -10,7 +10,7 @@ definition for a hand-placed configuration -- not by re-calling the oracle's own
 * TrajLength (Listing 1 cost): straight-line knots sum to ||q2 - q1||, a displaced middle
   knot to the closed form;
 * the weighted goal cost lambda_goal * obj_dist (Listing 2; S:188's unit
-  equilateral triangle gives 3, so lambda_goal * 3; a square of side s gives s (4 + 2 sqrt 2));
+  equilateral triangle gives 3, so 3 lambda_goal; a square of side s gives s (4 + 2 sqrt 2));
 * the held object at a MoveHold knot at T_ee T(g)^-1 (CFreeTrajHold): a box under the lowest held
   sphere at a known depth, sphere positions composed by hand with numpy's matrix inverse;
 * robot collision spheres on their link frames: world centres at q = 0 against the frames of
@@ -188,12 +188,13 @@ def test_traj_length_straight_and_bent_knots():
 # weighted goal cost (MinimizeObjDist)
 # ---------------------------------------------------------------------------------------------------
 def test_goal_cost_weighted_obj_dist():
-    """Config 3's goal cost lambda_goal * obj_dist (L7: lambda_goal = 0.25).  Final placements of three goal
-    objects at the corners of a unit equilateral triangle: obj_dist = 3 -> soft = 0.75; four at the
-    corners of a 10 cm square (at different heights does not matter: L24 uses xyz, so keep z equal):
-    obj_dist = 0.1 (4 + 2 sqrt 2).  J = sum lambda_c J_c + soft (Eq. 2)."""
+    """Config 3's goal cost lambda_goal * obj_dist (reading L7: lambda_goal = 0.025).  Final
+    placements of four goal objects at the corners of a 10 cm square: obj_dist = 0.1 (4 + 2 sqrt 2) (four sides, two
+    diagonals; L24 uses xyz, so equal z); three on a unit equilateral triangle: obj_dist = 3, soft = 3 lambda.
+    J = sum lambda_c J_c + soft (Eq. 2)."""
     spec = make_config(3, n=1)
-    assert spec.lam_goal == 0.25
+    lam = spec.lam_goal
+    assert lam == pytest.approx(0.025, rel=1e-7)
     csp = O.build_csp(spec)
     goal_vars = list(csp.goal.values())
     assert len(goal_vars) == 4
@@ -203,9 +204,9 @@ def test_goal_cost_weighted_obj_dist():
         x[0, csp.offsets[vi]:csp.offsets[vi] + 4] = [0.4 + px, 0.2 + py, 0.0, 0.7]
     g = _identity_grasps(csp)
     J, Jc, soft = _eval(spec, csp, x, g)
-    assert soft[0] == pytest.approx(0.25 * 0.1 * (4 + 2 * math.sqrt(2)), rel=1e-12)
-    lam = np.array([spec.lam[t.kind] for t in csp.terms])
-    assert J[0] == pytest.approx((lam * Jc[0]).sum() + soft[0], rel=1e-12)
+    assert soft[0] == pytest.approx(lam * 0.1 * (4 + 2 * math.sqrt(2)), rel=1e-12)
+    lamc = np.array([spec.lam[t.kind] for t in csp.terms])
+    assert J[0] == pytest.approx((lamc * Jc[0]).sum() + soft[0], rel=1e-12)
     # three goal objects on a unit equilateral triangle
     spec3 = copy.deepcopy(spec)
     spec3.goal_objs = spec.goal_objs[:3]
@@ -213,7 +214,7 @@ def test_goal_cost_weighted_obj_dist():
     tri = [(0.0, 0.0), (1.0, 0.0), (0.5, math.sqrt(3) / 2)]
     for (px, py), vi in zip(tri, list(csp3.goal.values())):
         x[0, csp3.offsets[vi]:csp3.offsets[vi] + 4] = [px, py, 0.0, 0.0]
-    assert _eval(spec3, csp3, x, g)[2][0] == pytest.approx(0.75, rel=1e-12)
+    assert _eval(spec3, csp3, x, g)[2][0] == pytest.approx(3 * lam, rel=1e-12)
 
 
 # ---------------------------------------------------------------------------------------------------

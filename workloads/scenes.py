@@ -125,7 +125,7 @@ class ProblemSpec:
     # cost weights lambda_c and tolerances eps_c
     lam: dict
     eps: dict
-    lam_goal: float = 0.25      # L7
+    lam_goal: float = 0.025     # L7 (revised): the main-text Table 3 value
     lam_traj: float = 0.01      # L8, revised: 1.0 let the plan cost overpower the Kin constraints
     eta: float = 0.0            # collision activation distance (L1)
     # Adam (L9)
