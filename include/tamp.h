@@ -228,7 +228,9 @@ tamp_status tamp_query_workspace(const tamp_problem_desc* desc, int64_t n_local,
 
 /* Compile the skeleton (host) and bind a context to `device` and the caller-owned
    workspace (>= tamp_query_workspace bytes, 256-B aligned).  This rank owns global particles
-   [global_offset, global_offset + n_local) of n_global.  The descriptor is copied. */
+   [global_offset, global_offset + n_local) of n_global.  The descriptor is copied.  No device work
+   and no synchronisation: the per-coordinate bounds are copied into the workspace on the stream of the first
+   tamp_sample_particles / tamp_set_state. */
 tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t n_local,
                               int64_t global_offset, int64_t n_global,
                               void* d_workspace, size_t ws_bytes, tamp_ctx** out);
@@ -269,6 +271,13 @@ tamp_status tamp_best_k(tamp_ctx* ctx, int32_t k, float* records, void* stream);
    k <= n_in <= 65536, k <= 1024. */
 tamp_status tamp_merge_best_k(tamp_ctx* ctx, const float* d_in, int32_t n_in, int32_t k, float* d_out,
                               void* stream);
+
+/* The same merge without a context (SURVEY §8(b)'s stateless form): records of width D + 4, caller-owned device
+   scratch of >= tamp_merge_scratch_bytes(n_in) bytes (256-B aligned), on the current device.  Same results as
+   tamp_merge_best_k.  Errors: TAMP_E_INVALID (arguments), TAMP_E_NOMEM (scratch too small). */
+tamp_status tamp_merge_scratch_bytes(int32_t n_in, size_t* bytes);
+tamp_status tamp_merge_records(const float* d_in, int32_t n_in, int32_t k, int32_t D, float* d_out, void* d_scratch,
+                               size_t scratch_bytes, void* stream);
 
 /* Test / inspection (not on the timed path): per-particle J, soft cost, Jc [n_local][n_hard] and
    the UNSCALED gradient dJ/dx [n_local][D] at the current x.  Any output may be NULL.  Device only. */

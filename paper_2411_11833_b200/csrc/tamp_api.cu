@@ -89,7 +89,8 @@ struct tamp_ctx {
     bool checked = false;        // cls / cost / counts are those of the current state (no step since)
     int32_t term_kind[TAMP_MAX_TERMS];
     int32_t term_action[TAMP_MAX_TERMS];
-    std::vector<float> coords;   // lr | lo | hi, uploaded at init
+    std::vector<float> coords;   // lr | lo | hi, uploaded (stream-ordered) by the first sample / set_state
+    bool coords_on_device = false;
     int64_t pairs_sb = 0, pairs_ss = 0;
     int32_t n_robot_spheres = 0;
 
@@ -1049,11 +1050,6 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         delete c;
         return fail(TAMP_E_INVALID, "workspace is not device memory");
     }
-    if (!c->coords.empty()) {
-        cudaError_t e = cudaMemcpy(c->at<float>(c->o_coords), c->coords.data(), c->coords.size() * 4,
-                                   cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) { delete c; return cuda_fail(e, "init: upload bounds"); }
-    }
     *out = c;
     return TAMP_OK;
 }
@@ -1100,10 +1096,21 @@ tamp_status tamp_get_info(const tamp_ctx* c, tamp_info* out) {
     return TAMP_OK;
 }
 
+// the per-coordinate lr | lo | hi arrays: copied into the workspace on the stream of the first call that may precede
+// every other (sample / set_state), so that init has no hidden synchronisation (tamp.h conventions)
+static cudaError_t upload_coords(tamp_ctx* c, cudaStream_t st) {
+    if (c->coords_on_device || c->coords.empty()) return cudaSuccess;
+    cudaError_t e = cudaMemcpyAsync(c->at<float>(c->o_coords), c->coords.data(), c->coords.size() * 4,
+                                    cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) c->coords_on_device = true;
+    return e;
+}
+
 tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
     if (!c) return fail(TAMP_E_INVALID, "null context");
     DeviceGuard g(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(upload_coords(c, st), "sample: upload bounds");
     CUDA_TRY(launch_sample(c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, st), "sample");
     CUDA_TRY(launch_ik(c->P, c->SP, c->at<float>(c->o_x), c->at<float>(c->o_grasp), c->n, c->gofs, seed, c->ik_iters,
                        c->ik_damping, c->ik_seeds, c->at<int32_t>(c->o_iklist), c->at<int32_t>(c->o_ikn),
@@ -1239,6 +1246,45 @@ tamp_status tamp_merge_best_k(tamp_ctx* c, const float* d_in, int32_t n_in, int3
     return TAMP_OK;
 }
 
+static size_t merge_scratch_layout(int32_t n_in, size_t* o_kb, size_t* o_pa, size_t* o_pb) {
+    const size_t n = (size_t)n_in;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+    take(n * 8);                      // keys a at offset 0
+    *o_kb = take(n * 8);
+    *o_pa = take(n * 4);
+    *o_pb = take(n * 4);
+    return o;
+}
+
+tamp_status tamp_merge_scratch_bytes(int32_t n_in, size_t* bytes) {
+    if (!bytes || n_in < 1 || n_in > 65536) return fail(TAMP_E_INVALID, "need bytes and 1 <= n_in <= 65536");
+    size_t a, b, c;
+    *bytes = merge_scratch_layout(n_in, &a, &b, &c);
+    return TAMP_OK;
+}
+
+tamp_status tamp_merge_records(const float* d_in, int32_t n_in, int32_t k, int32_t D, float* d_out, void* d_scratch,
+                               size_t scratch_bytes, void* stream) {
+    if (!d_in || !d_out || !d_scratch) return fail(TAMP_E_INVALID, "null argument");
+    if (n_in < 1 || n_in > 65536 || k < 1 || k > n_in || k > 1024) return fail(TAMP_E_INVALID, "need 1 <= k <= n_in <= 65536, k <= 1024");
+    if (D < 0 || D > TAMP_MAX_D) return fail(TAMP_E_INVALID, "D out of range");
+    if (reinterpret_cast<uintptr_t>(d_scratch) & 255) return fail(TAMP_E_INVALID, "scratch must be 256-byte aligned");
+    size_t o_kb, o_pa, o_pb;
+    if (scratch_bytes < merge_scratch_layout(n_in, &o_kb, &o_pa, &o_pb)) return fail(TAMP_E_NOMEM, "merge scratch too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* base = static_cast<char*>(d_scratch);
+    unsigned long long *ka = reinterpret_cast<unsigned long long*>(base), *kb = reinterpret_cast<unsigned long long*>(base + o_kb);
+    int32_t *pa = reinterpret_cast<int32_t*>(base + o_pa), *pb = reinterpret_cast<int32_t*>(base + o_pb);
+    const int width = D + 4;
+    CUDA_TRY(launch_record_keys(d_in, n_in, width, ka, pa, st), "merge: keys");
+    unsigned long long* kr;
+    int32_t* pr;
+    CUDA_TRY(launch_topk(ka, pa, kb, pb, n_in, k, st, &kr, &pr), "merge: sort");
+    CUDA_TRY(launch_gather_records(pr, k, d_in, width, d_out, st), "merge: gather");
+    return TAMP_OK;
+}
+
 tamp_status tamp_eval(tamp_ctx* c, float* J, float* soft, float* Jc, float* grad, void* stream) {
     if (!c) return fail(TAMP_E_INVALID, "null context");
     if (!c->ready) return fail(TAMP_E_STATE, "eval before sample/set_state");
@@ -1286,6 +1332,7 @@ tamp_status tamp_set_state(tamp_ctx* c, const float* x, const float* m, const fl
     if (!grasp && c->P.n_grasp && !c->ready) return fail(TAMP_E_STATE, "first set_state must provide grasps");
     DeviceGuard g(c->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(upload_coords(c, st), "set_state: upload bounds");
     const size_t nd = (size_t)c->n * c->P.D * 4;
     CUDA_TRY(cudaMemcpyAsync(c->base + c->o_x, x, nd, cudaMemcpyDefault, st), "set x");
     if (m) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_m, m, nd, cudaMemcpyDefault, st), "set m");

@@ -164,11 +164,16 @@ def cutamp(skeletons, n_particles: int, seed: int = 0, steps_per_pop: int = 200,
         if prune and failed and reinit_every > 0 and pops % reinit_every == 0:
             for sg, j in list(failed.items()):      # re-initialise the failed subgraphs
                 ctx = ctxs[j]
-                ctx.sample(fresh_seed(j))
+                ctx.sample(fresh_seed(j))            # (skeleton j restarts from fresh particles ...)
                 counts, _ = ctx.check()
                 t = tsigs[j].index(sg)
                 if int(counts[t]) > 0:               # counterexample: the subgraph is feasible
                     del failed[sg]
+                # ... so its queue key is that of the fresh particles, not of the state it replaced
+                queue[:] = [e for e in queue if e[1] != j]
+                heapq.heapify(queue)
+                h = plan_heuristic(counts.cpu(), ctx.n_hard, penalty)
+                heapq.heappush(queue, (-h, j))
             for i in list(pruned):
                 if not any(sg in failed for sg in tsigs[i] if sg is not None):
                     pruned.remove(i)

@@ -96,7 +96,8 @@ class Info(ctypes.Structure):
 EXPORTS = ["tamp_abi_version", "tamp_last_error", "tamp_sizeof_desc", "tamp_sizeof_info", "tamp_query_workspace",
            "tamp_init_problem", "tamp_get_info", "tamp_sample_particles", "tamp_optimize_step",
            "tamp_check_satisfied", "tamp_optimize_and_check", "tamp_best_k", "tamp_merge_best_k", "tamp_eval", "tamp_get_state",
-           "tamp_set_state", "tamp_destroy", "tamp_kernel_launches", "tamp_plan_heuristic"]
+           "tamp_set_state", "tamp_destroy", "tamp_kernel_launches", "tamp_plan_heuristic", "tamp_merge_scratch_bytes",
+           "tamp_merge_records"]
 
 _lib = None
 _lib_path = None
@@ -142,6 +143,10 @@ def load(path: str = None):
     lib.tamp_kernel_launches.restype = ctypes.c_uint64
     lib.tamp_plan_heuristic.restype = ctypes.c_double
     lib.tamp_plan_heuristic.argtypes = [vp, I32, ctypes.c_double]
+    lib.tamp_merge_scratch_bytes.argtypes = [I32, ctypes.POINTER(sz)]
+    lib.tamp_merge_scratch_bytes.restype = I32
+    lib.tamp_merge_records.argtypes = [vp, I32, I32, I32, vp, vp, sz, vp]
+    lib.tamp_merge_records.restype = I32
     for name in EXPORTS[4:15]:
         getattr(lib, name).restype = ctypes.c_int
     if lib.tamp_abi_version() != ABI_VERSION:
@@ -379,6 +384,21 @@ class TampContext:
         self._keep = (x, m, v, grasp, invalid)       # host tensors must outlive the async copy
         _check(self.lib.tamp_set_state(self.h, _ptr(x), _ptr(m), _ptr(v), _ptr(grasp), _ptr(invalid), int(t),
                                        _stream(self.device, stream)))
+
+
+def merge_records(records: torch.Tensor, k: int, stream=None) -> torch.Tensor:
+    """Stateless global top-k of best-k records [n][D+4] (tamp_merge_records; e.g. after an all-gather)."""
+    lib = load()
+    records = records.contiguous()
+    n, width = int(records.shape[0]), int(records.shape[1])
+    nb = ctypes.c_size_t()
+    _check(lib.tamp_merge_scratch_bytes(n, ctypes.byref(nb)))
+    scratch = torch.empty(nb.value + 256, dtype=torch.uint8, device=records.device)
+    off = (-scratch.data_ptr()) % 256
+    out = torch.empty(k, width, dtype=torch.float32, device=records.device)
+    _check(lib.tamp_merge_records(_ptr(records), n, int(k), width - 4, _ptr(out),
+                                  ctypes.c_void_p(scratch.data_ptr() + off), nb.value, _stream(records.device, stream)))
+    return out
 
 
 def plan_heuristic(counts, n_hard: int, penalty: float = -1e6) -> float:

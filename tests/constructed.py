@@ -150,10 +150,12 @@ def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2):
         terms_of.setdefault(t.action, []).append(ti)
     eps = np.array([spec.eps[t.kind] for t in csp.terms])
 
-    def eval_terms(tids):
+    def eval_terms(tids):            # the oracle on a CSP holding only these terms (one FK per conf involved)
+        import dataclasses
+        sub = dataclasses.replace(csp, terms=[csp.terms[t] for t in tids], goal={}, traj_costs=[])
         with torch.no_grad():
-            _, Jc, _ = O.evaluate(spec, csp, torch.as_tensor(x[None]), torch.as_tensor(G[None]))
-        return Jc.numpy()[0, tids]
+            _, Jc, _ = O.evaluate(spec, sub, torch.as_tensor(x[None]), torch.as_tensor(G[None]))
+        return Jc.numpy()[0]
 
     def set_conf(vi, q):
         x[csp.offsets[vi]:csp.offsets[vi] + 7] = q

@@ -267,6 +267,9 @@ def test_merge_best_k_equals_global_best_k():
         parts.append(c.best_k(k))
     merged = full.merge_best_k(torch.cat(parts), k)
     np.testing.assert_array_equal(merged.cpu().numpy(), ref.cpu().numpy())
+    # the stateless form (tamp_merge_records, caller scratch, no context)
+    from paper_2411_11833_b200 import merge_records
+    np.testing.assert_array_equal(merge_records(torch.cat(parts), k).cpu().numpy(), ref.cpu().numpy())
 
 
 @pytest.mark.parametrize("lanes", [4, 8, 16])

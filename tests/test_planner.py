@@ -222,3 +222,37 @@ def test_failed_subgraph_prunes_later_skeletons(monkeypatch):
         lambda c: ([t.kind for t in c.terms], [t.action for t in c.terms]))(O.build_csp(direct)))
     kp_blue = [s for s, k in zip(sig, [t.kind for t in O.build_csp(direct).terms]) if k == "KP"][1]
     assert kp_blue[1][1] == 4 and kp_blue[1][2] == "fingertip"        # (KP, conf of PressButton(fingertip))
+
+
+def test_reinit_requeues_the_reset_skeleton(monkeypatch):
+    """Re-initialising a failed subgraph re-samples its skeleton's whole context, so the skeleton must be queued
+    again with the heuristic of the fresh particles -- every sampling of a skeleton is followed by a push of that
+    skeleton, and the queue never holds two entries of one skeleton (planner.py)."""
+    events = []
+
+    class Ctx(_PruneCtx):
+        def sample(self, seed):
+            events.append(("sample", self.spec.name))
+            super().sample(seed)
+
+    monkeypatch.setattr(planner, "TampContext", Ctx)
+    monkeypatch.setattr(planner, "plan_heuristic", _heuristic)
+    real_push = planner.heapq.heappush
+    names = {}
+
+    def push(q, e):
+        assert e[1] not in [x[1] for x in q]
+        events.append(("push", names[e[1]]))
+        real_push(q, e)
+    monkeypatch.setattr(planner.heapq, "heappush", push)
+    _PruneCtx.sampled = []
+    direct = make_config(7, n=32)
+    stick = make_config(6, n=32)
+    for s_ in (direct, stick):
+        s_.ik_iters = 10
+    names.update({0: direct.name, 1: stick.name})
+    planner.cutamp([direct, stick], 32, seed=2, steps_per_pop=10, check_every=10, max_pops=3, reinit_every=2)
+    samples = [k for k, e in enumerate(events) if e == ("sample", direct.name)]
+    assert len(samples) >= 2                                   # the initial draw + a re-initialisation
+    for k in samples:
+        assert ("push", direct.name) in events[k + 1:k + 2]
