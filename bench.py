@@ -68,6 +68,9 @@ def parse():
     p.add_argument("--no-extra", action="store_true", help="skip the extra workloads (config 2, config 1 at 1M, SELF)")
     p.add_argument("--no-overlap", action="store_true", help="all-reduce of the counts on the launching stream")
     p.add_argument("--lib", default=None, help="A/B experiments: another in-tree build of libtamp.so (exp/<name>/)")
+    p.add_argument("--pipeline", type=int, default=-1,
+                   help="1: the next batch's sampling + IK on a second stream under this batch's optimisation "
+                        "(two contexts); 0: sequential; -1: auto (single-wave particle launches)")
     return p.parse_args()
 
 
@@ -240,14 +243,16 @@ def dist_init(args):
     return 1, 0, 0, None
 
 
-def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_rec=None, side=None):
+def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_rec=None, side=None, sampled=False):
     """One bench step (see module docstring).  Returns the merged global best-k records.
 
     With `side` (a CUDA stream) and NCCL, the SUM all-reduce of each interval's counts (C1) runs on the side
     stream while the next optimisation launch runs on the launching stream (particles never couple, Eq. 4,
     P:461-467, so nothing in the next launch waits for the counts); two count buffers alternate, and a buffer
-    is only rewritten after its all-reduce finished.  The counts are the same bytes either way."""
-    ctx.sample(seed)
+    is only rewritten after its all-reduce finished.  The counts are the same bytes either way.
+    sampled: the batch was already initialised (pipelined rounds, timed_rounds)."""
+    if not sampled:
+        ctx.sample(seed)
     n_int = args.adam_steps // args.check_every
     direct = host_counts is not None and world == 1
     overlap = side is not None and dist is not None and not direct
@@ -476,19 +481,37 @@ def roofline(ctx, args, opt_avg, clocks=None, cfg=None, n=None):
     return roof
 
 
-def timed_rounds(ctx, args, dist, world, flush, steps, seed0, side, opt_events=None):
+def timed_rounds(ctx, args, dist, world, flush, steps, seed0, side, opt_events=None, ctx2=None, prefetch=None):
     """Exactly `steps` bench steps between a barrier + synchronize on both sides; returns the max-over-ranks
-    device time (s) of the steps (CUDA events on the launching stream, L2 flushed before each step, untimed)."""
+    device time (s) of the steps (CUDA events on the launching stream, L2 flushed before each step, untimed).
+
+    Pipelined rounds (ctx2 and a `prefetch` stream given): two contexts alternate; during step s the next batch's
+    InitializeParticles (K1 + the conditional IK sampler) runs on the prefetch stream into the other
+    context while this batch's optimisation runs on the launching stream (batches never couple).  Every step waits
+    for its prefetch before its end event, so all of a step's work lies inside its timed window and nothing runs
+    under the untimed flush; step 0 samples its own batch inside its window.  Same particles, same results."""
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     ev = []
+    main = torch.cuda.current_stream()
+    cs = [ctx, ctx2]
     for s in range(steps):
         flush.zero_()                                 # L2 flush between timed steps (not timed)
         r0 = torch.cuda.Event(enable_timing=True)
         r1 = torch.cuda.Event(enable_timing=True)
         r0.record()
-        run_round(ctx, seed0 + s, args, dist, world, events=opt_events, side=side)
+        if ctx2 is None:
+            run_round(ctx, seed0 + s, args, dist, world, events=opt_events, side=side)
+        else:
+            cur, nxt = cs[s % 2], cs[(s + 1) % 2]
+            if s == 0:
+                cur.sample(seed0)
+            if s + 1 < steps:
+                prefetch.wait_stream(main)
+                nxt.sample(seed0 + s + 1, stream=prefetch)
+            run_round(cur, seed0 + s, args, dist, world, events=opt_events, side=side, sampled=True)
+            main.wait_stream(prefetch)
         r1.record()
         ev.append((r0, r1))
     torch.cuda.synchronize()
@@ -546,8 +569,20 @@ def main():
                       block_threads=args.block_threads, block_sync=args.block_sync)
     side = None if (args.no_overlap or dist is None) else torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
+    # pipelined rounds pay where the particle launches leave SMs idle (one partial wave: config 2); with full waves
+    # the prefetch only competes for them (config 3, measured)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    single_wave = ctx.lanes_per_particle > 1 and n <= nsm * (ctx.block_threads // ctx.lanes_per_particle)
+    pipeline = args.pipeline if args.pipeline >= 0 else int(single_wave)
+    ctx2 = prefetch = None
+    if pipeline:
+        ctx2 = TampContext(spec, n, global_offset=rank * n, n_global=n_global, device=dev,
+                           lanes_per_particle=args.lanes, block_threads=args.block_threads, block_sync=args.block_sync)
+        prefetch = torch.cuda.Stream(dev)
     for w in range(args.warmup):
         run_round(ctx, 10_000 + w, args, dist, world, side=side)
+        if ctx2 is not None:
+            run_round(ctx2, 11_000 + w, args, dist, world, side=side)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -555,7 +590,8 @@ def main():
     opt_events, reps = [], []
     with ClockSampler(local) as clk:
         for r in range(args.repeats):
-            t_round = timed_rounds(ctx, args, dist, world, flush, args.steps, 20_000 + 1000 * r, side, opt_events)
+            t_round = timed_rounds(ctx, args, dist, world, flush, args.steps, 20_000 + 1000 * r, side, opt_events,
+                                   ctx2=ctx2, prefetch=prefetch)
             reps.append((t_round, n_global * args.adam_steps * args.steps / t_round))
     launches = (kernel_launches() - launches0) // args.repeats
     t_round, value = sorted(reps, key=lambda tv: tv[1])[len(reps) // 2]        # median of the repeats
@@ -616,6 +652,7 @@ def main():
                            "ik_iters": args.ik_iters, "ik_seeds": args.ik_seeds, "self_collision": args.self_collision,
                            "lanes_per_particle": ctx.lanes_per_particle, "block_threads": ctx.block_threads,
                            "block_sync": ctx.block_sync, "allreduce": "side stream, overlapped" if side else "inline",
+                           "pipeline": "next batch's sampling + IK on a second stream" if pipeline else "sequential",
                            "parallelism": f"dp{world}"},
                 "repeats": {"n": len(reps), "values": [v for _, v in reps], "reported": "median"},
                 "kernel_ms_per_launch": opt_avg * 1e3, "kernel_steps_per_launch": args.check_every,
