@@ -1001,9 +1001,11 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
                 // SM: the rate per SM grows as w / (w + 20), fitted to config 3 (76 particles per SM = 19 warps,
                 // 3 waves: 2.29 ms; 96 = 24 warps, 3 waves: 2.59 ms).  Fewer, fuller waves win: config 3 at
                 // 32,768 runs 2 waves of 111 particles (888 threads, the 896-bound variant) instead of 3 of 74.
+                // (ties go to the larger block: fewer, larger blocks per SM share the instruction cache -- 4
+                // independent 128-thread blocks ran config 4 at half the speed of one 448-thread block)
                 double best_cost = 1e300;
                 int best_t = 128, best_b = 1, best_W = 1;
-                for (int t = 128; t <= max_threads; t += 32) {
+                for (int t = (max_threads / 32) * 32; t >= 128; t -= 32) {
                     const int ppb = t / c->gs;
                     if (ppb % ppw || ppb > max_pp) continue;
                     const int bps = blocks_per_sm(t);
