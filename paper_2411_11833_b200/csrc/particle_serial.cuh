@@ -219,8 +219,9 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 q[j] = xs(K.xoff + j);
                 fsincos(q[j], &sq[j], &cq[j]);
             }
-            // forward: T_{j+1} = T_j F_{j+1} Rz(q_{j+1}) (base folded into F_1), tool T_8 = T_7 F_ee
-            M34 T;
+            // forward: T_{j+1} = T_j F_{j+1} Rz(q_{j+1}) (base folded into F_1), tool T_8 = T_7 F_ee; T keeps its
+            // rows 0-1 packed (M34P: FFMA2 compose, the scalar compose's values)
+            M34P T;
 #pragma unroll
             for (int j = 0; j < TAMP_NJ; ++j) {
                 M34 Aj;
@@ -232,12 +233,12 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     Aj.r[3 * i + 2] = Fr[2];
                     Aj.t[i] = Fr[3];
                 }
-                T = j == 0 ? Aj : compose(T, Aj);
+                T = j == 0 ? pack_m34(Aj) : compose_p(T, Aj);
             }
             {
                 M34 Fe;
                 load_m34(Fe, P.F[kGroup - 1]);
-                T = compose(T, Fe);
+                T = compose_p(T, Fe);
             }
             Wrench sfx;      // suffix wrench of the links >= the current one (about the world origin)
             sfx.zero();
@@ -252,14 +253,15 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 }
                 const float ipk[12] = {ip(ki, 0), 0.f, 0.f, ip(ki, 2), ip(ki, 1), 0.f, 0.f, ip(ki, 3), 0.f, 0.f, 0.f, ip(ki, 4)};
                 const M34 Ts = compose_rz(ipk, Tg);   // T(p) T(g), T(p) = (Rz(yaw), t)
-                const float dx = T.t[0] - Ts.t[0], dy = T.t[1] - Ts.t[1], dz = T.t[2] - Ts.t[2];
+                const M34 Tu = unpack_m34(T);
+                const float dx = Tu.t[0] - Ts.t[0], dy = Tu.t[1] - Ts.t[1], dz = Tu.t[2] - Ts.t[2];
                 const float epos = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
                 float Mm[9];
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
                     for (int j = 0; j < 3; ++j)
-                        Mm[3 * i + j] = fmaf(T.r[i], Ts.r[j], fmaf(T.r[3 + i], Ts.r[3 + j], T.r[6 + i] * Ts.r[6 + j]));
+                        Mm[3 * i + j] = fmaf(Tu.r[i], Ts.r[j], fmaf(Tu.r[3 + i], Ts.r[3 + j], Tu.r[6 + i] * Ts.r[6 + j]));
                 const float wx = Mm[7] - Mm[5], wy = Mm[2] - Mm[6], wz = Mm[3] - Mm[1];
                 const float wn = sqrtf(fmaf(wx, wx, fmaf(wy, wy, wz * wz)));
                 const float erot = fatan2_pos(0.5f * wn, 0.5f * (Mm[0] + Mm[4] + Mm[8] - 1.f));
@@ -271,14 +273,14 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     if (K.term_kp >= 0 && epos > 0.f) {
                         const float k = P.term_lam[K.term_kp] / epos;
                         const float fx = dx * k, fy = dy * k, fz = dz * k;
-                        sfx.add_point(T.t[0], T.t[1], T.t[2], fx, fy, fz);
+                        sfx.add_point(Tu.t[0], Tu.t[1], Tu.t[2], fx, fy, fz);
                         tw.add_point(Ts.t[0], Ts.t[1], Ts.t[2], -fx, -fy, -fz);
                     }
                     if (K.term_kr >= 0 && wn > 0.f) {
                         const float k = P.term_lam[K.term_kr] / wn;
-                        const float ux = k * fmaf(T.r[0], wx, fmaf(T.r[1], wy, T.r[2] * wz));
-                        const float uy = k * fmaf(T.r[3], wx, fmaf(T.r[4], wy, T.r[5] * wz));
-                        const float uz = k * fmaf(T.r[6], wx, fmaf(T.r[7], wy, T.r[8] * wz));
+                        const float ux = k * fmaf(Tu.r[0], wx, fmaf(Tu.r[1], wy, Tu.r[2] * wz));
+                        const float uy = k * fmaf(Tu.r[3], wx, fmaf(Tu.r[4], wy, Tu.r[5] * wz));
+                        const float uz = k * fmaf(Tu.r[6], wx, fmaf(Tu.r[7], wy, Tu.r[8] * wz));
                         sfx.m[0] -= ux; sfx.m[1] -= uy; sfx.m[2] -= uz;
                         tw.m[0] += ux; tw.m[1] += uy; tw.m[2] += uz;
                     }
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 if (near) {
                     const float* lb = P.lbound[l];
                     float bx, by, bz;
-                    xform(T, lb[0], lb[1], lb[2], bx, by, bz);
+                    xform_p(T, lb[0], lb[1], lb[2], bx, by, bz);
                     const float br = lb[3] + P.eta + kLinkMargin;
                     near = false;
                     if (one_obb) {
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
 #pragma unroll
                     for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
                         const float4 c4 = s_rsph[l][k];
-                        xform(T, c4.x, c4.y, c4.z, wq[k][0], wq[k][1], wq[k][2]);
+                        xform_p(T, c4.x, c4.y, c4.z, wq[k][0], wq[k][1], wq[k][2]);
                         rq[k] = c4.w;
                         hit[k] = k < ns && obb_within(wq[k][0], wq[k][1], wq[k][2], rq[k], B0);
                     }
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
                         const float4 c4 = s_rsph[l][k];
                         float wx, wy, wz;
-                        xform(T, c4.x, c4.y, c4.z, wx, wy, wz);
+                        xform_p(T, c4.x, c4.y, c4.z, wx, wy, wz);
                         const float rr = c4.w;
                         float g[3] = {0.f, 0.f, 0.f};
                         if (one_obb) {
@@ -381,8 +383,8 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 }
                 if (l < TAMP_NJ) {     // joint l+1 rotates frame l+1 (= T here) about its z axis
                     if (G) {
-                        const float zx = T.r[2], zy = T.r[5], zz = T.r[8];
-                        const float ox = T.t[0], oy = T.t[1], oz = T.t[2];
+                        const float zx = T.r(0, 2), zy = T.r(1, 2), zz = T.r(2, 2);
+                        const float ox = T.t(0), oy = T.t(1), oz = T.t(2);
                         const float mx = sfx.m[0] - (oy * sfx.f[2] - oz * sfx.f[1]);
                         const float my = sfx.m[1] - (oz * sfx.f[0] - ox * sfx.f[2]);
                         const float mz = sfx.m[2] - (ox * sfx.f[1] - oy * sfx.f[0]);
@@ -399,16 +401,16 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     if (l < TAMP_NJ) {
                         float sl, cl;
                         fsincos(xs(K.xoff + l), &sl, &cl);
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) {
-                            const float a = T.r[3 * i], b = T.r[3 * i + 1];
-                            T.r[3 * i] = fmaf(a, cl, -b * sl);
-                            T.r[3 * i + 1] = fmaf(a, sl, b * cl);
-                        }
+                        const F2 a = T.r01[0], b = T.r01[1];
+                        T.r01[0] = fma2(a, bc(cl), mul2(b, bc(-sl)));
+                        T.r01[1] = fma2(a, bc(sl), mul2(b, bc(cl)));
+                        const float a2 = T.r2[0], b2 = T.r2[1];
+                        T.r2[0] = fmaf(a2, cl, -b2 * sl);
+                        T.r2[1] = fmaf(a2, sl, b2 * cl);
                     }
                     M34 Fi;
                     load_m34(Fi, P.Finv[l]);
-                    T = compose(T, Fi);
+                    T = compose_p(T, Fi);
                 }
             }
             if (K.term_cf >= 0) serial_term<M>(P, A, sink, K.term_cf, jcf, active, p, s_counts);

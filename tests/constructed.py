@@ -120,15 +120,16 @@ def tetris_tiled_placements(spec, W, H, shapes):
     return out
 
 
-def _ik(spec, T, rng, tries=24, iters=300):
-    """A conf reaching T exactly (errors < 1e-7), from random starts: the oracle's DLS IK (pinned)."""
+def _ik(spec, T, rng, tries=32, iters=300):
+    """Confs reaching T exactly (errors < 1e-7), from random starts solved as one batch: the oracle's DLS IK
+    (pinned)."""
     rob = spec.robot
-    for _ in range(tries):
-        q0 = rng.uniform(rob.joint_lo, rob.joint_hi)[None]
-        q = O.ik_dls(rob, q0, T[None], iters, 0.05)
-        ep, th = O.ik_errors(rob, q, T[None])
-        if ep[0] < 1e-7 and th[0] < 1e-7:
-            yield q[0]
+    q0 = rng.uniform(rob.joint_lo, rob.joint_hi, (tries, 7))
+    q = O.ik_dls(rob, q0, np.broadcast_to(T, (tries, 4, 4)).copy(), iters, 0.05)
+    ep, th = O.ik_errors(rob, q, np.broadcast_to(T, (tries, 4, 4)).copy())
+    for k in range(tries):
+        if ep[k] < 1e-7 and th[k] < 1e-7:
+            yield q[k]
 
 
 def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2):
@@ -174,8 +175,12 @@ def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2):
         gslot = csp.grasp_vars.index(a_pick.grasp)
         o = spec.objects[i]
         done = False
-        for gamma in rng.permutation(np.arange(24) * math.pi / 12):
-            Tg = O.top_down_grasp(torch.tensor([0.0]), torch.tensor([0.0]), torch.tensor([o.grasp_z]),
+        cands = [(0.0, 0.0, gm) for gm in rng.permutation(np.arange(24) * math.pi / 12)]
+        cands += [(gx, gy, gm) for gx, gy, gm in zip(rng.uniform(-o.grasp_xy, o.grasp_xy, 48),
+                                                      rng.uniform(-o.grasp_xy, o.grasp_xy, 48),
+                                                      rng.uniform(-math.pi, math.pi, 48))]
+        for gx, gy, gamma in cands:
+            Tg = O.top_down_grasp(torch.tensor([gx]), torch.tensor([gy]), torch.tensor([o.grasp_z]),
                                   torch.tensor([gamma]))[0].numpy()
             G[gslot] = Tg[:3]
             T_pick = (O.pose_xyzyaw(torch.tensor(V[a_pick.placement].value)).numpy() @ Tg)
