@@ -735,8 +735,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         for (int c = 0; c < 4; ++c) s_rsoa[l][TAMP_MAX_SPHERES_PER_LINK * c + k] = P.rsph[l][k][c];
         s_selfmask[threadIdx.x] = P.self_mask[threadIdx.x];
     }
-    float4* rsw = reinterpret_cast<float4*>(S + A.off_rsw) + (HP > 1 ? half : 0) * (kGroup * TAMP_MAX_SPHERES_PER_LINK + kGroup);
-    float4* rlb = rsw + kGroup * TAMP_MAX_SPHERES_PER_LINK;       // world bounding sphere of each link frame
+    float4* rsw = reinterpret_cast<float4*>(S + A.off_rsw) + (HP > 1 ? half : 0) * (kGroup * TAMP_MAX_SPHERES_PER_LINK);
     int nsph[LPL];
     float jlo[LPL], jhi[LPL];
 #pragma unroll
@@ -935,49 +934,44 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                         [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, mov, ip + 48, ll, half, real); }, smooth);
                 }
             }
-            // robot self-collision: every lane tests its own spheres against their pair
-            // partners (sphere centres shared through shared memory), keeping only its own spheres' gradient;
-            // each pair's hinge is counted once, by the lower sphere id.
+            // robot self-collision: every lane tests its own spheres against the configuration's
+            // robot spheres (centres shared through shared memory) in packed pairs -- d^2 - (r_a + r_b)^2 as the
+            // exact reject test, its sign bits ANDed with the pair mask -- and evaluates the exact hinges of the
+            // active pairs, keeping only its own spheres' gradient; each pair's hinge is counted once, by the lower
+            // sphere id
             if (K.term_self >= 0) {
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
                     rsw[ll * NS + s] = make_float4(rs.sx(s), rs.sy(s), rs.sz(s), rs.sr(s) - P.eta);
-#pragma unroll
-                for (int u = 0; u < LPL; ++u) {
-                    const float* lb = P.lbound[ll * LPL + u];
-                    float bx, by, bz;
-                    xform(T[u], lb[0], lb[1], lb[2], bx, by, bz);
-                    rlb[ll * LPL + u] = make_float4(bx, by, bz, lb[3] + P.eta);
-                }
                 __syncwarp();
                 float js = 0.f;
                 const float lam_self = P.term_lam[K.term_self];
+                uint32_t sact[NS];
 #pragma unroll
-                for (int u = 0; u < LPL; ++u) {
-                    // broad phase: links whose bounding spheres overlap this link's
-                    const float4 a4 = rlb[ll * LPL + u];
-                    uint32_t near = 0u;
+                for (int s = 0; s < NS; ++s) sact[s] = 0u;
+#pragma unroll 4
+                for (int t = 0; t < kGroup * TAMP_MAX_SPHERES_PER_LINK; ++t) {
+                    const float4 B = rsw[t];
 #pragma unroll
-                    for (int m = 0; m < kGroup; ++m) {
-                        const float4 b4 = rlb[m];
-                        const float dx = a4.x - b4.x, dy = a4.y - b4.y, dz = a4.z - b4.z;
-                        const float R = a4.w + b4.w;
-                        near |= (fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f ? 0xFu : 0u) << (4 * m);
+                    for (int j = 0; j < QSet<NS>::NP; ++j) {
+                        const F2 tt = reach2(sub2(rs.x[j], bc(B.x)), sub2(rs.y[j], bc(B.y)), sub2(rs.z[j], bc(B.z)),
+                                             rs.r[j], B.w);
+                        sact[2 * j] |= (__float_as_uint(lo(tt)) >> 31) << t;
+                        if (2 * j + 1 < NS) sact[2 * j + 1] |= (__float_as_uint(hi(tt)) >> 31) << t;
                     }
+                }
 #pragma unroll
-                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
-                        const int s = u * TAMP_MAX_SPHERES_PER_LINK + k;
-                        const int sid = ll * NS + s;
-                        uint32_t m = s_selfmask[sid] & near;
-                        while (m) {
-                            const int t = __ffs(m) - 1;
-                            m &= m - 1u;
-                            float ux, uy, uz;
-                            const float pen = sphere_sphere<G>(rs.sx(s), rs.sy(s), rs.sz(s), rs.sr(s), rsw[t], lam_self, ux, uy,
-                                                                  uz, smooth);
-                            if (sid < t) js += pen;
-                            if (G) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
-                        }
+                for (int s = 0; s < NS; ++s) {
+                    const int sid = ll * NS + s;
+                    uint32_t m = s_selfmask[sid] & sact[s];
+                    while (m) {
+                        const int t = __ffs(m) - 1;
+                        m &= m - 1u;
+                        float ux, uy, uz;
+                        const float pen = sphere_sphere<G>(rs.sx(s), rs.sy(s), rs.sz(s), rs.sr(s), rsw[t], lam_self, ux, uy,
+                                                              uz, smooth);
+                        if (sid < t) js += pen;
+                        if (G) { gw[s][0] -= ux; gw[s][1] -= uy; gw[s][2] -= uz; }
                     }
                 }
                 finish_term<M>(P, A, sinkB, K.term_self, term_sum<M, LPF>(js), ll, active, p, s_counts, real);

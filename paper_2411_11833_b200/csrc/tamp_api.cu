@@ -729,7 +729,7 @@ static void smem_layout(tamp_ctx* c) {
     off = r4(off);
     c->const_floats = kInstFloats * n_const;          // constant instances: once per block
     c->off_rsw = off;                                 // robot sphere centres for the SELF term (2 FK halves)
-    off += P.has_self ? 2 * 4 * (kGroup * TAMP_MAX_SPHERES_PER_LINK + kGroup) : 0;   // + link bounding spheres
+    off += P.has_self ? (c->gs == 16 ? 2 : 1) * 4 * (kGroup * TAMP_MAX_SPHERES_PER_LINK) : 0;   // per FK half
     // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
     int stride = ((off + 31) / 32) * 32 + 8;
     c->stride = stride;

@@ -120,24 +120,26 @@ def tetris_tiled_placements(spec, W, H, shapes):
     return out
 
 
-def _ik(spec, T, rng, tries=32, iters=300):
-    """Confs reaching T exactly (errors < 1e-7), from random starts solved as one batch: the oracle's DLS IK
-    (pinned)."""
+def _ik(spec, T, rng, tries=32, iters=300, tol=(1e-7, 1e-7)):
+    """Confs reaching T (errors below tol: exact by default), from random starts solved as one batch: the oracle's
+    DLS IK (pinned)."""
     rob = spec.robot
     q0 = rng.uniform(rob.joint_lo, rob.joint_hi, (tries, 7))
     q = O.ik_dls(rob, q0, np.broadcast_to(T, (tries, 4, 4)).copy(), iters, 0.05)
     ep, th = O.ik_errors(rob, q, np.broadcast_to(T, (tries, 4, 4)).copy())
     for k in range(tries):
-        if ep[k] < 1e-7 and th[k] < 1e-7:
+        if ep[k] < tol[0] and th[k] < tol[1]:
             yield q[k]
 
 
-def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2):
+def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2, ik_tol=(1e-7, 1e-7)):
     """Hand-constructed satisfying particle of a Tetris skeleton: pieces on an exact tiling of the grid (z on the
     region, yaws multiples of pi/2), top-down grasps over each piece's centroid with the gripper turned so its
     fingers lie along the piece's own cells (searched over 24 yaws), pick / place confs by exact IK
     (T(g) := placement-consistent, FK(q) = T(p) T(g)), each chosen among IK solutions so that its own CF terms are
-    exactly 0; knots (config 4) at confs reaching the same TCP poses lifted by `lift`.  Every pick / place and knot
+    exactly 0 (ik_tol: the Kin residual accepted -- exact by default; config 4's last pick is at the arm's reach,
+    where 1 mm / 0.01 rad, a fifth of the 5 mm / 0.05 rad tolerances of P:1133, is what the IK attains);
+    knots (config 4) at confs reaching the same TCP poses lifted by `lift`.  Every pick / place and knot
     is checked with the oracle (CF, JL; Kin by construction); returns (x [D], grasps [G, 3, 4])."""
     V = spec.variables
     vid = {v.name: i for i, v in enumerate(V)}
@@ -189,7 +191,7 @@ def satisfying_tetris(spec, csp, rng, W, H, shapes, lift=0.2):
             for a_idx, T in ((ai + 1, T_pick), (ai + 3, T_place)):
                 a = spec.actions[a_idx]
                 good = False
-                for q in _ik(spec, T, rng):
+                for q in _ik(spec, T, rng, tol=ik_tol):
                     set_conf(a.q1, q)
                     tids = [t for t in terms_of[a_idx] if csp.terms[t].kind in ("JL", "CF")]
                     if np.all(eval_terms(tids) == 0.0):

@@ -46,15 +46,17 @@ def test_constructed_tetris_particle_is_an_exact_tiling(cfg):
 
 @pytest.mark.parametrize("cfg", [3, 4])
 def test_constructed_tetris_particle_satisfies_eq3_in_the_oracle(cfg):
-    """Class 0: every collision / bounds / support / containment term is exactly 0, Kin residuals are rounding."""
+    """Class 0: every collision / bounds / support / containment term is exactly 0; the Kin residuals are rounding
+    (config 3) or at most a fifth of their tolerances (config 4, whose last pick is at the arm's reach)."""
     x, G, *_ = _fixture(cfg)
     spec = make_config(cfg, n=1)
     csp = O.build_csp(spec)
     cls, counts, J, soft, Jc = O.check(spec, csp, O.new_state(x[None], G[None]))
     assert cls[0] == 0 and counts[-2] == 1
     kin = np.array([t.kind in ("KP", "KR") for t in csp.terms])
+    eps = np.array([spec.eps[t.kind] for t in csp.terms])
     assert np.all(Jc[0, ~kin] == 0.0)
-    assert np.all(Jc[0, kin] < 1e-6)
+    assert np.all(Jc[0, kin] <= (1e-6 if cfg == 3 else 0.2 * eps[kin]))
 
 
 @pytest.mark.gpu

@@ -16,13 +16,14 @@ from workloads import make_config  # noqa: E402
 from constructed import satisfying_tetris  # noqa: E402
 
 CASES = {3: (4, 4, ["I", "L", "O", "J"]), 4: (6, 4, ["I", "L", "O", "J", "I", "I"])}
+IK_TOL = {3: (1e-7, 1e-7), 4: (1e-3, 1e-2)}     # config 4: its last piece's pick is at the arm's reach
 
 for cfg in [int(a) for a in sys.argv[1:]] or [3, 4]:
     W, H, shapes = CASES[cfg]
     t0 = time.time()
     spec = make_config(cfg, n=1)
     csp = O.build_csp(spec)
-    x, G = satisfying_tetris(spec, csp, np.random.default_rng(cfg), W, H, shapes)
+    x, G = satisfying_tetris(spec, csp, np.random.default_rng(cfg), W, H, shapes, ik_tol=IK_TOL[cfg])
     cls, counts, J, soft, Jc = O.check(spec, csp, O.new_state(x[None], G[None]))
     assert cls[0] == 0, "constructed particle is not satisfying"
     path = os.path.join(ROOT, "tests", "golden", f"tetris_satisfying_cfg{cfg}.npz")
