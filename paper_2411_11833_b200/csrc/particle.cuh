@@ -524,6 +524,36 @@ __device__ __forceinline__ float pairs_vs_instance(const QSet<NS>& q, const floa
     return j;
 }
 
+// sphere_obb's exact reject test for a packed pair of spheres with box-frame offsets p and radii r: a sphere reaches
+// the box unless s >= r^2, s = ||max(|p| - h, 0)||^2, evaluated as 4 s = ||a + |a|||^2 >= (2r)^2 (a = |p| - h; 2 max(a, 0)
+// = a + |a| on the FMA pipe, scaling by 4 exact)
+__device__ __forceinline__ void obb_reach_pair(F2 px, F2 py, F2 pz, F2 r, const KObb& B, bool& h0, bool& h1) {
+    float qq[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float ax = fabsf(h ? hi(px) : lo(px)) - B.h[0];
+        const float ay = fabsf(h ? hi(py) : lo(py)) - B.h[1];
+        const float az = fabsf(h ? hi(pz) : lo(pz)) - B.h[2];
+        qq[h][0] = ax + fabsf(ax);  qq[h][1] = ay + fabsf(ay);  qq[h][2] = az + fabsf(az);
+    }
+    const F2 qx = pk(qq[0][0], qq[1][0]), qy = pk(qq[0][1], qq[1][1]), qz = pk(qq[0][2], qq[1][2]);
+    const F2 s4 = fma2(qx, qx, fma2(qy, qy, mul2(qz, qz)));
+    const F2 r2 = add2(r, r);
+    const F2 r4 = mul2(r2, r2);
+    h0 = !(lo(s4) >= lo(r4));
+    h1 = !(hi(s4) >= hi(r4));
+}
+// box-frame offsets p = R^T (w - c) of a packed pair of points (aligned boxes: the offsets themselves)
+__device__ __forceinline__ void obb_offsets_pair(F2 x, F2 y, F2 z, const KObb& B, F2& px, F2& py, F2& pz) {
+    const F2 dx = sub2(x, bc(B.c[0])), dy = sub2(y, bc(B.c[1])), dz = sub2(z, bc(B.c[2]));
+    px = dx; py = dy; pz = dz;
+    if (!B.aligned) {
+        px = fma2(bc(B.R[0]), dx, fma2(bc(B.R[3]), dy, mul2(bc(B.R[6]), dz)));
+        py = fma2(bc(B.R[1]), dx, fma2(bc(B.R[4]), dy, mul2(bc(B.R[7]), dz)));
+        pz = fma2(bc(B.R[2]), dx, fma2(bc(B.R[5]), dy, mul2(bc(B.R[8]), dz)));
+    }
+}
+
 // NS query spheres per lane vs one OBB: the exact reject test of every sphere first (packed straight-line code),
 // hinge + gradient only for spheres that reach the box, and nothing at all unless some sphere of the warp does.
 // Small boxes are first gated by their bounding sphere.  The reject test is sphere_obb's own, s >= r^2 with
@@ -554,23 +584,13 @@ __device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B
                 pz = fma2(bc(B.R[2]), dx, fma2(bc(B.R[5]), dy, mul2(bc(B.R[8]), dz)));
             }
             if (TAMP_PACK_OBB == 1) {   // 2 max(a, 0) = a + |a| on the FMA pipe; 4 s >= (2r)^2 (scaling by 4 exact)
-                float qq[2][3];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const float ax = fabsf(h ? hi(px) : lo(px)) - B.h[0];
-                    const float ay = fabsf(h ? hi(py) : lo(py)) - B.h[1];
-                    const float az = fabsf(h ? hi(pz) : lo(pz)) - B.h[2];
-                    qq[h][0] = ax + fabsf(ax);  qq[h][1] = ay + fabsf(ay);  qq[h][2] = az + fabsf(az);
-                }
-                const F2 qx = pk(qq[0][0], qq[1][0]), qy = pk(qq[0][1], qq[1][1]), qz = pk(qq[0][2], qq[1][2]);
-                const F2 s4 = fma2(qx, qx, fma2(qy, qy, mul2(qz, qz)));
-                const F2 r2 = add2(q.r[j], q.r[j]);
-                const F2 r4 = mul2(r2, r2);
-                hit[2 * j] = !(lo(s4) >= lo(r4));
-                any = any || hit[2 * j];
+                bool h0, h1;
+                obb_reach_pair(px, py, pz, q.r[j], B, h0, h1);
+                hit[2 * j] = h0;
+                any = any || h0;
                 if (2 * j + 1 < NS) {
-                    hit[2 * j + 1] = !(hi(s4) >= hi(r4));
-                    any = any || hit[2 * j + 1];
+                    hit[2 * j + 1] = h1;
+                    any = any || h1;
                 }
             } else {                    // obb_within's own formula on the packed offsets
 #pragma unroll

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     };
 
     __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];
+    __shared__ __align__(16) float s_rsoa[kGroup][4 * TAMP_MAX_SPHERES_PER_LINK];   // the same, SoA x[4] y[4] z[4] r[4]
     for (int i = tid; i < TAMP_MAX_OBJECTS * TAMP_MAX_OBJ_SPHERES; i += NT) {
         const int o = i / TAMP_MAX_OBJ_SPHERES, k = i % TAMP_MAX_OBJ_SPHERES;
         s_osph[o][k] = make_float4(P.osph[o][k][0], P.osph[o][k][1], P.osph[o][k][2], P.osph[o][k][3]);
@@ -122,6 +123,9 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     for (int i = tid; i < kGroup * TAMP_MAX_SPHERES_PER_LINK; i += NT) {
         const int l = i / TAMP_MAX_SPHERES_PER_LINK, k = i % TAMP_MAX_SPHERES_PER_LINK;
         s_rsph[l][k] = make_float4(P.rsph[l][k][0], P.rsph[l][k][1], P.rsph[l][k][2], P.rsph[l][k][3] + P.eta);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            s_rsoa[l][TAMP_MAX_SPHERES_PER_LINK * c + k] = c < 3 ? P.rsph[l][k][c] : P.rsph[l][k][3] + P.eta;
     }
     if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = tid; i < P.n_terms + 2; i += NT) s_counts[i] = 0;
@@ -336,15 +340,29 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     // one box, no partner instances (pick-place): the exact reject test of all of the link's
                     // spheres first (straight-line code, independent chains), hinges and gradients only for those
                     // that reach the box -- the others add exact zeros, so the result is unchanged
+                    // (spheres in packed pairs: FFMA2 transforms and reject tests, the scalar code's values)
                     const int ns = P.rsph_n[l];
                     float wq[TAMP_MAX_SPHERES_PER_LINK][3], rq[TAMP_MAX_SPHERES_PER_LINK];
                     bool hit[TAMP_MAX_SPHERES_PER_LINK];
+                    const float* cs = s_rsoa[l];
 #pragma unroll
-                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
-                        const float4 c4 = s_rsph[l][k];
-                        xform_p(T, c4.x, c4.y, c4.z, wq[k][0], wq[k][1], wq[k][2]);
-                        rq[k] = c4.w;
-                        hit[k] = k < ns && obb_within(wq[k][0], wq[k][1], wq[k][2], rq[k], B0);
+                    for (int kp = 0; kp < TAMP_MAX_SPHERES_PER_LINK / 2; ++kp) {
+                        const F2 cx = *reinterpret_cast<const F2*>(cs + 2 * kp);
+                        const F2 cy = *reinterpret_cast<const F2*>(cs + 4 + 2 * kp);
+                        const F2 cz = *reinterpret_cast<const F2*>(cs + 8 + 2 * kp);
+                        const F2 cr = *reinterpret_cast<const F2*>(cs + 12 + 2 * kp);
+                        const F2 wx = fma2(bc(T.r(0, 0)), cx, fma2(bc(T.r(0, 1)), cy, fma2(bc(T.r(0, 2)), cz, bc(T.t(0)))));
+                        const F2 wy = fma2(bc(T.r(1, 0)), cx, fma2(bc(T.r(1, 1)), cy, fma2(bc(T.r(1, 2)), cz, bc(T.t(1)))));
+                        const F2 wz = fma2(bc(T.r(2, 0)), cx, fma2(bc(T.r(2, 1)), cy, fma2(bc(T.r(2, 2)), cz, bc(T.t(2)))));
+                        F2 px, py, pz;
+                        obb_offsets_pair(wx, wy, wz, B0, px, py, pz);
+                        bool h0, h1;
+                        obb_reach_pair(px, py, pz, cr, B0, h0, h1);
+                        const int k = 2 * kp;
+                        wq[k][0] = lo(wx); wq[k][1] = lo(wy); wq[k][2] = lo(wz); rq[k] = lo(cr);
+                        wq[k + 1][0] = hi(wx); wq[k + 1][1] = hi(wy); wq[k + 1][2] = hi(wz); rq[k + 1] = hi(cr);
+                        hit[k] = k < ns && h0;
+                        hit[k + 1] = k + 1 < ns && h1;
                     }
 #pragma unroll
                     for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
