@@ -864,3 +864,26 @@ def test_abi_error_behaviour():
         TampContext(spec, 16, lanes_per_particle=3)
     with pytest.raises(TampError, match="E_INVALID"):
         TampContext(spec, 16, lanes_per_particle=8, block_threads=100)
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 256), (3, 256), (4, 128)])
+def test_ik_sampler_every_kin_conf_matches_oracle(cfg, n):
+    """The conditional IK sampler with the bench's settings (20 iterations x 8 restarts, R6) on every Kin conf of the
+    skeleton: per conf, the fraction of particles whose conf satisfies its Kin position / rotation constraints agrees
+    with the oracle's sampler on the same seeded inputs (an iterative solver on a redundant arm: confs may differ by
+    null-space drift, the satisfaction rate may not)."""
+    spec = make_config(cfg, n=n)
+    spec.ik_iters, spec.ik_seeds = 20, 8
+    csp = O.build_csp(spec)
+    ctx = TampContext(spec, n)
+    ctx.sample(seed=720 + cfg)
+    _, _, Jc, _ = ctx.eval()
+    Jc = Jc.cpu().numpy()
+    xo, go = O.initialize_particles(spec, csp, 720 + cfg, np.arange(n))
+    _, Jco, _ = O.evaluate(spec, csp, torch.as_tensor(xo), torch.as_tensor(go))
+    Jco = Jco.detach().numpy()
+    for i, t in enumerate(csp.terms):
+        if t.kind in ("KP", "KR"):
+            e = spec.eps[t.kind]
+            fg, fo = (Jc[:, i] <= e).mean(), (Jco[:, i] <= e).mean()
+            assert abs(fg - fo) <= 0.1, (t.kind, t.action, fg, fo)
