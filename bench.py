@@ -280,8 +280,8 @@ def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_
             side.wait_stream(main_s)
             with torch.cuda.stream(side):
                 dist.all_reduce(counts)                   # NCCL SUM of satisfied counts (C1), overlapped
-            if host_counts is not None:
-                host_counts.copy_(counts)
+                if host_counts is not None:
+                    host_counts.copy_(counts, non_blocking=True)   # D2H after the all-reduce, same stream
         elif not direct:                                  # (direct: D2H through the C ABI into the host buffer)
             if dist is not None:
                 dist.all_reduce(counts)                   # NCCL SUM of satisfied counts (C1)
