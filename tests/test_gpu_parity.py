@@ -887,3 +887,26 @@ def test_ik_sampler_every_kin_conf_matches_oracle(cfg, n):
             e = spec.eps[t.kind]
             fg, fo = (Jc[:, i] <= e).mean(), (Jco[:, i] <= e).mean()
             assert abs(fg - fo) <= 0.1, (t.kind, t.action, fg, fo)
+
+
+def test_bench_pipelined_round_equals_sequential_round():
+    """bench.py's pipelined rounds: a batch sampled on a second stream into a second context, then optimised with
+    sampled=True, gives bit-identical merged best-k records and counts to the sequential round (batches never
+    couple; the prefetch only moves InitializeParticles to another stream)."""
+    import bench
+
+    class Args:
+        adam_steps, check_every, k = 30, 10, 8
+    spec = make_config(2, n=512)
+    spec.ik_iters, spec.ik_seeds = 20, 8
+    a = TampContext(spec, 512)
+    b2 = TampContext(spec, 512)
+    ref = bench.run_round(a, 77, Args, None, 1)
+    ca = a.counts_buf.clone()
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(torch.cuda.current_stream())
+    b2.sample(77, stream=s2)
+    torch.cuda.current_stream().wait_stream(s2)
+    out = bench.run_round(b2, 77, Args, None, 1, sampled=True)
+    assert torch.equal(out, ref)
+    assert torch.equal(b2.counts_buf, ca)

@@ -2,7 +2,7 @@
 # particle-count sweep (BASELINE config 5 shape): bench value / kernel rate / TTFS per N on one GPU
 CFG=${1:-5}; shift
 for N in "$@"; do
-  python bench.py --config $CFG --n $N --steps 3 --warmup 2 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "
+  python bench.py --config $CFG --n $N --steps 3 --warmup 3 --repeats 1 --no-e2e --no-cpu-baseline --no-extra 2>&1 | tail -1 | python -c "
 import json,sys
 l=sys.stdin.read()
 try:
