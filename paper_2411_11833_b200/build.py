@@ -7,7 +7,7 @@ ROOT = os.path.dirname(HERE)
 # one translation unit per instantiation group so the (slow) k_particle variants compile in parallel
 SRCS = [os.path.join(HERE, "csrc", f) for f in ("tamp_api.cu", "tamp_kernels.cu", "tamp_particle_hinge.cu",
                                                  "tamp_particle_smooth.cu", "tamp_particle_serial.cu",
-                                                 "tamp_particle_hinge_rich.cu", "tamp_particle_hinge_wide.cu")]
+                                                 "tamp_particle_hinge_rich.cu", "tamp_particle_hinge_wide.cu", "tamp_particle_hinge_16.cu")]
 HDRS = [os.path.join(HERE, "csrc", "tamp_program.h"), os.path.join(HERE, "csrc", "particle.cuh"),
         os.path.join(HERE, "csrc", "particle_serial.cuh"), os.path.join(HERE, "csrc", "particle_launch.cuh"),
         os.path.join(ROOT, "include", "tamp.h")]
@@ -17,7 +17,7 @@ OBJ_DIR = os.path.join(HERE, "csrc", "build")
 # branches in the step loop; the parity tolerances (1e-4 relative cost) are orders of magnitude wider
 FAST_DIV_SQRT = ["-prec-div=false", "-prec-sqrt=false"]
 FAST_UNITS = ("tamp_particle_hinge.cu", "tamp_particle_smooth.cu", "tamp_particle_serial.cu", "tamp_kernels.cu",
-              "tamp_particle_hinge_rich.cu", "tamp_particle_hinge_wide.cu")
+              "tamp_particle_hinge_rich.cu", "tamp_particle_hinge_wide.cu", "tamp_particle_hinge_16.cu")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 

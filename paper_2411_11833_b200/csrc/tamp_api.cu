@@ -968,14 +968,14 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         const int ppw = 32 / c->gs;                                     // particles per warp
         const int static_smem = 4096 + 4 * c->const_floats;   // + block-shared constant instances
         // __launch_bounds__ of the variants: 8 lanes up to 1024 threads (hinge; 768 for the smooth cost), else 512
-        const int max_threads = c->gs == 8 ? (C.P.smooth > 0.f ? 768 : 1024) : 512;
+        const int max_threads = C.P.smooth > 0.f ? (c->gs == 8 ? 768 : 512) : (c->gs == 8 ? 1024 : (c->gs == 16 ? 768 : 512));
         int max_pp = std::min(max_threads / c->gs, (smem_optin - static_smem) / c->stride_bytes);
         max_pp = (max_pp / ppw) * ppw;
         if (desc->block_threads) {
             if (desc->block_threads % 32 || desc->block_threads < 32 || desc->block_threads > max_threads) {
                 delete c;
-                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024] for 8 lanes (768 with "
-                                            "the smooth cost; 512 for 4 / 16 lanes)");
+                return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024] for 8 lanes, 768 for 16 "
+                                            "lanes (768 / 512 with the smooth cost), 512 for 4 lanes");
             }
             c->threads = desc->block_threads;
         } else {

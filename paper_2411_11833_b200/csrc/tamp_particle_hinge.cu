@@ -10,10 +10,14 @@ int particle_regs_hinge_rich(int gs);
 cudaError_t launch_particle_hinge_wide(int mode, int bsync, int threads, const KProgram& P, const KArgs& A,
                                        size_t smem, cudaStream_t st);
 int particle_regs_hinge_wide(int threads);
+cudaError_t launch_particle_hinge_16(int mode, int bsync, int threads, const KProgram& P, const KArgs& A, size_t smem,
+                                     cudaStream_t st);
+int particle_regs_hinge_16();
 
 // 16 lanes, and 8 lanes in blocks of <= 512 threads: the 512-thread-bound (register-rich) instantiations
 cudaError_t launch_particle_hinge(int mode, int gs, int bsync, int threads, const KProgram& P, const KArgs& A,
                                   size_t smem, cudaStream_t st) {
+    if (gs == 16 && threads > 512) return launch_particle_hinge_16(mode, bsync, threads, P, A, smem, st);
     if (gs == 16 || (gs == 8 && threads <= 512)) return launch_particle_hinge_rich(mode, gs, bsync, threads, P, A, smem, st);
     if (gs == 4) return launch_particle_map<4, 1, false, 512>(mode, bsync, P, A, threads, smem, st);
     if (threads > 768) return launch_particle_hinge_wide(mode, bsync, threads, P, A, smem, st);
@@ -22,6 +26,7 @@ cudaError_t launch_particle_hinge(int mode, int gs, int bsync, int threads, cons
 
 // registers per thread of the variant a block of `threads` threads would run (launch-configuration policy)
 int particle_kernel_regs_sm(int gs, int threads) {
+    if (gs == 16 && threads > 512) return particle_regs_hinge_16();
     if (gs == 16 || (gs == 8 && threads <= 512)) return particle_regs_hinge_rich(gs);
     if (gs == 4) return particle_regs_t<4, 1, false, 512>();
     if (threads > 768) return particle_regs_hinge_wide(threads);
