@@ -25,6 +25,25 @@
 #define TAMP_PACK_NARROW 1
 #endif
 
+// TAMP_DEVICE_CHECKS=1 (tools/device_checks.sh): device-side bounds checks of the shared-memory carve-outs and the
+// program's indices, trapping with a message (compute-sanitizer is not available on the GPU pool)
+#ifndef TAMP_DEVICE_CHECKS
+#define TAMP_DEVICE_CHECKS 0
+#endif
+#if TAMP_DEVICE_CHECKS
+#include <cstdio>
+#define TAMP_DCHECK(c)                                                                                    \
+    do {                                                                                                  \
+        if (!(c)) {                                                                                       \
+            printf("TAMP_DCHECK failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__,          \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                    \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define TAMP_DCHECK(c) do { } while (0)
+#endif
+
 namespace tamp {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -729,8 +748,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     // centres (float4) | wrench (movable only)]; constant instances live once per block, movable ones per particle
     auto inst = [&](int i) -> float* {
         const KInst& I = P.inst[i];
+        TAMP_DCHECK(i >= 0 && i < P.n_inst && I.slot >= 0);
+        TAMP_DCHECK(I.xoff >= 0 ? A.off_inst + kInstFloats * (I.slot + 1) <= A.stride
+                                : kInstFloats * (I.slot + 1) <= A.const_floats);
         return (I.xoff >= 0 ? minst : cinst) + kInstFloats * I.slot;
     };
+    TAMP_DCHECK(A.const_floats + (grp + 1) * A.stride <= A.smem_floats);
+    TAMP_DCHECK(A.off_g + P.D <= A.stride && A.off_gT + 12 * P.n_grasp <= A.stride);
+    TAMP_DCHECK(A.off_gTi < 0 || A.off_gTi + 12 * P.n_grasp <= A.stride);
+    TAMP_DCHECK(!P.has_self || A.off_rsw + 4 * HP * kGroup * TAMP_MAX_SPHERES_PER_LINK <= A.stride);
     auto ipose = [&](int i) -> float* { return inst(i); };
     auto iwr = [&](int i) -> float* { return inst(i) + 48; };
     const int D = P.D;
@@ -830,6 +856,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         for (int i = 0; i < P.n_inst; ++i) {
             const KInst& I = P.inst[i];
             if (I.xoff < 0) continue;      // constant instances: set up once per block (prologue)
+            TAMP_DCHECK(I.xoff + 4 <= D);
             const float px = xs[I.xoff], py = xs[I.xoff + 1], pz = xs[I.xoff + 2], yaw = xs[I.xoff + 3];
             float sy, cy;
             fsincos(yaw, &sy, &cy);
@@ -866,6 +893,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         for (int f0 = 0; f0 < P.n_fk; f0 += HP) {
             const KFk K = P.fk[f0 + (HP > 1 ? half : 0)];
             const bool real = !K.ghost;
+            TAMP_DCHECK(f0 + HP <= TAMP_MAX_FK && K.xoff >= 0 && K.xoff + TAMP_NJ <= D);
+            TAMP_DCHECK(K.part_begin >= 0 && K.part_begin + K.part_count <= kMaxPartners);
+            TAMP_DCHECK(K.kin_grasp < P.n_grasp && K.held_grasp < P.n_grasp);
             if (HP == 1 && !real) continue;
             // A_j = F_j Rz(q_j) for my joints, local product, product scan over the LPF lanes (FK)
             float q[LPL];

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     // per-thread state rows (odd pitch: a warp reading one field of its 32 rows is conflict-free); every field
     // access is my row base + a warp-uniform offset
     const int ROWP = serial_row_pitch(L);
+    TAMP_DCHECK((tid + 1) * ROWP <= A.smem_floats);
     float* const Sr = S + tid * ROWP;
     auto col = [&](int f) -> float& { return Sr[f]; };
     // block-cooperative, coalesced copy between the block's rows of a [n][w] array and fields c0..c0+w of the rows
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         for (int f = 0; f < P.n_fk; ++f) {
             const KFk K = P.fk[f];
             if (K.ghost) continue;
+            TAMP_DCHECK(K.xoff >= 0 && K.xoff + TAMP_NJ <= D && K.part_begin + K.part_count <= kMaxPartners);
             float q[TAMP_NJ], sq[TAMP_NJ], cq[TAMP_NJ];
 #pragma unroll
             for (int j = 0; j < TAMP_NJ; ++j) {

@@ -812,6 +812,7 @@ static KArgs base_args(tamp_ctx* c) {
     A.off_gTi = c->off_gTi;
     A.off_rsw = c->off_rsw;
     A.bsync = c->gs == 1 ? c->bsync : 0;
+    A.smem_floats = (int32_t)(c->smem / sizeof(float));
     return A;
 }
 

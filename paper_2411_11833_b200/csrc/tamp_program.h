@@ -142,6 +142,7 @@ struct KArgs {
     int32_t n_steps, t0;
     int32_t bsync;         // serial mapping: block barriers per configuration / phase (shared i-cache)
     int32_t check_after;   // MODE_OPT: run the Eq. 3 check of the final state in the same launch
+    int32_t smem_floats;   // dynamic shared memory of the launch (device-check builds verify every carve-out)
     // reciprocal Adam bias corrections 1 / (1 - beta^t) for the (<= kMaxStepsPerLaunch) steps of this launch,
     // computed on the host in double precision
     float rbc1[64], rbc2[64];
