@@ -304,7 +304,17 @@ __device__ __forceinline__ float sphere_sphere(float ax, float ay, float az, flo
 }
 
 constexpr float kFar = 1e18f;   // position of padded (absent) spheres: never within reach of anything
-constexpr float kBroadMaxRad = 0.5f;   // OBBs with a larger bounding sphere skip the broad phase and pre-test
+// OBBs whose bounding sphere is at least this large skip the bounding-sphere broad phase.  0: no box uses it -- with
+// the packed exact reject test (about 6 issued instructions per sphere) a thin wall's bounding sphere passed for
+// two thirds of the tests and only added work (config 3: 1.89 -> 1.85 ms per launch, profiles/README.md)
+#ifndef TAMP_BROAD_MAX_RAD
+#define TAMP_BROAD_MAX_RAD 0.0f
+#endif
+constexpr float kBroadMaxRad = TAMP_BROAD_MAX_RAD;
+#ifndef TAMP_NARROW_UNROLL
+#define TAMP_NARROW_UNROLL 2
+#endif
+constexpr int kNarrowUnroll = TAMP_NARROW_UNROLL;     // unrolling of the partner-sphere loop of the pair tests
 
 // ------------------------------------------------------------------------------------------------
 // packed fp32x2 arithmetic: FADD2 / FMUL2 / FFMA2 of sm_100a do two IEEE fp32 operations (round to nearest, each
@@ -491,7 +501,7 @@ __device__ __forceinline__ void instance_pair_tests(const QSet<NS>& q, const flo
             on(0, b + 1, hi(t));
         }
     } else {
-#pragma unroll 2
+#pragma unroll kNarrowUnroll
         for (int b = 0; b < TAMP_MAX_OBJ_SPHERES; ++b) {
             const F2 bx = bc(X[b]), by = bc(X[8 + b]), bz = bc(X[16 + b]);
             const float br = X[24 + b];
