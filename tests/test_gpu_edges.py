@@ -155,3 +155,31 @@ def test_tilted_boxes_cost_gradient_and_step(cfg, lanes):
     unstable = np.abs(grado) < 1e-4 * np.abs(grado).max(axis=1, keepdims=True)
     close = np.abs(x1 - so.x) <= STEP_RTOL * (np.abs(so.x) + csp.lr[None, :])
     assert np.all(close | unstable | kinks[:, None])
+
+
+def test_bench_json_line_contract():
+    """bench.py (a short run) prints one JSON line with the driver's keys: metric / value / unit / n_gpus / steps /
+    warmup / ms_per_step / higher_is_better / scaling / dtype / data / config.workload, plus roofline (bound,
+    achieved, peak, unit, frac, traffic), e2e (value, unit, h2d / d2h bytes), gpu_launches > 0, clocks, repeats."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "1", "--n", "512", "--steps", "2",
+                        "--warmup", "3", "--repeats", "2", "--no-extra", "--no-cpu-baseline", "--no-ttfs"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks", "repeats"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["config"]["workload"].startswith("config1")
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert len(d["repeats"]["values"]) == 2
