@@ -635,6 +635,15 @@ def main():
             extra.append(extra_workload(args, ecfg, en, dist, world, rank, dev, flush, side, self_collision=eself))
 
     tt = None if args.no_ttfs else ttfs(ctx, args, dist, world, seed=1000 * cfg)
+    # TTFS of config 4 at its global batch (131,072 particles, BASELINE.json: 8 GPUs x 16,384), split over the ranks
+    tt_extra = []
+    if not args.no_ttfs and not args.no_extra and cfg != 4:
+        n4 = 131072 // world
+        ctx4 = TampContext(make_spec(args, 4, n4), n4, global_offset=rank * n4, n_global=n4 * world, device=dev)
+        t4 = ttfs(ctx4, args, dist, world, seed=4000)
+        t4.update({"workload": f"config4:{CONFIG_NAMES[4]}", "particles_global": n4 * world, "particles_per_gpu": n4})
+        tt_extra.append(t4)
+        del ctx4
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # the oracle leg re-checks parity on the bench context: bring it back to the timed rounds' state
@@ -659,7 +668,8 @@ def main():
                 "kernel_launch": "check_every fused Adam steps + the Eq. 3 check of the final state",
                 "kernel_particle_steps_per_s": n_global * args.check_every / opt_avg,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "ttfs": tt, "extra": extra, "lib": os.path.relpath(lib_path(), ROOT),
+                "clocks": clocks, "ttfs": tt, "ttfs_extra": tt_extra, "extra": extra,
+                "lib": os.path.relpath(lib_path(), ROOT),
                 "scaling_note": "weak scaling (particles per GPU fixed); no multi-GPU curve exists until a driver "
                                 "SCALE run" if world == 1 else "weak scaling, max over ranks"}
         print(json.dumps(line), flush=True)
