@@ -24,6 +24,10 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_FUNNEL_MASK        // active-pair masks built with one funnel shift per pair (instance_pair_tests)
+#define TAMP_FUNNEL_MASK 1
+#endif
+static_assert(TAMP_MAX_OBJ_SPHERES <= 32, "active-pair masks hold one bit per partner sphere");
 
 // TAMP_DEVICE_CHECKS=1 (tools/device_checks.sh): device-side bounds checks of the shared-memory carve-outs and the
 // program's indices, trapping with a message (compute-sanitizer is not available on the GPU pool)
@@ -525,7 +529,13 @@ __device__ __forceinline__ float pairs_vs_instance(const QSet<NS>& q, const floa
     uint32_t act[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) act[k] = 0u;
+#if TAMP_FUNNEL_MASK
+    // (funnel shift: act[k] = act[k] << 1 | sign(t), one SHF per pair; the pairs arrive in ascending b, so pair b
+    // ends at bit 7 - b and the highest set bit is the lowest b)
+    instance_pair_tests(q, X, [&](int k, int b, float t) { act[k] = __funnelshift_l(__float_as_uint(t), act[k], 1); });
+#else
     instance_pair_tests(q, X, [&](int k, int b, float t) { act[k] |= (__float_as_uint(t) >> 31) << b; });
+#endif
     uint32_t any = 0u;
 #pragma unroll
     for (int k = 0; k < NS; ++k) any |= act[k];
@@ -538,8 +548,14 @@ __device__ __forceinline__ float pairs_vs_instance(const QSet<NS>& q, const floa
     for (int k = 0; k < NS; ++k) {
         uint32_t m = act[k];
         while (m) {
+#if TAMP_FUNNEL_MASK
+            const int hb = 31 - __clz(m);
+            m ^= 1u << hb;
+            const int b = (TAMP_MAX_OBJ_SPHERES - 1) - hb;
+#else
             const int b = __ffs(m) - 1;
             m &= m - 1u;
+#endif
             const float4 B = make_float4(X[b], X[8 + b], X[16 + b], X[24 + b]);
             float ux, uy, uz;
             j += sphere_sphere<GRAD>(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B, lam, ux, uy, uz, smooth);
@@ -999,6 +1015,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             // exact reject test, its sign bits ANDed with the pair mask -- and evaluates the exact hinges of the
             // active pairs, keeping only its own spheres' gradient; each pair's hinge is counted once, by the lower
             // sphere id
+            static_assert(kGroup * TAMP_MAX_SPHERES_PER_LINK == 32, "self-pair masks: one bit per robot sphere");
             if (K.term_self >= 0) {
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
@@ -1016,17 +1033,30 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     for (int j = 0; j < QSet<NS>::NP; ++j) {
                         const F2 tt = reach2(sub2(rs.x[j], bc(B.x)), sub2(rs.y[j], bc(B.y)), sub2(rs.z[j], bc(B.z)),
                                              rs.r[j], B.w);
+#if TAMP_FUNNEL_MASK                // (pair t ends at bit 31 - t: the pair mask is bit-reversed to match)
+                        sact[2 * j] = __funnelshift_l(__float_as_uint(lo(tt)), sact[2 * j], 1);
+                        if (2 * j + 1 < NS) sact[2 * j + 1] = __funnelshift_l(__float_as_uint(hi(tt)), sact[2 * j + 1], 1);
+#else
                         sact[2 * j] |= (__float_as_uint(lo(tt)) >> 31) << t;
                         if (2 * j + 1 < NS) sact[2 * j + 1] |= (__float_as_uint(hi(tt)) >> 31) << t;
+#endif
                     }
                 }
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {
                     const int sid = ll * NS + s;
+#if TAMP_FUNNEL_MASK
+                    uint32_t m = __brev(s_selfmask[sid]) & sact[s];
+                    while (m) {
+                        const int hb = 31 - __clz(m);
+                        m ^= 1u << hb;
+                        const int t = 31 - hb;
+#else
                     uint32_t m = s_selfmask[sid] & sact[s];
                     while (m) {
                         const int t = __ffs(m) - 1;
                         m &= m - 1u;
+#endif
                         float ux, uy, uz;
                         const float pen = sphere_sphere<G>(rs.sx(s), rs.sy(s), rs.sz(s), rs.sr(s), rsw[t], lam_self, ux, uy,
                                                               uz, smooth);
