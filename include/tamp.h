@@ -107,7 +107,8 @@ typedef struct {
 
 /* static oriented box ("oriented bounding boxes"): centre, half extents > 0 and its orientation:
    rot = the box-to-world rotation (3x3, row-major; must be orthonormal with det +1 to 1e-4, else TAMP_E_INVALID),
-   or all nine entries 0: the rotation Rz(yaw) about the world z axis */
+   or all nine entries 0: the rotation Rz(yaw) about the world z axis.  |center_k| + half_k <= 100 m
+   (TAMP_E_UNSUPPORTED beyond: the kernels' conservative reject test is sized for fp32 rounding at that scale) */
 typedef struct { float center[3]; float yaw; float half[3]; float rot[9]; } tamp_obb_desc;
 
 /* movable object as spheres in its frame (origin = bottom centre, L15); sampler parameters:

@@ -24,6 +24,9 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_BOX_CORNER         // aligned boxes: the conservative corner-form reject test (obb_reach_corner_pair)
+#define TAMP_BOX_CORNER 1
+#endif
 #ifndef TAMP_FUNNEL_MASK        // active-pair masks built with one funnel shift per pair (instance_pair_tests)
 #define TAMP_FUNNEL_MASK 1
 #endif
@@ -588,6 +591,23 @@ __device__ __forceinline__ void obb_reach_pair(F2 px, F2 py, F2 pz, F2 r, const 
     h0 = !(lo(s4) >= lo(r4));
     h1 = !(hi(s4) >= hi(r4));
 }
+// Conservative reject test for an axis-aligned box on the sphere centres themselves: per axis
+// q = max(w - hi, lo - w, 0) (one FADD2 per corner, a 3-input max) with the corners grown by kCornerSlack, so that
+// q <= the exact test's max(|w - c| - h, 0) whatever the fp32 rounding (|coordinates| <= kMaxCoord): a sphere this
+// test rejects (||q||^2 >= r^2) is rejected by sphere_obb too; the few it keeps within the slack are evaluated
+// exactly (zero hinge).  Results are unchanged.
+__device__ __forceinline__ void obb_reach_corner_pair(F2 x, F2 y, F2 z, F2 r, const KObb& B, bool& h0, bool& h1) {
+    const F2 ux = sub2(x, bc(B.hi[0])), vx = sub2(bc(B.lo[0]), x);
+    const F2 uy = sub2(y, bc(B.hi[1])), vy = sub2(bc(B.lo[1]), y);
+    const F2 uz = sub2(z, bc(B.hi[2])), vz = sub2(bc(B.lo[2]), z);
+    const F2 qx = pk(fmaxf(fmaxf(lo(ux), lo(vx)), 0.f), fmaxf(fmaxf(hi(ux), hi(vx)), 0.f));
+    const F2 qy = pk(fmaxf(fmaxf(lo(uy), lo(vy)), 0.f), fmaxf(fmaxf(hi(uy), hi(vy)), 0.f));
+    const F2 qz = pk(fmaxf(fmaxf(lo(uz), lo(vz)), 0.f), fmaxf(fmaxf(hi(uz), hi(vz)), 0.f));
+    const F2 s = fma2(qx, qx, fma2(qy, qy, mul2(qz, qz)));
+    const F2 r2 = mul2(r, r);
+    h0 = !(lo(s) >= lo(r2));
+    h1 = !(hi(s) >= hi(r2));
+}
 // box-frame offsets p = R^T (w - c) of a packed pair of points (aligned boxes: the offsets themselves)
 __device__ __forceinline__ void obb_offsets_pair(F2 x, F2 y, F2 z, const KObb& B, F2& px, F2& py, F2& pz) {
     const F2 dx = sub2(x, bc(B.c[0])), dy = sub2(y, bc(B.c[1])), dz = sub2(z, bc(B.c[2]));
@@ -617,6 +637,18 @@ __device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B
         for (int k = 0; k < NS; ++k) {
             hit[k] = obb_within(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B);
             any = any || hit[k];
+        }
+    } else if (TAMP_BOX_CORNER && TAMP_PACK_OBB == 1 && B.aligned) {
+#pragma unroll
+        for (int j = 0; j < QSet<NS>::NP; ++j) {
+            bool h0, h1;
+            obb_reach_corner_pair(q.x[j], q.y[j], q.z[j], q.r[j], B, h0, h1);
+            hit[2 * j] = h0;
+            any = any || h0;
+            if (2 * j + 1 < NS) {
+                hit[2 * j + 1] = h1;
+                any = any || h1;
+            }
         }
     } else {
 #pragma unroll

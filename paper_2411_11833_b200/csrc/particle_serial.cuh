@@ -356,10 +356,14 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         const F2 wx = fma2(bc(T.r(0, 0)), cx, fma2(bc(T.r(0, 1)), cy, fma2(bc(T.r(0, 2)), cz, bc(T.t(0)))));
                         const F2 wy = fma2(bc(T.r(1, 0)), cx, fma2(bc(T.r(1, 1)), cy, fma2(bc(T.r(1, 2)), cz, bc(T.t(1)))));
                         const F2 wz = fma2(bc(T.r(2, 0)), cx, fma2(bc(T.r(2, 1)), cy, fma2(bc(T.r(2, 2)), cz, bc(T.t(2)))));
-                        F2 px, py, pz;
-                        obb_offsets_pair(wx, wy, wz, B0, px, py, pz);
                         bool h0, h1;
-                        obb_reach_pair(px, py, pz, cr, B0, h0, h1);
+                        if (TAMP_BOX_CORNER && B0.aligned) {
+                            obb_reach_corner_pair(wx, wy, wz, cr, B0, h0, h1);
+                        } else {
+                            F2 px, py, pz;
+                            obb_offsets_pair(wx, wy, wz, B0, px, py, pz);
+                            obb_reach_pair(px, py, pz, cr, B0, h0, h1);
+                        }
                         const int k = 2 * kp;
                         wq[k][0] = lo(wx); wq[k][1] = lo(wy); wq[k][2] = lo(wz); rq[k] = lo(cr);
                         wq[k + 1][0] = hi(wx); wq[k + 1][1] = hi(wy); wq[k + 1][2] = hi(wz); rq[k + 1] = hi(cr);

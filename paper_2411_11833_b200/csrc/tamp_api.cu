@@ -347,6 +347,12 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             B.aligned &= B.R[k] == ((k % 4 == 0) ? 1.f : 0.f);
         }
         for (int k = 0; k < 3; ++k) { B.c[k] = o.center[k]; B.h[k] = o.half[k]; }
+        for (int k = 0; k < 3; ++k) {
+            REQUIRE(std::fabs((double)o.center[k]) + o.half[k] <= kMaxCoord, TAMP_E_UNSUPPORTED,
+                    "OBB extents beyond 100 m of the origin");
+            B.lo[k] = std::nextafter((float)((double)B.c[k] - B.h[k] - kCornerSlack), -INFINITY);
+            B.hi[k] = std::nextafter((float)((double)B.c[k] + B.h[k] + kCornerSlack), INFINITY);
+        }
         B.rad = (float)(std::sqrt((double)o.half[0] * o.half[0] + (double)o.half[1] * o.half[1] +
                                   (double)o.half[2] * o.half[2]) * (1.0 + 1e-6));
     }

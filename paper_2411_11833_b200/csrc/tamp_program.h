@@ -66,7 +66,10 @@ struct KObb {                          // oriented box: world pose R (r
     float h[3];
     float rad;                         // |h|: bounding-sphere radius
     int32_t aligned;                   // R is exactly the identity (axis-aligned fast path)
+    float lo[3], hi[3];                // aligned boxes: corners c -/+ h grown by kCornerSlack (conservative reject test)
 };
+constexpr double kCornerSlack = 2e-5;  // m: >> the fp32 rounding of w - c - h at |coordinates| <= kMaxCoord
+constexpr double kMaxCoord = 100.0;
 
 struct KProgram {
     int32_t D, n_terms, n_fk, n_inst, n_place, n_traj, n_goal, n_grasp, n_obb;

@@ -183,3 +183,45 @@ def test_bench_json_line_contract():
     for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
         assert k in d["e2e"], k
     assert len(d["repeats"]["values"]) == 2
+
+
+@pytest.mark.parametrize("lanes,single_box", [(8, False), (8, True), (1, True)])
+def test_box_reject_at_reach_boundary(lanes, single_box):
+    """The kernels skip a sphere's exact box test when a cheaper reject test says it cannot reach the box (for
+    axis-aligned boxes: the corner form with grown corners, obb_reach_corner_pair).  A small axis-aligned box is
+    placed against the robot sphere that reaches farthest along +x at the pick configuration, so that the sphere
+    penetrates it by d in {3e-5, 1e-5, 2e-6, 0, -2e-6, -1e-5} m: the CF hinge of that configuration equals the
+    oracle's (which grows by d for d > 0) to 2e-7.  single_box: the box is the only one (the serial mapping's
+    one-box path; the region then has no support box)."""
+    from workloads.scenes import OBB
+    from workloads.scenes import _f32
+    base = make_config(1, n=1)
+    csp0 = O.build_csp(base)
+    x, g = O.initialize_particles(base, csp0, 5, np.arange(1))
+    i_cf = [i for i, t in enumerate(csp0.terms) if t.kind == "CF"][0]
+    qo = csp0.offsets[csp0.terms[i_cf].conf[1]]       # conf = ("var", variable index)
+    q = torch.tensor(x[:, qo:qo + 7])
+    W = O.robot_sphere_centers(base.robot, O.forward_kinematics(base.robot, q))[0].numpy()
+    r = base.robot.spheres[:, 3] + base.eta
+    s = int(np.argmax(W[:, 0] + r))
+    vals = []
+    for d in (3e-5, 1e-5, 2e-6, 0.0, -2e-6, -1e-5):
+        spec = copy.deepcopy(base)
+        h = 0.01
+        box = _f32(OBB(np.array([W[s, 0] + r[s] - d + h, W[s, 1], W[s, 2]]), 0.0, np.array([h, h, h]), "probe"))
+        if single_box:
+            spec.obbs = [box]
+            for sf in spec.surfaces:
+                sf.support_obb = -1
+        else:
+            spec.obbs = spec.obbs + [box]
+        csp = O.build_csp(spec)
+        x32, g32 = x.astype(np.float32), g.astype(np.float32)
+        ctx = TampContext(spec, 1, lanes_per_particle=lanes)
+        ctx.set_state(torch.from_numpy(x32).cuda(), grasp=to_ctx_grasp(g32).cuda())
+        _, _, Jc, _ = (t.cpu().numpy() for t in ctx.eval())
+        _, Jco, _, _ = O.cost_and_grad(spec, csp, x32.astype(np.float64), g32.astype(np.float64))
+        np.testing.assert_allclose(Jc[0, i_cf], Jco[0, i_cf], rtol=1e-5, atol=2e-7)
+        vals.append(Jco[0, i_cf])
+    # the construction works: the oracle's hinge grows with the penetration (by 2e-5 from d = 1e-5 to 3e-5)
+    assert abs((vals[0] - vals[1]) - 2e-5) < 2e-6 and vals[1] > vals[2] > vals[3] - 1e-9

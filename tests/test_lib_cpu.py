@@ -139,3 +139,16 @@ def test_obb_rotation_validated(lib):
     for k, v in enumerate([-1, 0, 0, 0, 1, 0, 0, 0, 1]):       # det -1
         d.obb[0].rot[k] = v
     assert _query(lib, d, 10)[0] == 1
+
+
+def test_obb_extent_bound(lib):
+    """Boxes must lie within 100 m of the origin (|c_k| + h_k <= 100): the kernels' reject test for axis-aligned
+    boxes grows the corners by 2e-5 m, which covers fp32 rounding only up to that scale (TAMP_E_UNSUPPORTED = 5
+    beyond, include/tamp.h)."""
+    spec = make_config(1, n=4)
+    d = T.build_desc(spec)
+    d.obb[0].center[0] = 99.0
+    assert _query(lib, d, 10)[0] == 0
+    d.obb[0].center[0] = 101.0
+    st, _, msg = _query(lib, d, 10)
+    assert st == 5 and "100 m" in msg
