@@ -144,6 +144,19 @@ __device__ __forceinline__ float gsum(float v) {      // butterfly sum over the 
     return v;
 }
 
+// MUFU approximations without the denormal rescaling of sqrtf / division under -prec-sqrt=false / -prec-div=false
+// (inputs here are >= 0 Adam second moments and sums >= adam_eps > 0)
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // sin/cos without the large-argument (Payne-Hanek) path of sincosf: Cody-Waite reduction by pi/2 with a
 // three-part constant (exact for |x| < ~1e4; joint angles and yaws are within a few radians) and the
 // cephes single-precision minimax polynomials on [-pi/4, pi/4] (<= 2 ulp).  Branch-free and compact, so
@@ -431,6 +444,46 @@ __device__ __forceinline__ M34P shfl_up_m34p(const M34P& a, int d, int width) {
     o.t01 = pk(__shfl_up_sync(FULL, lo(a.t01), d, width), __shfl_up_sync(FULL, hi(a.t01), d, width));
     o.t2 = __shfl_up_sync(FULL, a.t2, d, width);
     return o;
+}
+// Modified-DH link step on the packed frame (columns X = (r01[0], r2[0]), Y, Z, origin o):
+// T_j = T_{j-1} Rx(alpha) Tx(a) Tz(d) Rz(q) with dh = (a, d, cos alpha, sin alpha) and (c, s) = (cos q, sin q):
+//   Y1 = ca Y + sa Z,  Z1 = -sa Y + ca Z,  o1 = o + a X + d Z1,  X2 = c X + s Y1,  Y2 = -s X + c Y1
+// (20 issued instructions instead of building F Rz(q) and a 3x4 compose)
+__device__ __forceinline__ void dh_fwd(M34P& T, const float* dh, float c, float s) {
+    const float a = dh[0], d = dh[1], ca = dh[2], sa = dh[3];
+    const F2 Y1 = fma2(bc(sa), T.r01[2], mul2(bc(ca), T.r01[1]));
+    const F2 Z1 = fma2(bc(ca), T.r01[2], mul2(bc(-sa), T.r01[1]));
+    const float y1 = fmaf(sa, T.r2[2], ca * T.r2[1]);
+    const float z1 = fmaf(ca, T.r2[2], -sa * T.r2[1]);
+    T.t01 = fma2(bc(d), Z1, fma2(bc(a), T.r01[0], T.t01));
+    T.t2 = fmaf(d, z1, fmaf(a, T.r2[0], T.t2));
+    const F2 X = T.r01[0];
+    const float x = T.r2[0];
+    T.r01[0] = fma2(bc(s), Y1, mul2(bc(c), X));
+    T.r01[1] = fma2(bc(c), Y1, mul2(bc(-s), X));
+    T.r01[2] = Z1;
+    T.r2[0] = fmaf(s, y1, c * x);
+    T.r2[1] = fmaf(c, y1, -s * x);
+    T.r2[2] = z1;
+}
+// its inverse: T_{j-1} = T_j Rz(-q) Tz(-d) Tx(-a) Rx(-alpha):
+//   X = c X2 - s Y2,  Y1 = s X2 + c Y2,  o = o1 - a X - d Z1,  Y = ca Y1 - sa Z1,  Z = sa Y1 + ca Z1
+__device__ __forceinline__ void dh_bwd(M34P& T, const float* dh, float c, float s) {
+    const float a = dh[0], d = dh[1], ca = dh[2], sa = dh[3];
+    const F2 X = fma2(bc(c), T.r01[0], mul2(bc(-s), T.r01[1]));
+    const F2 Y1 = fma2(bc(s), T.r01[0], mul2(bc(c), T.r01[1]));
+    const float x = fmaf(c, T.r2[0], -s * T.r2[1]);
+    const float y1 = fmaf(s, T.r2[0], c * T.r2[1]);
+    T.t01 = fma2(bc(-d), T.r01[2], fma2(bc(-a), X, T.t01));
+    T.t2 = fmaf(-d, T.r2[2], fmaf(-a, x, T.t2));
+    const F2 Z1 = T.r01[2];
+    const float z1 = T.r2[2];
+    T.r01[0] = X;
+    T.r01[1] = fma2(bc(-sa), Z1, mul2(bc(ca), Y1));
+    T.r01[2] = fma2(bc(ca), Z1, mul2(bc(sa), Y1));
+    T.r2[0] = x;
+    T.r2[1] = fmaf(-sa, z1, ca * y1);
+    T.r2[2] = fmaf(ca, z1, sa * y1);
 }
 __device__ __forceinline__ void xform_p(const M34P& T, float x, float y, float z, float& ox, float& oy, float& oz) {
     const F2 o = fma2(T.r01[0], bc(x), fma2(T.r01[1], bc(y), fma2(T.r01[2], bc(z), T.t01)));

@@ -43,8 +43,9 @@ constexpr int kSerialThreads = 512;   // launch bound (blocks of <= 512 threads,
 __host__ __device__ inline int serial_row_pitch(const SerialLayout& L) { return L.n | 1; }
 
 // dynamic shared memory of a serial-mapping block of `threads` particles (one row per thread)
+// (+ the Adam step sizes and bounds lr, lo, hi of the D coordinates once per block in optimisation mode)
 __host__ __device__ inline size_t serial_smem_bytes(const KProgram& P, int threads, bool mv) {
-    return (size_t)serial_row_pitch(serial_layout(P, mv)) * threads * sizeof(float);
+    return ((size_t)serial_row_pitch(serial_layout(P, mv)) * threads + (mv ? 3 * P.D : 0)) * sizeof(float);
 }
 
 // term bookkeeping: warp-aggregated counts (every thread of the warp calls it for the same term)
@@ -62,7 +63,23 @@ __device__ __forceinline__ void serial_term(const KProgram& P, const KArgs& A, T
     }
 }
 
-template <int MODE, bool SMOOTH>
+// Is the program of the pick-place class (PP): every configuration's robot collision is against at most one box and
+// no partner instances (config 1)?  Then k_serial<.., PP = true> unrolls the link sweep (the per-link robot data
+// become constant-bank operands: no indexed constant loads or loop control) and keeps only the packed one-box path.
+__host__ __device__ inline bool serial_program_pp(const KProgram& P) {
+    for (int f = 0; f < P.n_fk; ++f) {
+        const KFk& K = P.fk[f];
+        if (K.ghost || K.term_cf < 0) continue;
+        if (K.part_count != 0 || (K.obb_mask & (K.obb_mask - 1)) != 0) return false;
+    }
+    return true;
+}
+
+#ifndef TAMP_SERIAL_LINK_BROAD     // PP sweep: gate each link's packed sphere tests by its bounding sphere
+#define TAMP_SERIAL_LINK_BROAD 1
+#endif
+
+template <int MODE, bool SMOOTH, bool PP>
 __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     const float smooth = SMOOTH ? P.smooth : 0.f;
@@ -136,6 +153,10 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         load_rows(A.v, D, L.v);
     }
     if (P.n_grasp) load_rows(A.grasp, 12 * P.n_grasp, L.gT);
+    // Adam step sizes and bounds: per-coordinate, the same for every particle (broadcast shared-memory reads)
+    float* const s_lr = S + NT * ROWP;
+    if (MODE == MODE_OPT)
+        for (int i = tid; i < 3 * D; i += NT) s_lr[i] = i < D ? A.lr[i] : (i < 2 * D ? A.lo[i - D] : A.hi[i - 2 * D]);
     bool invalid = A.invalid[p] != 0;
     __syncthreads();
 
@@ -227,20 +248,22 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             }
             // forward: T_{j+1} = T_j F_{j+1} Rz(q_{j+1}) (base folded into F_1), tool T_8 = T_7 F_ee; T keeps its
             // rows 0-1 packed (M34P: FFMA2 compose, the scalar compose's values)
+            // (joints 2..7 as modified-DH steps on the packed frame, dh_fwd; joint 1's F also carries the base)
             M34P T;
-#pragma unroll
-            for (int j = 0; j < TAMP_NJ; ++j) {
-                M34 Aj;
+            {
+                M34 A0;
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    const float* Fr = P.F[j] + 4 * i;
-                    Aj.r[3 * i] = fmaf(Fr[0], cq[j], Fr[1] * sq[j]);
-                    Aj.r[3 * i + 1] = fmaf(Fr[1], cq[j], -Fr[0] * sq[j]);
-                    Aj.r[3 * i + 2] = Fr[2];
-                    Aj.t[i] = Fr[3];
+                    const float* Fr = P.F[0] + 4 * i;
+                    A0.r[3 * i] = fmaf(Fr[0], cq[0], Fr[1] * sq[0]);
+                    A0.r[3 * i + 1] = fmaf(Fr[1], cq[0], -Fr[0] * sq[0]);
+                    A0.r[3 * i + 2] = Fr[2];
+                    A0.t[i] = Fr[3];
                 }
-                T = j == 0 ? pack_m34(Aj) : compose_p(T, Aj);
+                T = pack_m34(A0);
             }
+#pragma unroll
+            for (int j = 1; j < TAMP_NJ; ++j) dh_fwd(T, P.dh[j], cq[j], sq[j]);
             {
                 M34 Fe;
                 load_m34(Fe, P.F[kGroup - 1]);
@@ -305,7 +328,6 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                 jl = sqrtf(e2);
                 serial_term<M>(P, A, sink, K.term_jl, jl, active, p, s_counts);
             }
-            (void)sq; (void)cq;
             // backward sweep over the links 8 -> 1: spheres of link l in T_l, suffix wrench, dJ/dq_l
             const float lam_cf = K.term_cf >= 0 ? P.term_lam[K.term_cf] : 0.f;
             float jcf = 0.f;
@@ -313,13 +335,22 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             const bool one_obb = K.obb_mask != 0 && (K.obb_mask & (K.obb_mask - 1)) == 0;
             KObb B0;
             if (one_obb) B0 = P.obb[__ffs(K.obb_mask) - 1];
-#pragma unroll 1
+            // PP: the sweep unrolled (per-link data as constant-bank operands), only the packed one-box path
+#pragma unroll (PP ? kGroup : 1)
             for (int l = kGroup - 1; l >= 0; --l) {
                 // link broad phase (conservative, results unchanged): the link's bounding sphere against the
                 // boxes and the partner instances' bounding spheres; a link that reaches none of them has only
                 // zero hinges and zero gradients, so its spheres are skipped
                 bool near = K.term_cf >= 0 && P.rsph_n[l] > 0;
-                if (near) {
+                if (PP) {
+                    near = near && one_obb;
+                    if (TAMP_SERIAL_LINK_BROAD && near) {
+                        const float* lb = P.lbound[l];
+                        float bx, by, bz;
+                        xform_p(T, lb[0], lb[1], lb[2], bx, by, bz);
+                        near = obb_within(bx, by, bz, lb[3] + P.eta + kLinkMargin, B0);
+                    }
+                } else if (near) {
                     const float* lb = P.lbound[l];
                     float bx, by, bz;
                     xform_p(T, lb[0], lb[1], lb[2], bx, by, bz);
@@ -338,7 +369,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         near = fmaf(-R, R, fmaf(dx, dx, fmaf(dy, dy, dz * dz))) < 0.f;
                     }
                 }
-                if (near && one_obb && K.part_count == 0) {
+                if (near && (PP || (one_obb && K.part_count == 0))) {
                     // one box, no partner instances (pick-place): the exact reject test of all of the link's
                     // spheres first (straight-line code, independent chains), hinges and gradients only for those
                     // that reach the box -- the others add exact zeros, so the result is unchanged
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         jcf += sphere_obb<G>(wq[k][0], wq[k][1], wq[k][2], rq[k], B0, lam_cf, g[0], g[1], g[2], smooth);
                         if (G) sfx.add_point(wq[k][0], wq[k][1], wq[k][2], g[0], g[1], g[2]);
                     }
-                } else if (near) {
+                } else if (!PP && near) {
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
                         const float4 c4 = s_rsph[l][k];
                         float wx, wy, wz;
@@ -422,19 +453,16 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     }
                 }
                 if (l > 0) {           // T_{l} -> T_{l-1}: right-multiply by (F_l Rz(q_l))^-1 = Rz(-q_l) F_l^-1
-                    if (l < TAMP_NJ) {
+                    if (l < TAMP_NJ) {   // a modified-DH joint (dh_bwd); PP: the forward pass's sin / cos
                         float sl, cl;
-                        fsincos(xs(K.xoff + l), &sl, &cl);
-                        const F2 a = T.r01[0], b = T.r01[1];
-                        T.r01[0] = fma2(a, bc(cl), mul2(b, bc(-sl)));
-                        T.r01[1] = fma2(a, bc(sl), mul2(b, bc(cl)));
-                        const float a2 = T.r2[0], b2 = T.r2[1];
-                        T.r2[0] = fmaf(a2, cl, -b2 * sl);
-                        T.r2[1] = fmaf(a2, sl, b2 * cl);
+                        if constexpr (PP) { sl = sq[l]; cl = cq[l]; }
+                        else fsincos(xs(K.xoff + l), &sl, &cl);
+                        dh_bwd(T, P.dh[l], cl, sl);
+                    } else {             // the tool frame
+                        M34 Fi;
+                        load_m34(Fi, P.Finv[l]);
+                        T = compose_p(T, Fi);
                     }
-                    M34 Fi;
-                    load_m34(Fi, P.Finv[l]);
-                    T = compose_p(T, Fi);
                 }
             }
             if (K.term_cf >= 0) serial_term<M>(P, A, sink, K.term_cf, jcf, active, p, s_counts);
@@ -610,12 +638,15 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             }
         } else {
             // ---- Adam (Kingma & Ba) with grad scale 1/N (Eq. 4) + projection (L11) ----
-            bool bad = !isfinite(Jtot);
-            for (int d = 0; d < D; ++d) bad |= !isfinite(gs(d));
-            invalid = invalid || bad;
+            // non-finite cost or gradient: g * 0 is 0 for finite g and NaN for an infinite or NaN one, so the sum
+            // is 0 exactly when every entry is finite (one FFMA per coordinate)
+            float nf = fmaf(Jtot, 0.f, 0.f);
+            for (int d = 0; d < D; ++d) nf = fmaf(gs(d), 0.f, nf);
+            invalid = invalid || !(nf == 0.f);
             const float rbc1 = A.rbc1[it];
             const float rbc2 = A.rbc2[it];
             if (!invalid) {
+#pragma unroll 2
                 for (int d = 0; d < D; ++d) {
                     const float g = gs(d) * P.grad_scale;
                     const float mm = fmaf(P.beta1, col(L.m + d), (1.f - P.beta1) * g);
@@ -624,8 +655,9 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     col(L.v + d) = vv;
                     const float mh = mm * rbc1;
                     const float vh = vv * rbc2;
-                    const float xn = xs(d) - A.lr[d] * mh / (sqrtf(vh) + P.adam_eps);
-                    xs(d) = fminf(fmaxf(xn, A.lo[d]), A.hi[d]);
+                    // MUFU square root and reciprocal (flush-to-zero forms: no denormal rescaling around them)
+                    const float xn = xs(d) - s_lr[d] * mh * rcp_approx(sqrt_approx(vh) + P.adam_eps);
+                    xs(d) = fminf(fmaxf(xn, s_lr[D + d]), s_lr[2 * D + d]);
                 }
             }
         }

@@ -32,7 +32,10 @@ cudaError_t launch_ik(const KProgram& P, const KSampleProgram& SP, float* x, con
                       uint64_t seed, int iters, float damping, int n_seeds, int32_t* lists, int32_t* list_n,
                       float* best, cudaStream_t st);
 int particle_kernel_regs(int gs, int threads);
-int serial_kernel_regs();
+int serial_kernel_regs(bool pp);
+#ifndef TAMP_SERIAL_PP
+#define TAMP_SERIAL_PP 1
+#endif
 cudaError_t launch_topk(unsigned long long* ka, int32_t* pa, unsigned long long* kb, int32_t* pb, int64_t n, int k,
                         cudaStream_t st, unsigned long long** kres, int32_t** pres);
 cudaError_t launch_make_keys(const uint8_t* cls, const float* cost, int64_t n, int64_t gofs, unsigned long long* keys,
@@ -269,6 +272,10 @@ static tamp_status compile(const tamp_problem_desc& d, int64_t n_global, Compile
             const double a = R.dh[j][0], dd = R.dh[j][1], al = R.dh[j][2];
             H34 F = h_mul(h_rx(al), h_tr(a, 0.0, dd));
             if (j == 0) F = h_mul(T, F);
+            P.dh[j][0] = (float)a;
+            P.dh[j][1] = (float)dd;
+            P.dh[j][2] = (float)std::cos(al);
+            P.dh[j][3] = (float)std::sin(al);
             h_store(F, P.F[j]);
             h_store(h_inv(F), P.Finv[j]);
             P.jlo[j] = R.joint_lo[j];
@@ -946,7 +953,7 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             int smem_sm = 228 * 1024;
             cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
             cudaGetLastError();
-            const int regs = std::max(32, serial_kernel_regs());
+            const int regs = std::max(32, serial_kernel_regs(TAMP_SERIAL_PP && c->P.smooth <= 0.f && serial_program_pp(c->P)));
             int best_w = -1;
             for (int t = 32; t <= (c->bsync ? kSerialThreads : 128); t += 32) {
                 const size_t sb = serial_smem_bytes(c->P, t, true) + 4096;   // + static smem, reserved

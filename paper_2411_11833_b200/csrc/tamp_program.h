@@ -90,6 +90,10 @@ struct KProgram {
     // into F_1) or, for lane 7, the tool transform F_ee; and the spheres attached to that frame.
     float F[kGroup][12];
     float Finv[kGroup][12];              // F^-1 of each (serial mapping: backward sweep over the links)
+    // modified-DH numbers of joints 2..7 (index 1..6): (a_{j-1}, d_j, cos alpha_{j-1}, sin alpha_{j-1}), F[j] =
+    // Rx(alpha) Tx(a) Tz(d) -- the serial mapping composes / inverts these factors directly (dh_fwd / dh_bwd);
+    // index 0 is unused (F[0] also carries the base)
+    float dh[TAMP_NJ][4];
     float rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK][4];
     int32_t rsph_n[kGroup];
     float jlo[TAMP_NJ], jhi[TAMP_NJ];
