@@ -232,14 +232,15 @@ __device__ __forceinline__ float smooth_cost(float p, float s, float& gsc) {
     return p;
 }
 
-template <bool GRAD>
+// ALIGNED: the caller guarantees B.aligned (R = I): the rotations are omitted (the same values)
+template <bool GRAD, bool ALIGNED = false>
 __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float rr, const KObb& B, float lam,
                                             float& gx, float& gy, float& gz, float smooth = 0.f) {
     // oriented box: p = R^T (w - c) with R the box's full rotation (row-major); for a box yawed
     // about z (R[2] = R[5] = R[6] = R[7] = 0, R[8] = 1) the extra terms are exact zeros
     const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
     float px = dx, py = dy, pz = dz;                     // axis-aligned box: R = I (the same values, exactly)
-    if (!B.aligned) {
+    if (!ALIGNED && !B.aligned) {
         px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
         py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
         pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));
@@ -271,7 +272,11 @@ __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float 
     float gsc;
     pen = smooth_cost(pen, smooth, gsc);
     lam *= gsc;
-    if (GRAD) {   // dJ/dw = -R grad_p
+    if (GRAD && ALIGNED) {   // R = I
+        gx = fmaf(-lam, gpx, gx);
+        gy = fmaf(-lam, gpy, gy);
+        gz = fmaf(-lam, gpz, gz);
+    } else if (GRAD) {   // dJ/dw = -R grad_p
         gx = fmaf(-lam, fmaf(B.R[0], gpx, fmaf(B.R[1], gpy, B.R[2] * gpz)), gx);
         gy = fmaf(-lam, fmaf(B.R[3], gpx, fmaf(B.R[4], gpy, B.R[5] * gpz)), gy);
         gz = fmaf(-lam, fmaf(B.R[6], gpx, fmaf(B.R[7], gpy, B.R[8] * gpz)), gz);
@@ -282,10 +287,11 @@ __device__ __forceinline__ float sphere_obb(float wx, float wy, float wz, float 
 // Can a sphere (centre w, radius r) reach the OBB?  false only if it is outside the box and its centre is at
 // least r from it -- the exact test sphere_obb rejects on, so a bounding sphere that fails it bounds only
 // spheres whose hinges are all zero.
+template <bool ALIGNED = false>
 __device__ __forceinline__ bool obb_within(float wx, float wy, float wz, float r, const KObb& B) {
     const float dx = wx - B.c[0], dy = wy - B.c[1], dz = wz - B.c[2];
     float px = dx, py = dy, pz = dz;                     // axis-aligned box: R = I (the same values, exactly)
-    if (!B.aligned) {
+    if (!ALIGNED && !B.aligned) {
         px = fmaf(B.R[0], dx, fmaf(B.R[3], dy, B.R[6] * dz));
         py = fmaf(B.R[1], dx, fmaf(B.R[4], dy, B.R[7] * dz));
         pz = fmaf(B.R[2], dx, fmaf(B.R[5], dy, B.R[8] * dz));

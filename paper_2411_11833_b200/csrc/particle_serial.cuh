@@ -63,14 +63,16 @@ __device__ __forceinline__ void serial_term(const KProgram& P, const KArgs& A, T
     }
 }
 
-// Is the program of the pick-place class (PP): every configuration's robot collision is against at most one box and
-// no partner instances (config 1)?  Then k_serial<.., PP = true> unrolls the link sweep (the per-link robot data
+// Is the program of the pick-place class (PP): every configuration's robot collision is against at most one
+// axis-aligned box and no partner instances (config 1)?  Then k_serial<.., PP = true> unrolls the link sweep (the per-link robot data
 // become constant-bank operands: no indexed constant loads or loop control) and keeps only the packed one-box path.
 __host__ __device__ inline bool serial_program_pp(const KProgram& P) {
     for (int f = 0; f < P.n_fk; ++f) {
         const KFk& K = P.fk[f];
         if (K.ghost || K.term_cf < 0) continue;
         if (K.part_count != 0 || (K.obb_mask & (K.obb_mask - 1)) != 0) return false;
+        for (int b = 0; b < TAMP_MAX_OBB; ++b)
+            if (((K.obb_mask >> b) & 1) && !P.obb[b].aligned) return false;
     }
     return true;
 }
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         const float* lb = P.lbound[l];
                         float bx, by, bz;
                         xform_p(T, lb[0], lb[1], lb[2], bx, by, bz);
-                        near = obb_within(bx, by, bz, lb[3] + P.eta + kLinkMargin, B0);
+                        near = obb_within<true>(bx, by, bz, lb[3] + P.eta + kLinkMargin, B0);
                     }
                 } else if (near) {
                     const float* lb = P.lbound[l];
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         const F2 wy = fma2(bc(T.r(1, 0)), cx, fma2(bc(T.r(1, 1)), cy, fma2(bc(T.r(1, 2)), cz, bc(T.t(1)))));
                         const F2 wz = fma2(bc(T.r(2, 0)), cx, fma2(bc(T.r(2, 1)), cy, fma2(bc(T.r(2, 2)), cz, bc(T.t(2)))));
                         bool h0, h1;
-                        if (TAMP_BOX_CORNER && B0.aligned) {
+                        if (TAMP_BOX_CORNER && (PP || B0.aligned)) {
                             obb_reach_corner_pair(wx, wy, wz, cr, B0, h0, h1);
                         } else {
                             F2 px, py, pz;
@@ -401,12 +403,23 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         hit[k] = k < ns && h0;
                         hit[k + 1] = k + 1 < ns && h1;
                     }
+                    // the exact hinges of the spheres that reach the box, in ascending sphere order (the same sums as
+                    // one unrolled block per sphere): one rolled copy of the rare path per link, its operands
+                    // selected from registers (a small kernel body: the link sweep is unrolled)
+                    unsigned hm = 0;
 #pragma unroll
-                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) {
-                        if (!hit[k]) continue;
+                    for (int k = 0; k < TAMP_MAX_SPHERES_PER_LINK; ++k) hm |= hit[k] ? 1u << k : 0u;
+#pragma unroll 1
+                    while (hm) {
+                        const int k = __ffs(hm) - 1;
+                        hm &= hm - 1;
+                        float x = wq[0][0], y = wq[0][1], z = wq[0][2], r = rq[0];
+#pragma unroll
+                        for (int u = 1; u < TAMP_MAX_SPHERES_PER_LINK; ++u)
+                            if (k == u) { x = wq[u][0]; y = wq[u][1]; z = wq[u][2]; r = rq[u]; }
                         float g[3] = {0.f, 0.f, 0.f};
-                        jcf += sphere_obb<G>(wq[k][0], wq[k][1], wq[k][2], rq[k], B0, lam_cf, g[0], g[1], g[2], smooth);
-                        if (G) sfx.add_point(wq[k][0], wq[k][1], wq[k][2], g[0], g[1], g[2]);
+                        jcf += sphere_obb<G, PP>(x, y, z, r, B0, lam_cf, g[0], g[1], g[2], smooth);
+                        if (G) sfx.add_point(x, y, z, g[0], g[1], g[2]);
                     }
                 } else if (!PP && near) {
                     for (int k = 0; k < P.rsph_n[l]; ++k) {
