@@ -144,6 +144,12 @@ __device__ __forceinline__ float gsum(float v) {      // butterfly sum over the 
     return v;
 }
 
+// opaque register copies: the compiler cannot re-derive the value (e.g. re-load it from the constant bank)
+__device__ __forceinline__ int opaque_int(int v) { asm volatile("" : "+r"(v)); return v; }
+__device__ __forceinline__ float opaque_f(float v) { asm volatile("" : "+f"(v)); return v; }
+template <class T>
+__device__ __forceinline__ T* opaque_ptr(T* v) { asm volatile("" : "+l"(v)); return v; }
+
 // MUFU approximations without the denormal rescaling of sqrtf / division under -prec-sqrt=false / -prec-div=false
 // (inputs here are >= 0 Adam second moments and sums >= adam_eps > 0)
 __device__ __forceinline__ float sqrt_approx(float x) {

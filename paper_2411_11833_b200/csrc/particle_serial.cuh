@@ -77,6 +77,10 @@ __host__ __device__ inline bool serial_program_pp(const KProgram& P) {
     return true;
 }
 
+#ifndef TAMP_SERIAL_CONF_BARRIER   // block barrier after every configuration (1) or only after the Place terms (0);
+#define TAMP_SERIAL_CONF_BARRIER 0 // the generic sweep keeps it (its larger body: the instruction cache)
+#endif
+
 #ifndef TAMP_SERIAL_LINK_BROAD     // PP sweep: gate each link's packed sphere tests by its bounding sphere
 #define TAMP_SERIAL_LINK_BROAD 1
 #endif
@@ -337,15 +341,32 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             const bool one_obb = K.obb_mask != 0 && (K.obb_mask & (K.obb_mask - 1)) == 0;
             KObb B0;
             if (one_obb) B0 = P.obb[__ffs(K.obb_mask) - 1];
+            // PP: the per-configuration values the unrolled sweep uses, pinned in registers (opaque copies: the
+            // compiler would otherwise re-load them from the constant bank with a computed index at every link)
+            bool pp_cf = false, pp_jl = false;
+            float pp_lam_jl = 0.f;
+            int pp_g = 0;
+            if constexpr (PP) {
+                pp_cf = opaque_int(K.term_cf >= 0 && one_obb) != 0;
+                pp_jl = opaque_int(K.term_jl >= 0 && jl > 0.f) != 0;
+                pp_lam_jl = opaque_f(K.term_jl >= 0 ? P.term_lam[K.term_jl] : 0.f);
+                pp_g = opaque_int(L.g + K.xoff);   // (an offset: the accesses stay shared-memory ones)
+                if (one_obb) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        B0.c[i] = opaque_f(B0.c[i]); B0.h[i] = opaque_f(B0.h[i]);
+                        B0.lo[i] = opaque_f(B0.lo[i]); B0.hi[i] = opaque_f(B0.hi[i]);
+                    }
+                }
+            }
             // PP: the sweep unrolled (per-link data as constant-bank operands), only the packed one-box path
 #pragma unroll (PP ? kGroup : 1)
             for (int l = kGroup - 1; l >= 0; --l) {
                 // link broad phase (conservative, results unchanged): the link's bounding sphere against the
                 // boxes and the partner instances' bounding spheres; a link that reaches none of them has only
                 // zero hinges and zero gradients, so its spheres are skipped
-                bool near = K.term_cf >= 0 && P.rsph_n[l] > 0;
+                bool near = PP ? (pp_cf && P.rsph_n[l] > 0) : (K.term_cf >= 0 && P.rsph_n[l] > 0);
                 if (PP) {
-                    near = near && one_obb;
                     if (TAMP_SERIAL_LINK_BROAD && near) {
                         const float* lb = P.lbound[l];
                         float bx, by, bz;
@@ -457,12 +478,19 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                         const float my = sfx.m[1] - (oz * sfx.f[0] - ox * sfx.f[2]);
                         const float mz = sfx.m[2] - (ox * sfx.f[1] - oy * sfx.f[0]);
                         float dq = fmaf(zx, mx, fmaf(zy, my, zz * mz));
-                        if (K.term_jl >= 0 && jl > 0.f) {
+                        if (PP) {
+                            if (pp_jl) {
+                                const float ql = q[l];
+                                const float e = fmaxf(fmaxf(P.jlo[l] - ql, ql - P.jhi[l]), 0.f);
+                                if (e > 0.f) dq += pp_lam_jl * (ql > P.jhi[l] ? e : -e) / jl;
+                            }
+                            col(pp_g + l) += dq;
+                        } else if (K.term_jl >= 0 && jl > 0.f) {
                             const float ql = xs(K.xoff + l);
                             const float e = fmaxf(fmaxf(P.jlo[l] - ql, ql - P.jhi[l]), 0.f);
                             if (e > 0.f) dq += P.term_lam[K.term_jl] * (ql > P.jhi[l] ? e : -e) / jl;
                         }
-                        gs(K.xoff + l) += dq;
+                        if (!PP) gs(K.xoff + l) += dq;
                     }
                 }
                 if (l > 0) {           // T_{l} -> T_{l-1}: right-multiply by (F_l Rz(q_l))^-1 = Rz(-q_l) F_l^-1
@@ -481,7 +509,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             if (K.term_cf >= 0) serial_term<M>(P, A, sink, K.term_cf, jcf, active, p, s_counts);
             // block-synchronous configurations: every warp of the block executes the same (large) code region at
             // a time and the instruction cache is shared (the kernel body is ~100 KB of SASS)
-            if (A.bsync) __syncthreads();
+            if (A.bsync && (!PP || TAMP_SERIAL_CONF_BARRIER)) __syncthreads();
         }
 
         // ---- StablePlace / press contact / CFreePlace per Place or press action ----
@@ -551,7 +579,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
                     const float4 c = inst_sphere(qi, obj, k);
                     const float rr = c.w + P.eta;
                     float g[3] = {0.f, 0.f, 0.f};
-                    jcp += sphere_vs_obbs(c.x, c.y, c.z, rr, Q.obb_mask, lam_cp, g);
+                    if (Q.obb_mask) jcp += sphere_vs_obbs(c.x, c.y, c.z, rr, Q.obb_mask, lam_cp, g);
                     for (int pi = 0; pi < Q.part_count; ++pi) {
                         const int jj = P.partners[Q.part_begin + pi];
                         Wrench pw;
