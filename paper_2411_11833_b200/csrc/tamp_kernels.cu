@@ -126,20 +126,25 @@ __global__ void __launch_bounds__(128) k_sample(const __grid_constant__ KSampleP
 //   e = [t* - t_ee ; rotvec(R* R_ee^T)],  J = [z_j x (t_ee - o_j) ; z_j],  dq = J^T (J J^T + mu^2 I)^-1 e
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float y[6]) {
-    // A: packed lower triangle, row-major (i, j <= i) -> index i*(i+1)/2 + j.  In-place Cholesky.
+    // A: packed lower triangle, row-major (i, j <= i) -> index i*(i+1)/2 + j.  In-place Cholesky.  (Every loop has
+    // a constant trip count with a guard: nvcc left an inner loop with a j-dependent bound rolled, which put A in
+    // local memory.)
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         float d = A[j * (j + 1) / 2 + j];
 #pragma unroll
-        for (int k = 0; k < j; ++k) d = fmaf(-A[j * (j + 1) / 2 + k], A[j * (j + 1) / 2 + k], d);
+        for (int k = 0; k < 6; ++k)
+            if (k < j) d = fmaf(-A[j * (j + 1) / 2 + k], A[j * (j + 1) / 2 + k], d);
         const float ljj = sqrtf(fmaxf(d, 1e-30f));
         const float inv = 1.f / ljj;
         A[j * (j + 1) / 2 + j] = ljj;
 #pragma unroll
-        for (int i = j + 1; i < 6; ++i) {
+        for (int i = 0; i < 6; ++i) {
+            if (i <= j) continue;
             float v = A[i * (i + 1) / 2 + j];
 #pragma unroll
-            for (int k = 0; k < j; ++k) v = fmaf(-A[i * (i + 1) / 2 + k], A[j * (j + 1) / 2 + k], v);
+            for (int k = 0; k < 6; ++k)
+                if (k < j) v = fmaf(-A[i * (i + 1) / 2 + k], A[j * (j + 1) / 2 + k], v);
             A[i * (i + 1) / 2 + j] = v * inv;
         }
     }
@@ -148,14 +153,16 @@ __device__ __forceinline__ void chol6_solve(float A[21], const float b[6], float
     for (int i = 0; i < 6; ++i) {     // L z = b
         float v = b[i];
 #pragma unroll
-        for (int k = 0; k < i; ++k) v = fmaf(-A[i * (i + 1) / 2 + k], z[k], v);
+        for (int k = 0; k < 6; ++k)
+            if (k < i) v = fmaf(-A[i * (i + 1) / 2 + k], z[k], v);
         z[i] = v / A[i * (i + 1) / 2 + i];
     }
 #pragma unroll
     for (int i = 5; i >= 0; --i) {    // L^T y = z
         float v = z[i];
 #pragma unroll
-        for (int k = i + 1; k < 6; ++k) v = fmaf(-A[k * (k + 1) / 2 + i], y[k], v);
+        for (int k = 0; k < 6; ++k)
+            if (k > i) v = fmaf(-A[k * (k + 1) / 2 + i], y[k], v);
         y[i] = v / A[i * (i + 1) / 2 + i];
     }
 }
@@ -171,28 +178,35 @@ constexpr float kIkTolPos = 1e-3f, kIkTolRot = 1e-3f;  // a restart counts as co
 constexpr int kIkRestartsPerRound = 2;                   // restarts per pair and round of k_ik_restarts
 
 // tool pose of the chain at q, and the Kin errors to T*: e_pos = ||t* - t_ee||, theta = angle(R* R_ee^T)
+// (joint 1 from its fixed transform, which carries the base; joints 2..7 as modified-DH steps on the packed frame,
+// dh_fwd; the joint axes z_j and origins o_j are frame j's third column and translation)
 __device__ __forceinline__ void ik_fk(const KProgram& P, const float (&q)[TAMP_NJ], M34& T, float (&z)[TAMP_NJ][3],
                                       float (&o)[TAMP_NJ][3]) {
+    M34P Tp;
 #pragma unroll
     for (int j = 0; j < TAMP_NJ; ++j) {
         float s, c;
         fsincos(q[j], &s, &c);
-        M34 Aj;
+        if (j == 0) {
+            M34 A0;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const float* Fr = P.F[j] + 4 * i;
-            Aj.r[3 * i] = fmaf(Fr[0], c, Fr[1] * s);
-            Aj.r[3 * i + 1] = fmaf(Fr[1], c, -Fr[0] * s);
-            Aj.r[3 * i + 2] = Fr[2];
-            Aj.t[i] = Fr[3];
+            for (int i = 0; i < 3; ++i) {
+                const float* Fr = P.F[0] + 4 * i;
+                A0.r[3 * i] = fmaf(Fr[0], c, Fr[1] * s);
+                A0.r[3 * i + 1] = fmaf(Fr[1], c, -Fr[0] * s);
+                A0.r[3 * i + 2] = Fr[2];
+                A0.t[i] = Fr[3];
+            }
+            Tp = pack_m34(A0);
+        } else {
+            dh_fwd(Tp, P.dh[j], c, s);
         }
-        T = j == 0 ? Aj : compose(T, Aj);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) { z[j][i] = T.r[3 * i + 2]; o[j][i] = T.t[i]; }
+        z[j][0] = lo(Tp.r01[2]); z[j][1] = hi(Tp.r01[2]); z[j][2] = Tp.r2[2];
+        o[j][0] = lo(Tp.t01); o[j][1] = hi(Tp.t01); o[j][2] = Tp.t2;
     }
     M34 Fe;
     load_m34(Fe, P.F[kGroup - 1]);
-    T = compose(T, Fe);
+    T = unpack_m34(compose_p(Tp, Fe));
 }
 
 __device__ __forceinline__ void ik_error(const M34& Ts, const M34& T, float (&e)[6], float& epos, float& th) {
