@@ -150,6 +150,13 @@ __device__ __forceinline__ float opaque_f(float v) { asm volatile("" : "+f"(v));
 template <class T>
 __device__ __forceinline__ T* opaque_ptr(T* v) { asm volatile("" : "+l"(v)); return v; }
 
+// 4-byte asynchronous copy global -> shared (cp.async.ca; completed by cp_async_wait_all)
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // MUFU approximations without the denormal rescaling of sqrtf / division under -prec-sqrt=false / -prec-div=false
 // (inputs here are >= 0 Adam second moments and sums >= adam_eps > 0)
 __device__ __forceinline__ float sqrt_approx(float x) {

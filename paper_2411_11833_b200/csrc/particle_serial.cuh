@@ -113,8 +113,11 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         const float* base = src + row0 * w;
         const int dq = NT / w, dr = NT % w;
         int q = tid / w, r = tid % w;
+        // cp.async (global -> shared, no register round trip): every load of the block is in flight at once
+        // instead of one HBM latency per element the thread copies; completed by cp_async_wait_all before the
+        // block barrier that ends the prologue
         for (int e = tid; e < nrows * w; e += NT) {
-            S[q * ROWP + c0 + r] = base[e];
+            cp_async4(&S[q * ROWP + c0 + r], base + e);
             q += dq; r += dr;
             if (r >= w) { r -= w; ++q; }
         }
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     if (MODE == MODE_OPT)
         for (int i = tid; i < 3 * D; i += NT) s_lr[i] = i < D ? A.lr[i] : (i < 2 * D ? A.lo[i - D] : A.hi[i - 2 * D]);
     bool invalid = A.invalid[p] != 0;
+    cp_async_wait_all();
     __syncthreads();
 
     // world sphere k of an instance at pose (cos, sin, px, py, pz)
