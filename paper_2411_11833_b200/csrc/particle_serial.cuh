@@ -18,16 +18,16 @@
 namespace tamp {
 
 struct SerialLayout {
-    int x, m, v, g, gT, ipose, iwr, n;   // column offsets (floats per thread)
+    int x, g, gT, ipose, iwr, n;   // column offsets (floats per thread)
 };
 
-// mv: Adam moments resident in shared memory for the launch (optimisation mode only)
-__host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool mv) {
+// The Adam moments are not in the rows: they stay in global memory (L2-resident for the launch) in the 32-particle
+// tile layout of the serial mapping (mv_w32_index), read and written once per step by Adam -- which frees 2 D floats
+// of shared memory per particle for more resident warps.
+__host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool /*mv*/ = true) {
     SerialLayout L;
     int f = 0;
     L.x = f;     f += P.D;
-    L.m = f;     f += mv ? P.D : 0;
-    L.v = f;     f += mv ? P.D : 0;
     L.g = f;     f += P.D;
     L.gT = f;    f += 12 * P.n_grasp;
     L.ipose = f; f += 8 * P.n_inst;    // cos, sin, px, py, pz, world bounding-sphere centre xyz
@@ -37,6 +37,10 @@ __host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool mv
 }
 
 constexpr int kSerialThreads = 512;   // launch bound (blocks of <= 512 threads, <= 128 registers)
+#ifndef TAMP_SERIAL_MAXT_PP
+#define TAMP_SERIAL_MAXT_PP 640          // pick-place variant: <= 102 registers
+#endif
+constexpr int kSerialThreadsPP = TAMP_SERIAL_MAXT_PP;
 
 // floats per thread row of the shared-memory state: the layout's size rounded up to odd, so that the 32 threads
 // of a warp reading the same field (stride = row pitch) hit 32 distinct banks
@@ -86,7 +90,7 @@ __host__ __device__ inline bool serial_program_pp(const KProgram& P) {
 #endif
 
 template <int MODE, bool SMOOTH, bool PP>
-__global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_constant__ KProgram P, const KArgs A) {
+__global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_serial(const __grid_constant__ KProgram P, const KArgs A) {
     constexpr bool GRAD = MODE != MODE_CHECK;
     const float smooth = SMOOTH ? P.smooth : 0.f;
     extern __shared__ float4 smem4[];
@@ -157,10 +161,6 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
     if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = tid; i < P.n_terms + 2; i += NT) s_counts[i] = 0;
     load_rows(A.x, D, L.x);
-    if (MODE == MODE_OPT) {
-        load_rows(A.m, D, L.m);
-        load_rows(A.v, D, L.v);
-    }
     if (P.n_grasp) load_rows(A.grasp, 12 * P.n_grasp, L.gT);
     // Adam step sizes and bounds: per-coordinate, the same for every particle (broadcast shared-memory reads)
     float* const s_lr = S + NT * ROWP;
@@ -690,19 +690,34 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
             invalid = invalid || !(nf == 0.f);
             const float rbc1 = A.rbc1[it];
             const float rbc2 = A.rbc2[it];
-            if (!invalid) {
-#pragma unroll 2
-                for (int d = 0; d < D; ++d) {
-                    const float g = gs(d) * P.grad_scale;
-                    const float mm = fmaf(P.beta1, col(L.m + d), (1.f - P.beta1) * g);
-                    const float vv = fmaf(P.beta2, col(L.v + d), (1.f - P.beta2) * g * g);
-                    col(L.m + d) = mm;
-                    col(L.v + d) = vv;
-                    const float mh = mm * rbc1;
-                    const float vh = vv * rbc2;
-                    // MUFU square root and reciprocal (flush-to-zero forms: no denormal rescaling around them)
-                    const float xn = xs(d) - s_lr[d] * mh * rcp_approx(sqrt_approx(vh) + P.adam_eps);
-                    xs(d) = fminf(fmaxf(xn, s_lr[D + d]), s_lr[2 * D + d]);
+            if (!invalid && active) {
+                // moments in the 32-particle tile layout: a warp's accesses to coordinate d are one 128-byte line;
+                // loaded in batches of kB coordinates (one L2 latency per batch)
+                float* const mt = A.m + mv_w32_index(pid, 0, D);
+                float* const vt = A.v + mv_w32_index(pid, 0, D);
+                constexpr int kB = 6;
+                for (int d0 = 0; d0 < D; d0 += kB) {
+                    float mo[kB], vo[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        mo[u] = d0 + u < D ? mt[(d0 + u) * 32] : 0.f;
+                        vo[u] = d0 + u < D ? vt[(d0 + u) * 32] : 0.f;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        const int d = d0 + u;
+                        if (d >= D) break;
+                        const float g = gs(d) * P.grad_scale;
+                        const float mm = fmaf(P.beta1, mo[u], (1.f - P.beta1) * g);
+                        const float vv = fmaf(P.beta2, vo[u], (1.f - P.beta2) * g * g);
+                        mt[d * 32] = mm;
+                        vt[d * 32] = vv;
+                        const float mh = mm * rbc1;
+                        const float vh = vv * rbc2;
+                        // MUFU square root and reciprocal (flush-to-zero forms: no denormal rescaling around them)
+                        const float xn = xs(d) - s_lr[d] * mh * rcp_approx(sqrt_approx(vh) + P.adam_eps);
+                        xs(d) = fminf(fmaxf(xn, s_lr[D + d]), s_lr[2 * D + d]);
+                    }
                 }
             }
         }
@@ -719,8 +734,6 @@ __global__ void __launch_bounds__(kSerialThreads, 1) k_serial(const __grid_const
         if (active) A.invalid[p] = invalid ? 1 : 0;
         __syncthreads();
         store_rows(A.x, D, L.x);
-        store_rows(A.m, D, L.m);
-        store_rows(A.v, D, L.v);
     }
     if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after)) {
         __syncthreads();

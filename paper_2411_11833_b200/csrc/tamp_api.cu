@@ -44,6 +44,7 @@ cudaError_t launch_record_keys(const float* rec, int32_t n, int32_t width, unsig
                                cudaStream_t st);
 cudaError_t launch_gather_particles(const int32_t* pay, const unsigned long long* keys, int k, const float* x,
                                     const float* cost, int D, int64_t gofs, float* rec, cudaStream_t st);
+cudaError_t launch_mv_layout(const float* src, float* dst, int64_t n, int D, int to_w32, cudaStream_t st);
 cudaError_t launch_gather_records(const int32_t* pay, int k, const float* rin, int width, float* rout, cudaStream_t st);
 uint64_t launch_count();
 }  // namespace tamp
@@ -749,6 +750,8 @@ static void smem_layout(tamp_ctx* c) {
     c->stride_bytes = stride * (int)sizeof(float);
 }
 
+static size_t mv_bytes(const tamp_ctx* c) { return (size_t)((c->n + 31) & ~(int64_t)31) * c->P.D * 4; }
+
 static void ws_layout(tamp_ctx* c) {
     const int64_t n = c->n;
     const int D = c->P.D, G = c->P.n_grasp;
@@ -756,8 +759,9 @@ static void ws_layout(tamp_ctx* c) {
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
     c->o_x = take((size_t)n * D * 4);
-    c->o_m = take((size_t)n * D * 4);
-    c->o_v = take((size_t)n * D * 4);
+    // Adam moments: padded to whole 32-particle tiles (the serial mapping's layout, mv_w32_index)
+    c->o_m = take(mv_bytes(c));
+    c->o_v = take(mv_bytes(c));
     c->o_grasp = take((size_t)n * G * 12 * 4);
     c->o_inv = take((size_t)n);
     c->o_cls = take((size_t)n);
@@ -939,9 +943,11 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
         cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
         cudaGetLastError();
         c->threads = desc->block_threads ? desc->block_threads : 128;
-        if (c->threads % 32 || c->threads < 32 || c->threads > kSerialThreads) {
+        const int maxt = (TAMP_SERIAL_PP && c->P.smooth <= 0.f && serial_program_pp(c->P)) ? kSerialThreadsPP : kSerialThreads;
+        if (c->threads % 32 || c->threads < 32 || c->threads > maxt) {
             delete c;
-            return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 512] for 1 lane per particle");
+            return fail(TAMP_E_INVALID, "block_threads must be a multiple of 32 in [32, 512] for 1 lane per particle "
+                                        "(pick-place class programs: [32, 640])");
         }
         // block-synchronous configurations (default): one large block per SM whose warps walk the ~100 KB kernel
         // body together and share the instruction cache (`no_instruction` was the top stall with independent
@@ -954,15 +960,31 @@ tamp_status tamp_init_problem(const tamp_problem_desc* desc, int device, int64_t
             cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
             cudaGetLastError();
             const int regs = std::max(32, serial_kernel_regs(TAMP_SERIAL_PP && c->P.smooth <= 0.f && serial_program_pp(c->P)));
+            int n_sm = 148;
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+            cudaGetLastError();
             int best_w = -1;
-            for (int t = 32; t <= (c->bsync ? kSerialThreads : 128); t += 32) {
+            double best_cost = 1e300;
+            for (int t = 32; t <= (c->bsync ? maxt : 128); t += 32) {
                 const size_t sb = serial_smem_bytes(c->P, t, true) + 4096;   // + static smem, reserved
                 if (sb > (size_t)smem_optin) continue;
                 const int by_smem = (int)((size_t)smem_sm / sb);
                 const int by_regs = 65536 / (((regs + 7) & ~7) * t);
                 const int blocks = c->bsync ? std::min(std::min(by_smem, by_regs), 1) : std::min(std::min(by_smem, by_regs), 32);
+                if (blocks < 1) continue;
                 const int w = blocks * (t / 32);
-                if (w > best_w || (w == best_w && t > c->threads)) { best_w = w; c->threads = t; }
+                if (c->bsync) {
+                    // balanced waves (as for the lane mappings): W waves of w resident warps per SM cost W (w + 20)
+                    // -- the per-SM rate w / (w + 20) fitted to the serial kernel's warp sweep (9 / 11 / 13 / 15
+                    // warps: 2268 / 2729 / 2869 / 3117 particles per ms per wave)
+                    const int64_t nb = (n_local + t - 1) / t;
+                    const int64_t waves = (nb + n_sm - 1) / n_sm;
+                    const double cost = (double)waves * (w + 20);
+                    if (cost < best_cost || (cost == best_cost && t > c->threads)) { best_cost = cost; c->threads = t; }
+                } else if (w > best_w || (w == best_w && t > c->threads)) {
+                    best_w = w;
+                    c->threads = t;
+                }
             }
         }
         c->smem = serial_smem_bytes(c->P, c->threads, true);
@@ -1132,8 +1154,8 @@ tamp_status tamp_sample_particles(tamp_ctx* c, uint64_t seed, void* stream) {
                        c->ik_damping, c->ik_seeds, c->at<int32_t>(c->o_iklist), c->at<int32_t>(c->o_ikn),
                        c->at<float>(c->o_ikbest), st),
              "sample: IK");
-    CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero m");
-    CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, (size_t)c->n * c->P.D * 4, st), "sample: zero v");
+    CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, mv_bytes(c), st), "sample: zero m");
+    CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, mv_bytes(c), st), "sample: zero v");
     CUDA_TRY(cudaMemsetAsync(c->base + c->o_inv, 0, (size_t)c->n, st), "sample: zero invalid");
     c->t = 0;
     c->ready = true;
@@ -1316,6 +1338,34 @@ tamp_status tamp_eval(tamp_ctx* c, float* J, float* soft, float* Jc, float* grad
     return TAMP_OK;
 }
 
+// Adam moments between the caller's [n][D] layout and the context's: [n][D] for the lane mappings, 32-particle tiles
+// for the serial mapping (mv_w32_index) -- converted by a kernel for device-accessible buffers, on the host (through
+// a staging copy, synchronous) for host buffers
+static cudaError_t get_moments(tamp_ctx* c, float* dst, size_t off, cudaStream_t st) {
+    const size_t nd = (size_t)c->n * c->P.D * 4;
+    if (c->gs != 1) return cudaMemcpyAsync(dst, c->base + off, nd, cudaMemcpyDefault, st);
+    if (!is_host_ptr(dst)) return launch_mv_layout(c->at<float>(off), dst, c->n, c->P.D, 0, st);
+    std::vector<float> t(mv_bytes(c) / 4);
+    cudaError_t e = cudaMemcpyAsync(t.data(), c->base + off, mv_bytes(c), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    const int D = c->P.D;
+    for (int64_t p = 0; p < c->n; ++p)
+        for (int d = 0; d < D; ++d) dst[p * D + d] = t[mv_w32_index(p, d, D)];
+    return cudaSuccess;
+}
+static cudaError_t set_moments(tamp_ctx* c, const float* src, size_t off, cudaStream_t st) {
+    const size_t nd = (size_t)c->n * c->P.D * 4;
+    if (c->gs != 1) return cudaMemcpyAsync(c->base + off, src, nd, cudaMemcpyDefault, st);
+    if (!is_host_ptr(src)) return launch_mv_layout(src, c->at<float>(off), c->n, c->P.D, 1, st);
+    const int D = c->P.D;
+    std::vector<float> t(mv_bytes(c) / 4, 0.f);
+    for (int64_t p = 0; p < c->n; ++p)
+        for (int d = 0; d < D; ++d) t[mv_w32_index(p, d, D)] = src[p * D + d];
+    cudaError_t e = cudaMemcpyAsync(c->base + off, t.data(), mv_bytes(c), cudaMemcpyHostToDevice, st);
+    return e == cudaSuccess ? cudaStreamSynchronize(st) : e;   // the staging vector must outlive the copy
+}
+
 tamp_status tamp_get_state(tamp_ctx* c, float* x, float* m, float* v, float* grasp, uint8_t* invalid, int32_t* t,
                            void* stream) {
     if (!c) return fail(TAMP_E_INVALID, "null context");
@@ -1325,8 +1375,8 @@ tamp_status tamp_get_state(tamp_ctx* c, float* x, float* m, float* v, float* gra
     const size_t nd = (size_t)c->n * c->P.D * 4;
     bool host = false;
     if (x) { CUDA_TRY(cudaMemcpyAsync(x, c->base + c->o_x, nd, cudaMemcpyDefault, st), "get x"); host |= is_host_ptr(x); }
-    if (m) { CUDA_TRY(cudaMemcpyAsync(m, c->base + c->o_m, nd, cudaMemcpyDefault, st), "get m"); host |= is_host_ptr(m); }
-    if (v) { CUDA_TRY(cudaMemcpyAsync(v, c->base + c->o_v, nd, cudaMemcpyDefault, st), "get v"); host |= is_host_ptr(v); }
+    if (m) { CUDA_TRY(get_moments(c, m, c->o_m, st), "get m"); host |= is_host_ptr(m); }
+    if (v) { CUDA_TRY(get_moments(c, v, c->o_v, st), "get v"); host |= is_host_ptr(v); }
     if (grasp && c->P.n_grasp) {
         CUDA_TRY(cudaMemcpyAsync(grasp, c->base + c->o_grasp, (size_t)c->n * c->P.n_grasp * 48, cudaMemcpyDefault, st), "get grasp");
         host |= is_host_ptr(grasp);
@@ -1351,10 +1401,10 @@ tamp_status tamp_set_state(tamp_ctx* c, const float* x, const float* m, const fl
     CUDA_TRY(upload_coords(c, st), "set_state: upload bounds");
     const size_t nd = (size_t)c->n * c->P.D * 4;
     CUDA_TRY(cudaMemcpyAsync(c->base + c->o_x, x, nd, cudaMemcpyDefault, st), "set x");
-    if (m) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_m, m, nd, cudaMemcpyDefault, st), "set m");
-    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, nd, st), "zero m");
-    if (v) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_v, v, nd, cudaMemcpyDefault, st), "set v");
-    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, nd, st), "zero v");
+    if (m) CUDA_TRY(set_moments(c, m, c->o_m, st), "set m");
+    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_m, 0, mv_bytes(c), st), "zero m");
+    if (v) CUDA_TRY(set_moments(c, v, c->o_v, st), "set v");
+    else CUDA_TRY(cudaMemsetAsync(c->base + c->o_v, 0, mv_bytes(c), st), "zero v");
     if (grasp && c->P.n_grasp)
         CUDA_TRY(cudaMemcpyAsync(c->base + c->o_grasp, grasp, (size_t)c->n * c->P.n_grasp * 48, cudaMemcpyDefault, st), "set grasp");
     if (invalid) CUDA_TRY(cudaMemcpyAsync(c->base + c->o_inv, invalid, (size_t)c->n, cudaMemcpyDefault, st), "set invalid");

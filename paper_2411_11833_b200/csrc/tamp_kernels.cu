@@ -520,6 +520,26 @@ __global__ void k_gather_records(const int32_t* __restrict__ pay, int k, const f
 // ------------------------------------------------------------------------------------------------
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count() { return g_launches.load(); }
+void note_launch();
+
+// Adam moments [n][D] <-> the serial mapping's 32-particle tiles (tamp_get_state / tamp_set_state)
+__global__ void k_mv_layout(const float* __restrict__ src, float* __restrict__ dst, int64_t n, int D, int to_w32) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * D) return;
+    const int64_t p = e / D;
+    const int d = (int)(e - p * D);
+    const int64_t w = mv_w32_index(p, d, D);
+    if (to_w32) dst[w] = src[e];
+    else dst[e] = src[w];
+}
+
+cudaError_t launch_mv_layout(const float* src, float* dst, int64_t n, int D, int to_w32, cudaStream_t st) {
+    if (n <= 0 || D <= 0) return cudaSuccess;
+    k_mv_layout<<<(unsigned)((n * D + 255) / 256), 256, 0, st>>>(src, dst, n, D, to_w32);
+    note_launch();
+    return cudaGetLastError();
+}
+
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static inline void counted() { note_launch(); }
 

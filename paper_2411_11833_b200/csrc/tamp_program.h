@@ -16,6 +16,12 @@ constexpr int kMaxTraj = 32;          // motions carrying knots
 constexpr int kMaxPartners = 1024;    // collision partner instance references
 constexpr int kMaxConstConf = 8;      // constant confs referenced by trajectories (q0)
 constexpr int kGroup = 8;             // lanes per particle: one per link frame (7 joints + tool)
+// Adam moments of the serial mapping (one thread per particle): 32-particle tiles, coordinate-major inside a tile
+// (element (p, d) at ((p / 32) * D + d) * 32 + p % 32; the arrays hold ceil(n / 32) * 32 * D floats).  The lane
+// mappings use [n][D]; tamp_get_state / tamp_set_state convert.
+__host__ __device__ inline int64_t mv_w32_index(int64_t p, int d, int D) {
+    return ((p >> 5) * D + d) * 32 + (p & 31);
+}
 constexpr int kMaxStepsPerLaunch = 64; // fused Adam steps per particle-kernel launch
 constexpr int kInstFloats = 56;        // shared memory per object instance: pose 3x4, bounding sphere, 8 spheres, wrench
 
