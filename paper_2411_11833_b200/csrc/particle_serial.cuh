@@ -85,6 +85,10 @@ __host__ __device__ inline bool serial_program_pp(const KProgram& P) {
 #define TAMP_SERIAL_CONF_BARRIER 0 // the generic sweep keeps it (its larger body: the instruction cache)
 #endif
 
+#ifndef TAMP_SERIAL_ADAM_BATCH      // coordinates whose moments are loaded together (one L2 latency per batch)
+#define TAMP_SERIAL_ADAM_BATCH 6
+#endif
+
 #ifndef TAMP_SERIAL_LINK_BROAD     // PP sweep: gate each link's packed sphere tests by its bounding sphere
 #define TAMP_SERIAL_LINK_BROAD 1
 #endif
@@ -579,7 +583,9 @@ __global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_s
             if (Q.term_cp >= 0) {   // CFreePlace: the object's spheres vs OBBs (support excluded) and other objects
                 const float lam_cp = P.term_lam[Q.term_cp];
                 float jcp = 0.f;
-                for (int k = 0; k < no; ++k) {
+                // no box besides the support and no partner (config 1): every hinge is zero -- nothing to test
+                const int ncp = (Q.obb_mask || Q.part_count) ? no : 0;
+                for (int k = 0; k < ncp; ++k) {
                     const float4 c = inst_sphere(qi, obj, k);
                     const float rr = c.w + P.eta;
                     float g[3] = {0.f, 0.f, 0.f};
@@ -695,7 +701,7 @@ __global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_s
                 // loaded in batches of kB coordinates (one L2 latency per batch)
                 float* const mt = A.m + mv_w32_index(pid, 0, D);
                 float* const vt = A.v + mv_w32_index(pid, 0, D);
-                constexpr int kB = 6;
+                constexpr int kB = TAMP_SERIAL_ADAM_BATCH;
                 for (int d0 = 0; d0 < D; d0 += kB) {
                     float mo[kB], vo[kB];
 #pragma unroll
