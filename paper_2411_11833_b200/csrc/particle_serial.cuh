@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_s
     if (P.n_grasp) load_rows(A.grasp, 12 * P.n_grasp, L.gT);
     // Adam step sizes and bounds: per-coordinate, the same for every particle (broadcast shared-memory reads)
     float* const s_lr = S + NT * ROWP;
+    TAMP_DCHECK(MODE != MODE_OPT || NT * ROWP + 3 * D <= A.smem_floats);
     if (MODE == MODE_OPT)
         for (int i = tid; i < 3 * D; i += NT) s_lr[i] = i < D ? A.lr[i] : (i < 2 * D ? A.lo[i - D] : A.hi[i - 2 * D]);
     bool invalid = A.invalid[p] != 0;

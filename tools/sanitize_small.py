@@ -12,7 +12,7 @@ torch.cuda.set_device(0)
 cases = [(1, 8, False, 0), (2, 16, True, 0), (4, 4, False, 0), (3, 8, False, 0), (1, 1, False, 0), (6, 8, False, 0),
          (4, 16, False, 0), (4, 16, True, 0), (4, 16, False, 640), (3, 8, False, 896), (3, 8, False, 1024),
          (3, 8, True, 0), (2, 8, False, 768),
-         (7, 8, False, 0), (5, 8, False, 512)]
+         (7, 8, False, 0), (5, 8, False, 512), (1, 1, False, 640), (1, 1, False, 96), (2, 1, False, 0)]
 for cfg, lanes, selfc, threads in cases:
     n = 300
     spec = make_config(cfg, n=n)
