@@ -24,6 +24,9 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_ROLLED_HITS          // spheres_vs_obb: the exact hinges of the hit spheres as one rolled loop in the
+#define TAMP_ROLLED_HITS 1        // 16-lane variants (config 4: 8.13 -> 7.90 ms per launch); the 8-lane 896-thread
+#endif                            // variant (72 registers) was slower with it (config 3: 1.81 -> 1.91 ms)
 #ifndef TAMP_BOX_CORNER         // aligned boxes: the conservative corner-form reject test (obb_reach_corner_pair)
 #define TAMP_BOX_CORNER 1
 #endif
@@ -696,7 +699,7 @@ __device__ __forceinline__ void obb_offsets_pair(F2 x, F2 y, F2 z, const KObb& B
 // Small boxes are first gated by their bounding sphere.  The reject test is sphere_obb's own, s >= r^2 with
 // s = ||max(|R^T (w - c)| - h, 0)||^2, evaluated as 4 s = ||a + |a|||^2 >= (2r)^2 (a = |p| - h; scaling by 4 is
 // exact) on the FMA pipe; skipped spheres would add exact zeros: results are unchanged.
-template <bool GRAD, int NS>
+template <bool GRAD, int NS, bool ROLLED = false>
 __device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B, float lam, float (&g)[NS][3],
                                                 float smooth) {
     if (B.rad < kBroadMaxRad) {      // broad phase: bounding sphere of the box (not for boxes larger than the
@@ -759,9 +762,32 @@ __device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B
     }
     float j = 0.f;
     if (__any_sync(FULL, any)) {
+        if (ROLLED) {
+            // one rolled copy of the exact hinge over the hit bits in ascending sphere order (the same sums and
+            // the same fused accumulations as one unrolled block per sphere): operands and the sphere's gradient
+            // accumulator selected from registers -- a smaller kernel body (instruction cache)
+            unsigned hm = 0;
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
-            if (hit[k]) j += sphere_obb<GRAD>(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B, lam, g[k][0], g[k][1], g[k][2], smooth);
+            for (int k = 0; k < NS; ++k) hm |= hit[k] ? 1u << k : 0u;
+#pragma unroll 1
+            while (hm) {
+                const int k = __ffs(hm) - 1;
+                hm &= hm - 1;
+                float x = q.sx(0), y = q.sy(0), z = q.sz(0), r = q.sr(0);
+                float gx = g[0][0], gy = g[0][1], gz = g[0][2];
+#pragma unroll
+                for (int u = 1; u < NS; ++u)
+                    if (k == u) { x = q.sx(u); y = q.sy(u); z = q.sz(u); r = q.sr(u); gx = g[u][0]; gy = g[u][1]; gz = g[u][2]; }
+                j += sphere_obb<GRAD>(x, y, z, r, B, lam, gx, gy, gz, smooth);
+#pragma unroll
+                for (int u = 0; u < NS; ++u)
+                    if (k == u) { g[u][0] = gx; g[u][1] = gy; g[u][2] = gz; }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (hit[k]) j += sphere_obb<GRAD>(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B, lam, g[k][0], g[k][1], g[k][2], smooth);
+        }
     }
     return j;
 }
@@ -1104,7 +1130,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             if (K.term_cf >= 0) {
                 // robot spheres vs OBBs (constant cache)
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS>(rs, P.obb[b], lam_cf, gw, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS, TAMP_ROLLED_HITS && (HP > 1)>(rs, P.obb[b], lam_cf, gw, smooth);
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
@@ -1205,7 +1231,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
                 hq.finish();
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH>(hq, P.obb[b], lam_cf, gh, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH, TAMP_ROLLED_HITS && (HP > 1)>(hq, P.obb[b], lam_cf, gh, smooth);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
                     float* ip = inst(ii);
@@ -1464,7 +1490,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 qe.finish();
                 float jcp = 0.f;
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO>(qe, P.obb[b], lam_cp, gq, smooth);
+                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO, TAMP_ROLLED_HITS && (HP > 1)>(qe, P.obb[b], lam_cp, gq, smooth);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
                     float* jp = inst(jj);
