@@ -24,6 +24,9 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_OBB_SMEM             // lane mappings: boxes' fast-path data staged in shared memory once per block
+#define TAMP_OBB_SMEM 1           // (config 3 -0.3 %, config 4 -1.4 % per launch)
+#endif
 #ifndef TAMP_ROLLED_HITS          // spheres_vs_obb: the exact hinges of the hit spheres as one rolled loop in the
 #define TAMP_ROLLED_HITS 1        // 16-lane variants (config 4: 8.13 -> 7.90 ms per launch); the 8-lane 896-thread
 #endif                            // variant (72 registers) was slower with it (config 3: 1.81 -> 1.91 ms)
@@ -671,10 +674,11 @@ __device__ __forceinline__ void obb_reach_pair(F2 px, F2 py, F2 pz, F2 r, const 
 // q <= the exact test's max(|w - c| - h, 0) whatever the fp32 rounding (|coordinates| <= kMaxCoord): a sphere this
 // test rejects (||q||^2 >= r^2) is rejected by sphere_obb too; the few it keeps within the slack are evaluated
 // exactly (zero hinge).  Results are unchanged.
-__device__ __forceinline__ void obb_reach_corner_pair(F2 x, F2 y, F2 z, F2 r, const KObb& B, bool& h0, bool& h1) {
-    const F2 ux = sub2(x, bc(B.hi[0])), vx = sub2(bc(B.lo[0]), x);
-    const F2 uy = sub2(y, bc(B.hi[1])), vy = sub2(bc(B.lo[1]), y);
-    const F2 uz = sub2(z, bc(B.hi[2])), vz = sub2(bc(B.lo[2]), z);
+__device__ __forceinline__ void obb_reach_corner_pair(F2 x, F2 y, F2 z, F2 r, const float4& lo4, const float4& hi4,
+                                                      bool& h0, bool& h1) {
+    const F2 ux = sub2(x, bc(hi4.x)), vx = sub2(bc(lo4.x), x);
+    const F2 uy = sub2(y, bc(hi4.y)), vy = sub2(bc(lo4.y), y);
+    const F2 uz = sub2(z, bc(hi4.z)), vz = sub2(bc(lo4.z), z);
     const F2 qx = pk(fmaxf(fmaxf(lo(ux), lo(vx)), 0.f), fmaxf(fmaxf(hi(ux), hi(vx)), 0.f));
     const F2 qy = pk(fmaxf(fmaxf(lo(uy), lo(vy)), 0.f), fmaxf(fmaxf(hi(uy), hi(vy)), 0.f));
     const F2 qz = pk(fmaxf(fmaxf(lo(uz), lo(vz)), 0.f), fmaxf(fmaxf(hi(uz), hi(vz)), 0.f));
@@ -682,6 +686,10 @@ __device__ __forceinline__ void obb_reach_corner_pair(F2 x, F2 y, F2 z, F2 r, co
     const F2 r2 = mul2(r, r);
     h0 = !(lo(s) >= lo(r2));
     h1 = !(hi(s) >= hi(r2));
+}
+__device__ __forceinline__ void obb_reach_corner_pair(F2 x, F2 y, F2 z, F2 r, const KObb& B, bool& h0, bool& h1) {
+    obb_reach_corner_pair(x, y, z, r, make_float4(B.lo[0], B.lo[1], B.lo[2], 0.f),
+                          make_float4(B.hi[0], B.hi[1], B.hi[2], 0.f), h0, h1);
 }
 // box-frame offsets p = R^T (w - c) of a packed pair of points (aligned boxes: the offsets themselves)
 __device__ __forceinline__ void obb_offsets_pair(F2 x, F2 y, F2 z, const KObb& B, F2& px, F2& py, F2& pz) {
@@ -699,12 +707,21 @@ __device__ __forceinline__ void obb_offsets_pair(F2 x, F2 y, F2 z, const KObb& B
 // Small boxes are first gated by their bounding sphere.  The reject test is sphere_obb's own, s >= r^2 with
 // s = ||max(|R^T (w - c)| - h, 0)||^2, evaluated as 4 s = ||a + |a|||^2 >= (2r)^2 (a = |p| - h; scaling by 4 is
 // exact) on the FMA pipe; skipped spheres would add exact zeros: results are unchanged.
+// fb (optional): the box's fast-path data in shared memory (TAMP_OBB_SMEM: (c, rad), (lo, aligned), (hi, 0)), read
+// with three broadcast 16-byte loads instead of indexed constant loads; the exact hinge reads B
 template <bool GRAD, int NS, bool ROLLED = false>
 __device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B, float lam, float (&g)[NS][3],
-                                                float smooth) {
-    if (B.rad < kBroadMaxRad) {      // broad phase: bounding sphere of the box (not for boxes larger than the
+                                                float smooth, const float4* fb = nullptr) {
+    float4 cr, lo4, hi4;
+    if (fb) { cr = fb[0]; lo4 = fb[1]; hi4 = fb[2]; }
+    else {
+        cr = make_float4(B.c[0], B.c[1], B.c[2], B.rad);
+        lo4 = make_float4(B.lo[0], B.lo[1], B.lo[2], B.aligned ? 1.f : 0.f);
+        hi4 = make_float4(B.hi[0], B.hi[1], B.hi[2], 0.f);
+    }
+    if (cr.w < kBroadMaxRad) {       // broad phase: bounding sphere of the box (not for boxes larger than the
                                      // arm's reach, e.g. the table, where it would rarely reject)
-        if (!__any_sync(FULL, qset_near(q, B.c[0], B.c[1], B.c[2], B.rad))) return 0.f;
+        if (!__any_sync(FULL, qset_near(q, cr.x, cr.y, cr.z, cr.w))) return 0.f;
     }
     bool hit[NS], any = false;
     if (TAMP_PACK_OBB == 0) {         // scalar: obb_within per sphere
@@ -713,11 +730,11 @@ __device__ __forceinline__ float spheres_vs_obb(const QSet<NS>& q, const KObb& B
             hit[k] = obb_within(q.sx(k), q.sy(k), q.sz(k), q.sr(k), B);
             any = any || hit[k];
         }
-    } else if (TAMP_BOX_CORNER && TAMP_PACK_OBB == 1 && B.aligned) {
+    } else if (TAMP_BOX_CORNER && TAMP_PACK_OBB == 1 && lo4.w != 0.f) {
 #pragma unroll
         for (int j = 0; j < QSet<NS>::NP; ++j) {
             bool h0, h1;
-            obb_reach_corner_pair(q.x[j], q.y[j], q.z[j], q.r[j], B, h0, h1);
+            obb_reach_corner_pair(q.x[j], q.y[j], q.z[j], q.r[j], lo4, hi4, h0, h1);
             hit[2 * j] = h0;
             any = any || h0;
             if (2 * j + 1 < NS) {
@@ -884,6 +901,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     __shared__ float4 s_rsph[kGroup][TAMP_MAX_SPHERES_PER_LINK];   // spheres of each link frame
     __shared__ __align__(16) float s_rsoa[kGroup][4 * TAMP_MAX_SPHERES_PER_LINK];   // the same, SoA x[4] y[4] z[4] r[4]
     __shared__ uint32_t s_selfmask[kGroup * TAMP_MAX_SPHERES_PER_LINK];
+    // boxes' fast-path data (broad phase and corner reject test): (c, rad), (lo, aligned), (hi, 0) per box
+    __shared__ float4 s_obb[TAMP_OBB_SMEM ? TAMP_MAX_OBB : 1][3];
 
     const int gl = threadIdx.x & (GS - 1);          // lane within the particle group
     const int ll = gl & (LPF - 1);                  // lane within the FK segment
@@ -926,6 +945,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     }
     if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
+    if (TAMP_OBB_SMEM && threadIdx.x < P.n_obb) {
+        const KObb& B = P.obb[threadIdx.x];
+        s_obb[threadIdx.x][0] = make_float4(B.c[0], B.c[1], B.c[2], B.rad);
+        s_obb[threadIdx.x][1] = make_float4(B.lo[0], B.lo[1], B.lo[2], B.aligned ? 1.f : 0.f);
+        s_obb[threadIdx.x][2] = make_float4(B.hi[0], B.hi[1], B.hi[2], 0.f);
+    }
     if (threadIdx.x < kGroup * 3) {
         const int l = threadIdx.x / 3, r = threadIdx.x % 3;
         s_F[l][r] = make_float4(P.F[l][4 * r], P.F[l][4 * r + 1], P.F[l][4 * r + 2], P.F[l][4 * r + 3]);
@@ -1130,7 +1155,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
             if (K.term_cf >= 0) {
                 // robot spheres vs OBBs (constant cache)
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS, TAMP_ROLLED_HITS && (HP > 1)>(rs, P.obb[b], lam_cf, gw, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS, TAMP_ROLLED_HITS && (HP > 1)>(rs, P.obb[b], lam_cf, gw, smooth, TAMP_OBB_SMEM ? s_obb[b] : nullptr);
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
@@ -1231,7 +1256,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 }
                 hq.finish();
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH, TAMP_ROLLED_HITS && (HP > 1)>(hq, P.obb[b], lam_cf, gh, smooth);
+                    if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH, TAMP_ROLLED_HITS && (HP > 1)>(hq, P.obb[b], lam_cf, gh, smooth, TAMP_OBB_SMEM ? s_obb[b] : nullptr);
                 for (int pi = 0; pi < K.part_count; ++pi) {
                     const int ii = P.partners[K.part_begin + pi];
                     float* ip = inst(ii);
@@ -1490,7 +1515,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 qe.finish();
                 float jcp = 0.f;
                 for (int b = 0; b < P.n_obb; ++b)
-                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO, TAMP_ROLLED_HITS && (HP > 1)>(qe, P.obb[b], lam_cp, gq, smooth);
+                    if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO, TAMP_ROLLED_HITS && (HP > 1)>(qe, P.obb[b], lam_cp, gq, smooth, TAMP_OBB_SMEM ? s_obb[b] : nullptr);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
                     const int jj = P.partners[Q.part_begin + pi];
                     float* jp = inst(jj);
