@@ -5,6 +5,7 @@ TAG=${1:-final}
 O=gpurun_out/$TAG
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q > $O/gputests.log 2>&1; tail -3 $O/gputests.log
+bash tools/device_checks.sh > $O/device_checks.log 2>&1; tail -1 $O/device_checks.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
 python bench.py > $O/bench_default.log 2>&1
 python bench.py --impl reference > $O/bench_reference.log 2>&1
