@@ -286,7 +286,10 @@ tamp_status tamp_eval(tamp_ctx* ctx, float* J, float* soft, float* Jc, float* gr
 
 /* State access (checkpoint / parity).  x, m, v [n_local][D]; grasp [n_local][n_grasp][12];
    invalid [n_local] u8.  Device or host; any pointer may be NULL (get: skipped; set: m, v, invalid
-   NULL -> zero, grasp NULL -> keep, x must be given).  set_state also sets the Adam counter t. */
+   NULL -> zero, grasp NULL -> keep, x must be given).  set_state also sets the Adam counter t.
+   The context's internal layout of m and v is its own (the 1-lane-per-particle mapping keeps them in 32-particle
+   tiles); these calls always exchange [n_local][D] and convert (a kernel for device buffers; for host buffers a
+   host reorder through a staging copy, synchronous). */
 tamp_status tamp_get_state(tamp_ctx* ctx, float* x, float* m, float* v, float* grasp,
                            uint8_t* invalid, int32_t* t, void* stream);
 tamp_status tamp_set_state(tamp_ctx* ctx, const float* x, const float* m, const float* v,
