@@ -536,6 +536,36 @@ def test_serial_mapping_launch_configuration_invariance_bit_exact():
             assert np.array_equal(out[0], ref[0]) and np.array_equal(out[1], ref[1]), (threads, bsync)
 
 
+def test_serial_pick_place_variant_equals_generic_sweep_bit_exact():
+    """The serial mapping's pick-place variant (k_serial<.., PP = true>: unrolled link sweep, one axis-aligned box,
+    rolled hinge loop, CFreePlace skipped when it has nothing to test) against the generic sweep on the same
+    problem: config 1 plus a far-away second box (never reached) is not of the pick-place class, so it runs the
+    generic sweep, whose extra terms are exact zeros -- x, the moments and the satisfied counts after 2 x 10 fused
+    steps + checks are identical (values compared with ==: signed zeros may differ)."""
+    from workloads.scenes import OBB
+    n = 3000
+    a = make_config(1, n=n)
+    a.ik_iters = 5
+    bspec = dataclasses.replace(a, obbs=list(a.obbs) + [OBB(np.array([6.0, 6.0, 6.0]), 0.0, np.array([0.1, 0.1, 0.1]), "far")])
+    out, pairs = [], []
+    for sp in (a, bspec):
+        c = TampContext(sp, n, lanes_per_particle=1, block_threads=480)
+        pairs.append(c.work["pairs_sphere_obb"])
+        c.sample(seed=12)
+        cnt = []
+        for _ in range(2):
+            counts, _ = c.optimize_check(10)
+            cnt.append(counts.cpu().numpy().copy())
+        st = c.get_state()
+        out.append((st["x"].cpu().numpy(), st["m"].cpu().numpy(), st["v"].cpu().numpy(), cnt))
+    assert pairs[1] > pairs[0]            # the far box is in the collision terms: the generic sweep ran
+    for k in range(3):
+        assert (out[0][k] == out[1][k]).all(), k
+    for ca, cb in zip(out[0][3], out[1][3]):
+        assert np.array_equal(ca, cb)
+    assert out[0][3][-1][-2] > 0          # some particles satisfy: the comparison covers class-0 decisions
+
+
 @pytest.mark.parametrize("host", [False, True])
 def test_serial_mapping_checkpoint_resume_bit_exact(host):
     """The serial mapping keeps the Adam moments in 32-particle tiles (mv_w32_index); tamp_get_state /
