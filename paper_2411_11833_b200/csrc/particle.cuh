@@ -24,6 +24,9 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_FK_SMEM              // lane mappings: the configurations' descriptors in shared memory (<= 768-thread
+#define TAMP_FK_SMEM 1            // variants)
+#endif
 #ifndef TAMP_OBB_SMEM             // lane mappings: boxes' fast-path data staged in shared memory once per block
 #define TAMP_OBB_SMEM 1           // (config 3 -0.3 %, config 4 -1.4 % per launch)
 #endif
@@ -929,6 +932,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         return (I.xoff >= 0 ? minst : cinst) + kInstFloats * I.slot;
     };
     TAMP_DCHECK(A.const_floats + (grp + 1) * A.stride <= A.smem_floats);
+    TAMP_DCHECK(A.fk_off + P.n_fk * (int)(sizeof(KFk) / 4) <= A.const_floats);
     TAMP_DCHECK(A.off_g + P.D <= A.stride && A.off_gT + 12 * P.n_grasp <= A.stride);
     TAMP_DCHECK(A.off_gTi < 0 || A.off_gTi + 12 * P.n_grasp <= A.stride);
     TAMP_DCHECK(!P.has_self || A.off_rsw + 4 * HP * kGroup * TAMP_MAX_SPHERES_PER_LINK <= A.stride);
@@ -945,6 +949,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     }
     if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
+    // the configurations' descriptors, once per block (FKS: read by reference in the FK loop -- an indexed constant
+    // load plus its address computation at every use of a field otherwise; config 4 -2.4 %, config 2 -1.3 %; the
+    // register-tight 896 / 1024-bound variants keep the register copy, config 3 was 0.5 % slower with the table)
+    constexpr bool FKS = TAMP_FK_SMEM && MAXT <= 768;
+    KFk* const s_fk = reinterpret_cast<KFk*>(cinst + A.fk_off);
+    if (FKS)
+        for (int i = threadIdx.x; i < P.n_fk; i += blockDim.x) s_fk[i] = P.fk[i];
     if (TAMP_OBB_SMEM && threadIdx.x < P.n_obb) {
         const KObb& B = P.obb[threadIdx.x];
         s_obb[threadIdx.x][0] = make_float4(B.c[0], B.c[1], B.c[2], B.rad);
@@ -1072,7 +1083,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         // discarded), so control flow stays warp-uniform.  HP = 1: ghosts are skipped.
         TermSink<M> sinkB;                  // this half's share of the phase-B terms
         for (int f0 = 0; f0 < P.n_fk; f0 += HP) {
-            const KFk K = P.fk[f0 + (HP > 1 ? half : 0)];
+            KFk Kc;
+            if (!FKS) Kc = P.fk[f0 + (HP > 1 ? half : 0)];
+            const KFk& K = FKS ? s_fk[f0 + (HP > 1 ? half : 0)] : Kc;
             const bool real = !K.ghost;
             TAMP_DCHECK(f0 + HP <= TAMP_MAX_FK && K.xoff >= 0 && K.xoff + TAMP_NJ <= D);
             TAMP_DCHECK(K.part_begin >= 0 && K.part_begin + K.part_count <= kMaxPartners);

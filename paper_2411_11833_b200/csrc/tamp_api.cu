@@ -79,7 +79,7 @@ struct tamp_ctx {
     size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, o_iklist, o_ikn, o_ikbest, total;
     int64_t n_keys = 0;
     // shared-memory layout of the particle kernel (floats per particle)
-    int stride, off_g, off_inst, off_gT, off_gTi, off_rsw, const_floats;
+    int stride, off_g, off_inst, off_gT, off_gTi, off_rsw, const_floats, fk_off;
     size_t smem = 0;
     int gs = 8;                  // lanes per particle in the particle kernel
     int ik_iters = 0;            // conditional IK sampler iterations
@@ -742,6 +742,9 @@ static void smem_layout(tamp_ctx* c) {
     off += held ? 12 * P.n_grasp : 0;
     off = r4(off);
     c->const_floats = kInstFloats * n_const;          // constant instances: once per block
+    c->fk_off = c->const_floats;                      // then the configurations' descriptors, once per block
+    c->const_floats += ((P.n_fk * (int)sizeof(KFk) / 4) + 3) & ~3;
+    static_assert(sizeof(KFk) % 4 == 0, "KFk must be a whole number of floats");
     c->off_rsw = off;                                 // robot sphere centres for the SELF term (2 FK halves)
     off += P.has_self ? (c->gs == 16 ? 2 : 1) * 4 * (kGroup * TAMP_MAX_SPHERES_PER_LINK) : 0;   // per FK half
     // stride = 8 (mod 32) floats so the particles of a warp hit distinct banks on broadcasts
@@ -825,6 +828,7 @@ static KArgs base_args(tamp_ctx* c) {
     A.off_g = c->off_g;
     A.off_inst = c->off_inst;
     A.const_floats = c->const_floats;
+    A.fk_off = c->fk_off;
     A.off_gT = c->off_gT;
     A.off_gTi = c->off_gTi;
     A.off_rsw = c->off_rsw;

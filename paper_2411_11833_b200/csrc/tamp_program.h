@@ -151,7 +151,8 @@ struct KArgs {
     int64_t gofs;
     int32_t stride, off_g, off_inst, off_gT, off_gTi, off_rsw;   // per-particle shared memory (floats); off_gTi < 0:
                                                                // no held object at a knot, no inverse grasps
-    int32_t const_floats;  // block-shared constant instances at the start of dynamic shared memory
+    int32_t const_floats;  // block-shared constant instances at the start of dynamic shared memory, then the
+    int32_t fk_off;        // configurations' descriptors (KFk[n_fk], lane mappings) at float offset fk_off
     int32_t n_steps, t0;
     int32_t bsync;         // serial mapping: block barriers per configuration / phase (shared i-cache)
     int32_t check_after;   // MODE_OPT: run the Eq. 3 check of the final state in the same launch
