@@ -31,7 +31,9 @@ __host__ __device__ inline SerialLayout serial_layout(const KProgram& P, bool /*
     L.g = f;     f += P.D;
     L.gT = f;    f += 12 * P.n_grasp;
     L.ipose = f; f += 8 * P.n_inst;    // cos, sin, px, py, pz, world bounding-sphere centre xyz
-    L.iwr = f;   f += 6 * P.n_inst;    // wrench (F, M about the world origin) on each instance
+    int nm = 0;                        // movable instances (slot = index among them)
+    for (int i = 0; i < P.n_inst; ++i) nm += P.inst[i].xoff >= 0;
+    L.iwr = f;   f += 6 * nm;          // wrench (F, M about the world origin) on each movable instance
     L.n = f;
     return L;
 }
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_s
     auto xs = [&](int d) -> float& { return col(L.x + d); };
     auto gs = [&](int d) -> float& { return col(L.g + d); };
     auto ip = [&](int i, int k) -> float& { return col(L.ipose + 8 * i + k); };
-    auto iw = [&](int i, int k) -> float& { return col(L.iwr + 6 * i + k); };
+    auto iw = [&](int i, int k) -> float& { return col(L.iwr + 6 * P.inst[i].slot + k); };   // movable i only
     auto add_iw = [&](int i, const Wrench& w) {
         iw(i, 0) += w.f[0]; iw(i, 1) += w.f[1]; iw(i, 2) += w.f[2];
         iw(i, 3) += w.m[0]; iw(i, 4) += w.m[1]; iw(i, 5) += w.m[2];
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_s
                 ip(i, 6) = fmaf(sy, ob[0], fmaf(cy, ob[1], py));
                 ip(i, 7) = pz + ob[2];
             }
-            if (G)
+            if (G && I.xoff >= 0)
                 for (int k = 0; k < 6; ++k) iw(i, k) = 0.f;
         }
         if (G)
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(PP ? kSerialThreadsPP : kSerialThreads, 1) k_s
                 }
                 serial_term<M>(P, A, sink, Q.term_cp, jcp, active, p, s_counts);
             }
-            if (G) add_iw(ii, own);
+            if (G && I.xoff >= 0) add_iw(ii, own);
             if (A.bsync) __syncthreads();
         }
 
