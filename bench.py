@@ -67,6 +67,7 @@ def parse():
     p.add_argument("--repeats", type=int, default=5, help="timed regions of exactly --steps steps; value = median")
     p.add_argument("--no-extra", action="store_true", help="skip the extra workloads (config 2, config 1 at 1M, SELF)")
     p.add_argument("--no-overlap", action="store_true", help="all-reduce of the counts on the launching stream")
+    p.add_argument("--nvtx", action="store_true", help="NVTX ranges around the phases of a step (profiling)")
     p.add_argument("--lib", default=None, help="A/B experiments: another in-tree build of libtamp.so (exp/<name>/)")
     p.add_argument("--pipeline", type=int, default=-1,
                    help="1: the next batch's sampling + IK on a second stream under this batch's optimisation "
@@ -251,8 +252,13 @@ def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_
     P:461-467, so nothing in the next launch waits for the counts); two count buffers alternate, and a buffer
     is only rewritten after its all-reduce finished.  The counts are the same bytes either way.
     sampled: the batch was already initialised (pipelined rounds, timed_rounds)."""
+    nvtx = getattr(args, "nvtx", False)
     if not sampled:
+        if nvtx:
+            torch.cuda.nvtx.range_push("sample+IK (K1, K1b)")
         ctx.sample(seed)
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
     n_int = args.adam_steps // args.check_every
     direct = host_counts is not None and world == 1
     overlap = side is not None and dist is not None and not direct
@@ -267,12 +273,16 @@ def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
+        if nvtx:
+            torch.cuda.nvtx.range_push(f"K2 x{args.check_every} + check")
         if overlap:
             if i >= 2:
                 main_s.wait_stream(side)                  # buffer i % 2 free again (its all-reduce is done)
             counts, _ = ctx.optimize_check(args.check_every, counts=bufs[i % 2])
         else:
             counts, _ = ctx.optimize_check(args.check_every, counts=host_counts if direct else None)
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
         if events is not None:
             e1.record()
             events.append((e0, e1))
@@ -289,6 +299,16 @@ def run_round(ctx, seed, args, dist, world, events=None, host_counts=None, host_
                 host_counts.copy_(counts)                 # D2H
     if overlap:
         main_s.wait_stream(side)
+    if nvtx:
+        torch.cuda.nvtx.range_push("best-k (K4), all-gather, merge (K5)")
+    try:
+        return _finish_round(ctx, args, dist, world, host_rec)
+    finally:
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
+
+
+def _finish_round(ctx, args, dist, world, host_rec):
     if host_rec is not None and world == 1:
         ctx.best_k(args.k, out=host_rec)
         return host_rec
