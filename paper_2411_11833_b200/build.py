@@ -55,18 +55,19 @@ def build(force=False, verbose=False):
             fcntl.flock(lock, fcntl.LOCK_UN)
 
 
-def build_variant(name, defines, verbose=False):
-    """A/B build of the same sources with extra -D defines into exp/<name>/libtamp.so (in-tree, git-ignored; bench
-    --lib loads it).  Not part of the product build."""
+def build_variant(name, defines, verbose=False, flags=()):
+    """A/B build of the same sources with extra -D defines (and nvcc flags) into exp/<name>/libtamp.so (in-tree,
+    git-ignored; bench --lib loads it).  Not part of the product build."""
     out = os.path.join(ROOT, "exp", name)
-    return _build(verbose, defines=defines, obj_dir=os.path.join(out, "obj"), lib=os.path.join(out, "libtamp.so"))
+    return _build(verbose, defines=defines, obj_dir=os.path.join(out, "obj"), lib=os.path.join(out, "libtamp.so"),
+                  flags=flags)
 
 
-def _build(verbose=False, defines=(), obj_dir=OBJ_DIR, lib=LIB):
+def _build(verbose=False, defines=(), obj_dir=OBJ_DIR, lib=LIB, flags=()):
     os.makedirs(obj_dir, exist_ok=True)
     objs = [os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o") for s in SRCS]
     procs = [subprocess.Popen([nvcc()] + NVCC_FLAGS + (FAST_DIV_SQRT if os.path.basename(s) in FAST_UNITS else [])
-                              + [f"-D{d}" for d in defines] + ["-c", "-o", o, s], stdout=subprocess.PIPE,
+                              + [f"-D{d}" for d in defines] + list(flags) + ["-c", "-o", o, s], stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True) for s, o in zip(SRCS, objs)]
     logs, failed = [], []
     for s, p in zip(SRCS, procs):
