@@ -373,9 +373,10 @@ def _bounded_exclusions(kinks):
     assert (~kinks).sum() >= 20
 
 
-@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20)])
+@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20), (5, 1 << 18), (5, 1 << 20)])
 def test_full_size_sampled_against_oracle(cfg, n):
-    """BASELINE sizes (config 4: its per-GPU share of 128K over 8 GPUs; config 1: the 1M throughput run) in
+    """BASELINE sizes (config 4: its per-GPU share of 128K over 8 GPUs; config 1: the 1M throughput run; config 5:
+    the sweep's 2^18 and 2^20 points, the 1024-thread variant in multi-wave launches) in
     the auto launch configuration bench uses: sample + eval + 1 fused step on all particles; 48 sampled
     particles recomputed by the oracle one by one from the same start (particles never couple); at most
     10 % of them excluded as kinks."""
@@ -407,7 +408,7 @@ def test_full_size_sampled_against_oracle(cfg, n):
     assert np.all(close | unstable | kinks[:, None])
 
 
-@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20)])
+@pytest.mark.parametrize("cfg,n", [(2, 8192), (3, 32768), (4, 16384), (1, 1 << 20), (5, 1 << 18)])
 def test_full_size_mid_optimisation_against_oracle(cfg, n):
     """The bench's own state: IK-initialised particles (ik_iters = 20, as bench.py) after 3 launches of 10 fused
     steps (contact-rich: the IK puts grippers at their targets), in the auto launch configuration.  On 48
