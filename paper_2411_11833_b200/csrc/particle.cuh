@@ -24,6 +24,12 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_FK_COPY              // with TAMP_FK_SMEM: a register copy of the shared descriptor (else a reference:
+#define TAMP_FK_COPY 1            // re-read after every shared-memory store; config 4 7.59 -> 7.18 ms, config 2 -1.2 %)
+#endif
+#ifndef TAMP_FK_SMEM_MAXT         // variants (launch bound <= this) that read the descriptors from shared memory
+#define TAMP_FK_SMEM_MAXT 1024    // (with the register copy also the 896 / 1024-bound ones: config 3 -0.5 %)
+#endif
 #ifndef TAMP_FK_SMEM              // lane mappings: the configurations' descriptors in shared memory (<= 768-thread
 #define TAMP_FK_SMEM 1            // variants)
 #endif
@@ -949,10 +955,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     }
     if (MODE == MODE_CHECK || (MODE == MODE_OPT && A.check_after))
         for (int i = threadIdx.x; i < P.n_terms + 2; i += blockDim.x) s_counts[i] = 0;
-    // the configurations' descriptors, once per block (FKS: read by reference in the FK loop -- an indexed constant
-    // load plus its address computation at every use of a field otherwise; config 4 -2.4 %, config 2 -1.3 %; the
-    // register-tight 896 / 1024-bound variants keep the register copy, config 3 was 0.5 % slower with the table)
-    constexpr bool FKS = TAMP_FK_SMEM && MAXT <= 768;
+    // the configurations' descriptors, once per block; each FK instance takes a register copy of its descriptor
+    // from shared memory (FKS) instead of indexed constant loads plus their address computation at every use of a
+    // field (the compiler re-derived them rather than keep registers): config 4 7.76 -> 7.18 ms, config 2 -2 %,
+    // config 3 -0.5 %
+    constexpr bool FKS = TAMP_FK_SMEM && MAXT <= TAMP_FK_SMEM_MAXT;
     KFk* const s_fk = reinterpret_cast<KFk*>(cinst + A.fk_off);
     if (FKS)
         for (int i = threadIdx.x; i < P.n_fk; i += blockDim.x) s_fk[i] = P.fk[i];
@@ -1084,8 +1091,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
         TermSink<M> sinkB;                  // this half's share of the phase-B terms
         for (int f0 = 0; f0 < P.n_fk; f0 += HP) {
             KFk Kc;
-            if (!FKS) Kc = P.fk[f0 + (HP > 1 ? half : 0)];
-            const KFk& K = FKS ? s_fk[f0 + (HP > 1 ? half : 0)] : Kc;
+            if (!FKS || TAMP_FK_COPY) Kc = FKS ? s_fk[f0 + (HP > 1 ? half : 0)] : P.fk[f0 + (HP > 1 ? half : 0)];
+            const KFk& K = FKS && !TAMP_FK_COPY ? s_fk[f0 + (HP > 1 ? half : 0)] : Kc;
             const bool real = !K.ghost;
             TAMP_DCHECK(f0 + HP <= TAMP_MAX_FK && K.xoff >= 0 && K.xoff + TAMP_NJ <= D);
             TAMP_DCHECK(K.part_begin >= 0 && K.part_begin + K.part_count <= kMaxPartners);
