@@ -24,6 +24,9 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_PLACE_PIN            // lane mappings: the Place descriptor's fields pinned in registers
+#define TAMP_PLACE_PIN 1
+#endif
 #ifndef TAMP_FK_COPY              // with TAMP_FK_SMEM: a register copy of the shared descriptor (else a reference:
 #define TAMP_FK_COPY 1            // re-read after every shared-memory store; config 4 7.59 -> 7.18 ms, config 2 -1.2 %)
 #endif
@@ -1432,7 +1435,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
 
         // ---- phase C: StablePlace (support, containment) and CFreePlace per Place ----
         for (int pl = 0; pl < P.n_place; ++pl) {
-            const KPlace& Q = P.place[pl];
+            // (TAMP_PLACE_PIN: the Place descriptor's fields pinned in registers by opaque copies -- else re-derived
+            // from the constant bank at every use)
+            KPlace Qc = P.place[pl];
+            if (TAMP_PLACE_PIN) {
+                Qc.inst = (int16_t)opaque_int(Qc.inst); Qc.term_ss = (int16_t)opaque_int(Qc.term_ss);
+                Qc.term_sc = (int16_t)opaque_int(Qc.term_sc); Qc.term_cp = (int16_t)opaque_int(Qc.term_cp);
+                Qc.term_pc = (int16_t)opaque_int(Qc.term_pc); Qc.surface = (int16_t)opaque_int(Qc.surface);
+                Qc.part_begin = (int16_t)opaque_int(Qc.part_begin); Qc.part_count = (int16_t)opaque_int(Qc.part_count);
+                Qc.obb_mask = (uint16_t)opaque_int(Qc.obb_mask);
+            }
+            const KPlace& Q = TAMP_PLACE_PIN ? Qc : P.place[pl];
             const int ii = Q.inst;
             const KInst& I = P.inst[ii];
             const KSurface& Sf = P.surf[Q.surface];
