@@ -24,6 +24,9 @@
 #ifndef TAMP_PACK_NARROW
 #define TAMP_PACK_NARROW 1
 #endif
+#ifndef TAMP_PARTNER_TABLE         // lane mappings: partner references as shared-memory offset words in the
+#define TAMP_PARTNER_TABLE 1       // register-rich (512-bound) variants: config 2 -2.7 %; the 768 / 896-bound ones
+#endif                             // were slower with it (config 4 +1.5 %, config 3 +0.6 %)
 #ifndef TAMP_PLACE_PIN            // lane mappings: the Place descriptor's fields pinned in registers
 #define TAMP_PLACE_PIN 1
 #endif
@@ -964,6 +967,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     // config 3 -0.5 %
     constexpr bool FKS = TAMP_FK_SMEM && MAXT <= TAMP_FK_SMEM_MAXT;
     KFk* const s_fk = reinterpret_cast<KFk*>(cinst + A.fk_off);
+    // partner reference k as an offset word (>= 0: movable instance, from the particle's area; < 0: constant, ~offset
+    // from the block's constant area): one shared load per partner instead of the instance lookup
+    constexpr bool PTAB = TAMP_PARTNER_TABLE && MAXT <= 512;
+    int* const s_pw = reinterpret_cast<int*>(cinst + A.pw_off);
+    if (PTAB)
+        for (int k = threadIdx.x; k < A.n_pw; k += blockDim.x) {
+            const KInst& I = P.inst[P.partners[k]];
+            s_pw[k] = I.xoff >= 0 ? A.off_inst + kInstFloats * I.slot : ~(kInstFloats * I.slot);
+        }
     if (FKS)
         for (int i = threadIdx.x; i < P.n_fk; i += blockDim.x) s_fk[i] = P.fk[i];
     if (TAMP_OBB_SMEM && threadIdx.x < P.n_obb) {
@@ -1181,9 +1193,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NS, TAMP_ROLLED_HITS && (HP > 1)>(rs, P.obb[b], lam_cf, gw, smooth, TAMP_OBB_SMEM ? s_obb[b] : nullptr);
                 // robot spheres vs movable objects' spheres (shared memory)
                 for (int pi = 0; pi < K.part_count; ++pi) {
-                    const int ii = P.partners[K.part_begin + pi];
-                    float* ip = inst(ii);
-                    const bool mov = P.inst[ii].xoff >= 0;
+                    float* ip;
+                    bool mov;
+                    if (PTAB) {
+                        const int w = s_pw[K.part_begin + pi];
+                        ip = w >= 0 ? S + w : cinst + ~w;
+                        mov = w >= 0;
+                    } else {
+                        const int ii = P.partners[K.part_begin + pi];
+                        ip = inst(ii);
+                        mov = P.inst[ii].xoff >= 0;
+                    }
                     jcf += pairs_vs_instance<G, NS>(rs, ip + 16, *reinterpret_cast<const float4*>(ip + 12), lam_cf, gw,
                         [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, mov, ip + 48, ll, half, real); }, smooth);
                 }
@@ -1281,9 +1301,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 for (int b = 0; b < P.n_obb; ++b)
                     if ((K.obb_mask >> b) & 1) jcf += spheres_vs_obb<G, NH, TAMP_ROLLED_HITS && (HP > 1)>(hq, P.obb[b], lam_cf, gh, smooth, TAMP_OBB_SMEM ? s_obb[b] : nullptr);
                 for (int pi = 0; pi < K.part_count; ++pi) {
-                    const int ii = P.partners[K.part_begin + pi];
-                    float* ip = inst(ii);
-                    const bool mov = P.inst[ii].xoff >= 0;
+                    float* ip;
+                    bool mov;
+                    if (PTAB) {
+                        const int w = s_pw[K.part_begin + pi];
+                        ip = w >= 0 ? S + w : cinst + ~w;
+                        mov = w >= 0;
+                    } else {
+                        const int ii = P.partners[K.part_begin + pi];
+                        ip = inst(ii);
+                        mov = P.inst[ii].xoff >= 0;
+                    }
                     jcf += pairs_vs_instance<G, NH>(hq, ip + 16, *reinterpret_cast<const float4*>(ip + 12), lam_cf, gh,
                         [&](Wrench& pw) { flush_partner_b<G, HP, LPF>(pw, mov, ip + 48, ll, half, real); }, smooth);
                 }
@@ -1550,9 +1578,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 for (int b = 0; b < P.n_obb; ++b)
                     if ((Q.obb_mask >> b) & 1) jcp += spheres_vs_obb<G, NSO, TAMP_ROLLED_HITS && (HP > 1)>(qe, P.obb[b], lam_cp, gq, smooth, TAMP_OBB_SMEM ? s_obb[b] : nullptr);
                 for (int pi = 0; pi < Q.part_count; ++pi) {
-                    const int jj = P.partners[Q.part_begin + pi];
-                    float* jp = inst(jj);
-                    const bool mov = P.inst[jj].xoff >= 0;
+                    float* jp;
+                    bool mov;
+                    if (PTAB) {
+                        const int w = s_pw[Q.part_begin + pi];
+                        jp = w >= 0 ? S + w : cinst + ~w;
+                        mov = w >= 0;
+                    } else {
+                        const int jj = P.partners[Q.part_begin + pi];
+                        jp = inst(jj);
+                        mov = P.inst[jj].xoff >= 0;
+                    }
                     jcp += pairs_vs_instance<G, NSO>(qe, jp + 16, *reinterpret_cast<const float4*>(jp + 12), lam_cp, gq,
                         [&](Wrench& pw) { flush_partner<G, GS>(pw, mov, jp + 48, gl); }, smooth);
                 }

@@ -79,7 +79,7 @@ struct tamp_ctx {
     size_t o_x, o_m, o_v, o_grasp, o_inv, o_cls, o_cost, o_ka, o_kb, o_pa, o_pb, o_coords, o_counts, o_stage, o_iklist, o_ikn, o_ikbest, total;
     int64_t n_keys = 0;
     // shared-memory layout of the particle kernel (floats per particle)
-    int stride, off_g, off_inst, off_gT, off_gTi, off_rsw, const_floats, fk_off;
+    int stride, off_g, off_inst, off_gT, off_gTi, off_rsw, const_floats, fk_off, pw_off, n_pw;
     size_t smem = 0;
     int gs = 8;                  // lanes per particle in the particle kernel
     int ik_iters = 0;            // conditional IK sampler iterations
@@ -744,6 +744,12 @@ static void smem_layout(tamp_ctx* c) {
     c->const_floats = kInstFloats * n_const;          // constant instances: once per block
     c->fk_off = c->const_floats;                      // then the configurations' descriptors, once per block
     c->const_floats += ((P.n_fk * (int)sizeof(KFk) / 4) + 3) & ~3;
+    int n_pw = 0;                                     // then the partner references' shared-memory offset words
+    for (int f = 0; f < P.n_fk; ++f) n_pw = std::max(n_pw, P.fk[f].part_begin + P.fk[f].part_count);
+    for (int q = 0; q < P.n_place; ++q) n_pw = std::max(n_pw, P.place[q].part_begin + P.place[q].part_count);
+    c->pw_off = c->const_floats;
+    c->n_pw = n_pw;
+    c->const_floats += (n_pw + 3) & ~3;              // (read by the 512-bound variants: TAMP_PARTNER_TABLE)
     static_assert(sizeof(KFk) % 4 == 0, "KFk must be a whole number of floats");
     c->off_rsw = off;                                 // robot sphere centres for the SELF term (2 FK halves)
     off += P.has_self ? (c->gs == 16 ? 2 : 1) * 4 * (kGroup * TAMP_MAX_SPHERES_PER_LINK) : 0;   // per FK half
@@ -829,6 +835,8 @@ static KArgs base_args(tamp_ctx* c) {
     A.off_inst = c->off_inst;
     A.const_floats = c->const_floats;
     A.fk_off = c->fk_off;
+    A.pw_off = c->pw_off;
+    A.n_pw = c->n_pw;
     A.off_gT = c->off_gT;
     A.off_gTi = c->off_gTi;
     A.off_rsw = c->off_rsw;

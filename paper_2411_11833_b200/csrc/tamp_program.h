@@ -153,6 +153,7 @@ struct KArgs {
                                                                // no held object at a knot, no inverse grasps
     int32_t const_floats;  // block-shared constant instances at the start of dynamic shared memory, then the
     int32_t fk_off;        // configurations' descriptors (KFk[n_fk], lane mappings) at float offset fk_off
+    int32_t pw_off, n_pw;  // and the partner references' offset words (int[n_pw], TAMP_PARTNER_TABLE)
     int32_t n_steps, t0;
     int32_t bsync;         // serial mapping: block barriers per configuration / phase (shared i-cache)
     int32_t check_after;   // MODE_OPT: run the Eq. 3 check of the final state in the same launch
