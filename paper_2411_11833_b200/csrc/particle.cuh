@@ -945,6 +945,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
     };
     TAMP_DCHECK(A.const_floats + (grp + 1) * A.stride <= A.smem_floats);
     TAMP_DCHECK(A.fk_off + P.n_fk * (int)(sizeof(KFk) / 4) <= A.const_floats);
+    TAMP_DCHECK(A.pw_off + A.n_pw <= A.const_floats);
     TAMP_DCHECK(A.off_g + P.D <= A.stride && A.off_gT + 12 * P.n_grasp <= A.stride);
     TAMP_DCHECK(A.off_gTi < 0 || A.off_gTi + 12 * P.n_grasp <= A.stride);
     TAMP_DCHECK(!P.has_self || A.off_rsw + 4 * HP * kGroup * TAMP_MAX_SPHERES_PER_LINK <= A.stride);
@@ -1196,6 +1197,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     float* ip;
                     bool mov;
                     if (PTAB) {
+                        TAMP_DCHECK(K.part_begin + pi < A.n_pw);
                         const int w = s_pw[K.part_begin + pi];
                         ip = w >= 0 ? S + w : cinst + ~w;
                         mov = w >= 0;
@@ -1304,6 +1306,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     float* ip;
                     bool mov;
                     if (PTAB) {
+                        TAMP_DCHECK(K.part_begin + pi < A.n_pw);
                         const int w = s_pw[K.part_begin + pi];
                         ip = w >= 0 ? S + w : cinst + ~w;
                         mov = w >= 0;
@@ -1581,6 +1584,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                     float* jp;
                     bool mov;
                     if (PTAB) {
+                        TAMP_DCHECK(Q.part_begin + pi < A.n_pw);
                         const int w = s_pw[Q.part_begin + pi];
                         jp = w >= 0 ? S + w : cinst + ~w;
                         mov = w >= 0;
