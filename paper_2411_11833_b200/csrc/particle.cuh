@@ -36,8 +36,8 @@
 #ifndef TAMP_FK_SMEM_MAXT         // variants (launch bound <= this) that read the descriptors from shared memory
 #define TAMP_FK_SMEM_MAXT 1024    // (with the register copy also the 896 / 1024-bound ones: config 3 -0.5 %)
 #endif
-#ifndef TAMP_FK_SMEM              // lane mappings: the configurations' descriptors in shared memory (<= 768-thread
-#define TAMP_FK_SMEM 1            // variants)
+#ifndef TAMP_FK_SMEM              // lane mappings: the configurations' descriptors in the block's shared constant
+#define TAMP_FK_SMEM 1            // area (variants with a launch bound <= TAMP_FK_SMEM_MAXT)
 #endif
 #ifndef TAMP_OBB_SMEM             // lane mappings: boxes' fast-path data staged in shared memory once per block
 #define TAMP_OBB_SMEM 1           // (config 3 -0.3 %, config 4 -1.4 % per launch)
@@ -168,8 +168,6 @@ __device__ __forceinline__ float gsum(float v) {      // butterfly sum over the 
 // opaque register copies: the compiler cannot re-derive the value (e.g. re-load it from the constant bank)
 __device__ __forceinline__ int opaque_int(int v) { asm volatile("" : "+r"(v)); return v; }
 __device__ __forceinline__ float opaque_f(float v) { asm volatile("" : "+f"(v)); return v; }
-template <class T>
-__device__ __forceinline__ T* opaque_ptr(T* v) { asm volatile("" : "+l"(v)); return v; }
 
 // 4-byte asynchronous copy global -> shared (cp.async.ca; completed by cp_async_wait_all)
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
