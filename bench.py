@@ -67,6 +67,9 @@ def parse():
     p.add_argument("--repeats", type=int, default=5, help="timed regions of exactly --steps steps; value = median")
     p.add_argument("--no-extra", action="store_true", help="skip the extra workloads (config 2, config 1 at 1M, SELF)")
     p.add_argument("--no-overlap", action="store_true", help="all-reduce of the counts on the launching stream")
+    p.add_argument("--dist", action="store_true",
+                   help="initialise torch.distributed (NCCL) even with one rank: runs the collective path (overlapped "
+                        "C1 all-reduce, C2 all-gather, K5 merge) on one GPU")
     p.add_argument("--nvtx", action="store_true", help="NVTX ranges around the phases of a step (profiling)")
     p.add_argument("--lib", default=None, help="A/B experiments: another in-tree build of libtamp.so (exp/<name>/)")
     p.add_argument("--pipeline", type=int, default=-1,
@@ -233,8 +236,12 @@ def dist_init(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world} (launch one process per GPU)")
-    if world > 1:
+    if world > 1 or getattr(args, "dist", False):
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         if args.impl == "ours":
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
