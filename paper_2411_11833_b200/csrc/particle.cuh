@@ -1649,12 +1649,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_particle(const __grid_constant__ KP
                 if (j == nseg) return Tj.q2_xoff;
                 return Tj.knot_xoff + 7 * (j - 1);
             };
+            // (each knot's coordinates read once: the segment's end becomes the next segment's start)
+            float prev[NJL];
+#pragma unroll
+            for (int u = 0; u < NJL; ++u) prev[u] = val(0, gl + GS * u);
             for (int j = 0; j < nseg; ++j) {
                 float dlt[NJL], s2 = 0.f;
 #pragma unroll
                 for (int u = 0; u < NJL; ++u) {
                     const int jt = gl + GS * u;
-                    dlt[u] = val(j + 1, jt) - val(j, jt);
+                    const float cur = val(j + 1, jt);
+                    dlt[u] = cur - prev[u];
+                    prev[u] = cur;
                     s2 = fmaf(dlt[u], dlt[u], s2);
                 }
                 const float len = sqrtf(gsum<GS>(s2));
