@@ -185,6 +185,24 @@ def test_bench_json_line_contract():
     assert len(d["repeats"]["values"]) == 2
 
 
+def test_bench_collective_path_one_rank():
+    """bench.py --dist: torch.distributed with the NCCL backend for one rank -- the overlapped C1 all-reduce on the
+    side stream, the C2 all-gather and the K5 merge run on the GPU and the line reports the overlapped all-reduce."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_PORT="29611")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dist", "--config", "2", "--n", "1024",
+                        "--steps", "2", "--warmup", "3", "--repeats", "1", "--no-extra", "--no-cpu-baseline", "--no-ttfs"],
+                       capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    assert "overlapped" in d["config"]["allreduce"]
+
+
 @pytest.mark.parametrize("lanes,single_box", [(8, False), (8, True), (1, True)])
 def test_box_reject_at_reach_boundary(lanes, single_box):
     """The kernels skip a sphere's exact box test when a cheaper reject test says it cannot reach the box (for
